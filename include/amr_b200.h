@@ -1,0 +1,185 @@
+/*
+ * amr_b200.h — C ABI of the B200-native LTS/GTS octree wave solver.
+ *
+ * The reference (`amrlts`, pure Python) has no FFI: its boundary is the Python
+ * module API.  These entry points are what that API's hot calls bind to
+ * (ctypes); each cites the reference function it replaces.
+ * Plain pointers and sizes only.  Device pointers are owned by the caller
+ * (torch tensors in our Python facade); nothing here allocates or frees
+ * caller memory.  Every function returns 0 on success, otherwise an AMR_E*
+ * code; amr_last_error() returns a message for the calling thread.
+ *
+ * Index conventions: a leaf is identified by its position in the tree's SFC
+ * order; anchors are in finest-cell units (octree.py:5-8); lattice points are
+ * in units of a finest cell / (ppo-1) (mesh.py:8-11); gids are the zip-node
+ * ids of the reference (first-claim order, mesh.py:235-245).
+ */
+#ifndef AMR_B200_H
+#define AMR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  AMR_OK = 0,
+  AMR_EINVAL = 1,     /* bad argument (maps to ValueError) */
+  AMR_ESTATE = 2,     /* inconsistent state (maps to RuntimeError) */
+  AMR_ECUDA = 3,      /* CUDA launch/runtime failure */
+  AMR_ENOMEM = 4
+};
+
+const char* amr_last_error(void);
+int amr_abi_version(void);
+
+/* ---------------------------------------------------------------- octree -- */
+
+/* Morton order (x lowest bit, ancestors first) of n octants:
+ * perm[k] = index of the k-th octant.  Replaces the sort in construct /
+ * balance_2to1 / parse_dump with SfcOrdering("morton") (octree.py:175-198,270,329). */
+int amr_morton_sort(int dim, int max_depth, int64_t n, const int32_t* anchors,
+                    const int32_t* levels, int64_t* perm);
+
+/* Unique minimal 2:1 (face+edge+corner) balanced refinement
+ * (octree.py:289-330).  Two-call: first with anchors_out == NULL returns the
+ * leaf count in *n_out; the second fills Morton-sorted outputs. */
+typedef struct AmrTree AmrTree;
+AmrTree* amr_balance(int dim, int max_depth, int64_t n, const int32_t* anchors,
+                     const int32_t* levels, int64_t* n_out);
+int amr_tree_fetch(const AmrTree* t, int32_t* anchors_out, int32_t* levels_out);
+void amr_tree_free(AmrTree* t);
+
+/* ------------------------------------------------------------------ mesh -- */
+
+/* Node registry + leaf-tile gather tables (mesh.py:214-398).  `owners` (may be
+ * NULL) are the partition ranks used only to split the public maximal blocks
+ * (decompose_blocks, mesh.py:87-135).  Leaves must be in the tree's SFC
+ * order (any SFC), complete and 2:1 balanced. */
+typedef struct AmrMesh AmrMesh;
+AmrMesh* amr_mesh_build(int dim, int max_depth, int ppo, int pad, int64_t n_leaves,
+                        const int32_t* anchors, const int32_t* levels, const int32_t* owners,
+                        int n_threads);
+void amr_mesh_free(AmrMesh* m);
+
+int64_t amr_mesh_n_nodes(const AmrMesh* m);
+/* leaf_slices (mesh.py:250-254): starts[n_leaves+1]; leaf i owns [starts[i], starts[i+1]) */
+int amr_mesh_leaf_starts(const AmrMesh* m, int64_t* starts);
+/* leaf_gids (mesh.py:249): [n_leaves][ppo^dim], -1 = hanging */
+int amr_mesh_leaf_gids(const AmrMesh* m, int32_t* gids);
+/* node_coords (mesh.py:257-265): [n_nodes][dim] lattice coordinates */
+int amr_mesh_node_coords(const AmrMesh* m, int32_t* coords);
+
+/* Leaf-tile unzip tables: per leaf, amr_tile_entries(dim,ppo) int32 entries
+ * over the stencil cross (ppo^dim interior + 2*dim*pad*ppo^(dim-1) face halo).
+ * entry >= 0: copy of zip node `entry`; -1: outside the domain (zero row);
+ * <= -2: interpolation row (-entry-2) of the CSR below. */
+int64_t amr_tile_entries(int dim, int ppo);
+int amr_mesh_tile_table(const AmrMesh* m, int32_t* table);
+int64_t amr_mesh_interp_rows(const AmrMesh* m);
+int64_t amr_mesh_interp_nnz(const AmrMesh* m);
+/* rows sorted by gid (mesh.py:391-393); weights from the recursive
+ * tensor-product Lagrange resolution (mesh.py:316-351) */
+int amr_mesh_interp_csr(const AmrMesh* m, int64_t* row_ptr, int32_t* gid, double* w);
+
+/* Public maximal blocks (decompose_blocks, mesh.py:87-135) */
+int64_t amr_mesh_n_blocks(const AmrMesh* m);
+int amr_mesh_blocks(const AmrMesh* m, int32_t* root_anchor, int32_t* root_level,
+                    int32_t* leaf_level, int64_t* leaf_range, int32_t* owner);
+/* Gather CSR of one block's padded grid (mesh.py:355-398).  Two-call: with
+ * row_ptr == NULL returns rows and nnz; then fills (row_ptr[rows+1]). */
+int amr_mesh_block_gather(AmrMesh* m, int64_t block, int64_t* rows, int64_t* nnz,
+                          int64_t* row_ptr, int64_t* col, double* val);
+
+/* --------------------------------------------------------------- kernels -- */
+
+/* Per-slice LTS coefficient block (device memory, built by the host from
+ * rkcorrect.stage_transfer_matrix, stepper.py:238-314).  Levels are absolute
+ * octree levels < AMR_MAXL. */
+#define AMR_MAXL 16
+#define AMR_MAXP 4
+typedef struct {
+  int32_t cur[AMR_MAXL];                 /* u_curr buffer (0/1) per cadence level */
+  int32_t mode[AMR_MAXL][AMR_MAXL];      /* [reader][source]: 0 verbatim, 1 delta=0 transfer, 2 virtual substep */
+  double cstage[AMR_MAXL][AMR_MAXP][AMR_MAXP]; /* dt_to * a[s][j] per reader level */
+  double comb[AMR_MAXL][AMR_MAXP];       /* dt * w[s] per stepping level */
+  double M[AMR_MAXL][AMR_MAXL][AMR_MAXP][AMR_MAXP];  /* stage transfer (tril when delta=0) */
+  double Mv[AMR_MAXL][AMR_MAXL][AMR_MAXP][AMR_MAXP]; /* virtual-substep transfer */
+  double dtw[AMR_MAXL][AMR_MAXL][AMR_MAXP];          /* delta*dt_fine*w[i] */
+} AmrSliceCoef;
+
+typedef struct {
+  int dim, ppo, pad;
+  int lts;             /* 0: global stepping (all verbatim), 1: local stepping */
+  int stage, n_stages; /* s, p */
+  int nonlinear;       /* 0 none, 1 sin(2chi)/r^2 (wave.py:162-163), 2 cubic chi^3 */
+  int gts_cur;         /* GTS: u_curr buffer index */
+  int64_t n_tiles;
+  int64_t n_nodes;
+  const int32_t* tile_ids;     /* leaf per CTA */
+  const int32_t* tile_table;   /* [n_leaves][entries] */
+  const int64_t* interp_ptr;
+  const int32_t* interp_gid;
+  const double* interp_w;
+  const int32_t* leaf_anchor;  /* [n_leaves][3] */
+  const int32_t* leaf_level;   /* [n_leaves] octree level (spacing, faces) */
+  const int32_t* leaf_cadence; /* [n_leaves] time level (== level for LTS; promoted for single-stage) */
+  const int64_t* leaf_start;   /* [n_leaves+1] */
+  const uint8_t* node_cadence; /* [n_nodes] cadence of the owning leaf (LTS) */
+  double* U0;                  /* [n_nodes][2] interleaved (chi, phi) */
+  double* U1;
+  double* K;                   /* [n_stages][n_nodes][2] */
+  const AmrSliceCoef* coef;    /* LTS only (device) */
+  /* GTS coefficients */
+  double g_cstage[AMR_MAXP][AMR_MAXP];
+  double g_comb[AMR_MAXP];
+  /* geometry (mesh.py:459-492, wave.py:124-144) */
+  int max_depth;
+  int64_t top_nodes;
+  double lo[3], extent[3];
+  double h[AMR_MAXL], h2[AMR_MAXL];
+  int32_t h2_pow2[AMR_MAXL];   /* 1: h**2 is a power of two -> multiply by inv_h2 (bit-identical) */
+  double inv_h2[AMR_MAXL];
+  double r_eps, r_eps2;
+  double k_chi, k_phi, f0_chi, f0_phi;
+  /* stencil weights: the reference's Fornberg arrays, bit for bit (wave.py:49-54) */
+  double d2c[5], d2e0[6], d2e1[6], d1c[5], d1e0[5], d1e1[5];
+} AmrStageParams;
+
+/* One RK stage over a prefix of the tile list: fused unzip (spatial + LTS time
+ * interpolation) + RHS stencil + zip of K_s; the last stage also fuses the RK
+ * combine and record rotation.  Replaces Engine._stage_source +
+ * gathers[b].dot + wave_rhs + the K/state scatter (stepper.py:274-314,
+ * 395-453). */
+int amr_stage(const AmrStageParams* p, void* stream);
+
+/* Mesh.unzip (mesh.py:413-420): out[v][r] = 0 + sum_k w_k * z[v][col_k] over
+ * CSR rows (ascending col), z/out in (nv, n) layout. */
+int amr_gather_rows(int64_t n_rows, const int64_t* row_ptr, const int64_t* col,
+                    const double* val, int nv, const double* z, int64_t z_stride,
+                    double* out, int64_t out_stride, void* stream);
+
+/* wave_rhs on one padded block array (wave.py:147-201).  y: [2][n+2pad]^dim,
+ * out: [2][n]^dim; faces bitmask bit(2*axis+side); coords: per-axis interior
+ * physical coordinates (n each). */
+int amr_block_rhs(int dim, int n, int pad, const double* y, double* out, double h, double h2,
+                  const double* coords, double r_eps, int faces, int nonlinear,
+                  double k_chi, double k_phi, double f0_chi, double f0_phi,
+                  const AmrStageParams* weights, void* stream);
+
+/* Ghost exchange pack/unpack of contiguous zip ranges (the byte-level
+ * exchange of partition.py:182-207 / stepper.py:318-361): buf holds the
+ * ranges back to back, each node `width` doubles. */
+int amr_pack_ranges(int64_t n_ranges, const int64_t* range_start, const int64_t* range_len,
+                    const int64_t* range_off, int width, const double* src, double* buf,
+                    int64_t total, void* stream);
+int amr_unpack_ranges(int64_t n_ranges, const int64_t* range_start, const int64_t* range_len,
+                      const int64_t* range_off, int width, const double* buf, double* dst,
+                      int64_t total, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

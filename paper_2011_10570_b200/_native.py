@@ -1,0 +1,138 @@
+"""ctypes binding of the C ABI in include/amr_b200.h.
+
+The library is built in-tree (paper_2011_10570_b200/_lib/libamr_b200.so) and
+is mandatory: there is no Python or CPU fallback for anything it provides.
+If it cannot be loaded (or built, when nvcc is present) every caller raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import build as _build
+
+AMR_MAXL = 16
+AMR_MAXP = 4
+
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_f64p = C.POINTER(C.c_double)
+_vp = C.c_void_p
+
+
+class AmrSliceCoef(C.Structure):
+    _fields_ = [
+        ("cur", C.c_int32 * AMR_MAXL),
+        ("mode", (C.c_int32 * AMR_MAXL) * AMR_MAXL),
+        ("cstage", ((C.c_double * AMR_MAXP) * AMR_MAXP) * AMR_MAXL),
+        ("comb", (C.c_double * AMR_MAXP) * AMR_MAXL),
+        ("M", (((C.c_double * AMR_MAXP) * AMR_MAXP) * AMR_MAXL) * AMR_MAXL),
+        ("Mv", (((C.c_double * AMR_MAXP) * AMR_MAXP) * AMR_MAXL) * AMR_MAXL),
+        ("dtw", ((C.c_double * AMR_MAXP) * AMR_MAXL) * AMR_MAXL),
+    ]
+
+
+class AmrStageParams(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int), ("ppo", C.c_int), ("pad", C.c_int),
+        ("lts", C.c_int), ("stage", C.c_int), ("n_stages", C.c_int),
+        ("nonlinear", C.c_int), ("gts_cur", C.c_int),
+        ("n_tiles", C.c_int64), ("n_nodes", C.c_int64),
+        ("tile_ids", _vp), ("tile_table", _vp),
+        ("interp_ptr", _vp), ("interp_gid", _vp), ("interp_w", _vp),
+        ("leaf_anchor", _vp), ("leaf_level", _vp), ("leaf_cadence", _vp), ("leaf_start", _vp),
+        ("node_cadence", _vp),
+        ("U0", _vp), ("U1", _vp), ("K", _vp),
+        ("coef", _vp),
+        ("g_cstage", (C.c_double * AMR_MAXP) * AMR_MAXP),
+        ("g_comb", C.c_double * AMR_MAXP),
+        ("max_depth", C.c_int),
+        ("top_nodes", C.c_int64),
+        ("lo", C.c_double * 3), ("extent", C.c_double * 3),
+        ("h", C.c_double * AMR_MAXL), ("h2", C.c_double * AMR_MAXL),
+        ("h2_pow2", C.c_int32 * AMR_MAXL),
+        ("inv_h2", C.c_double * AMR_MAXL),
+        ("r_eps", C.c_double), ("r_eps2", C.c_double),
+        ("k_chi", C.c_double), ("k_phi", C.c_double), ("f0_chi", C.c_double), ("f0_phi", C.c_double),
+        ("d2c", C.c_double * 5), ("d2e0", C.c_double * 6), ("d2e1", C.c_double * 6),
+        ("d1c", C.c_double * 5), ("d1e0", C.c_double * 5), ("d1e1", C.c_double * 5),
+    ]
+
+
+# every symbol the header declares (checked by tests/test_native_abi.py)
+SIGNATURES = {
+    "amr_last_error": ([], C.c_char_p),
+    "amr_abi_version": ([], C.c_int),
+    "amr_morton_sort": ([C.c_int, C.c_int, C.c_int64, _i32p, _i32p, _i64p], C.c_int),
+    "amr_balance": ([C.c_int, C.c_int, C.c_int64, _i32p, _i32p, _i64p], _vp),
+    "amr_tree_fetch": ([_vp, _i32p, _i32p], C.c_int),
+    "amr_tree_free": ([_vp], None),
+    "amr_mesh_build": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, _i32p, _i32p, _i32p, C.c_int], _vp),
+    "amr_mesh_free": ([_vp], None),
+    "amr_mesh_n_nodes": ([_vp], C.c_int64),
+    "amr_mesh_leaf_starts": ([_vp, _i64p], C.c_int),
+    "amr_mesh_leaf_gids": ([_vp, _i32p], C.c_int),
+    "amr_mesh_node_coords": ([_vp, _i32p], C.c_int),
+    "amr_tile_entries": ([C.c_int, C.c_int], C.c_int64),
+    "amr_mesh_tile_table": ([_vp, _i32p], C.c_int),
+    "amr_mesh_interp_rows": ([_vp], C.c_int64),
+    "amr_mesh_interp_nnz": ([_vp], C.c_int64),
+    "amr_mesh_interp_csr": ([_vp, _i64p, _i32p, _f64p], C.c_int),
+    "amr_mesh_n_blocks": ([_vp], C.c_int64),
+    "amr_mesh_blocks": ([_vp, _i32p, _i32p, _i32p, _i64p, _i32p], C.c_int),
+    "amr_mesh_block_gather": ([_vp, C.c_int64, _i64p, _i64p, _i64p, _i64p, _f64p], C.c_int),
+    "amr_stage": ([C.POINTER(AmrStageParams), _vp], C.c_int),
+    "amr_gather_rows": ([C.c_int64, _vp, _vp, _vp, C.c_int, _vp, C.c_int64, _vp, C.c_int64, _vp], C.c_int),
+    "amr_block_rhs": ([C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_double, C.c_double, _vp, C.c_double,
+                       C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
+                       C.POINTER(AmrStageParams), _vp], C.c_int),
+    "amr_pack_ranges": ([C.c_int64, _vp, _vp, _vp, C.c_int, _vp, _vp, C.c_int64, _vp], C.c_int),
+    "amr_unpack_ranges": ([C.c_int64, _vp, _vp, _vp, C.c_int, _vp, _vp, C.c_int64, _vp], C.c_int),
+}
+
+_LIB = None
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+def lib() -> C.CDLL:
+    """Load (building first if stale and nvcc is available) the native library."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = _build.LIB
+    nvcc = os.path.exists(_build.NVCC)
+    if nvcc and os.path.isdir(_build.CSRC):
+        _build.build()
+    if not os.path.exists(path):
+        raise NativeError(
+            f"native library {path} is missing and cannot be built (nvcc: {nvcc}); "
+            "run `python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    L = C.CDLL(path)
+    for name, (args, res) in SIGNATURES.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _LIB = L
+    return L
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = lib().amr_last_error().decode(errors="replace")
+        if rc == 1:
+            raise ValueError(f"{what}: {msg}")
+        raise NativeError(f"{what} failed (code {rc}): {msg}")
+
+
+def ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+def last_error() -> str:
+    return lib().amr_last_error().decode(errors="replace")

@@ -1,0 +1,53 @@
+"""Build the native library in-tree: paper_2011_10570_b200/_lib/libamr_b200.so.
+
+One nvcc invocation compiles the sm_100a kernels (amr_kernels.cu) and the host
+C++ mesh builder (amr_mesh.cpp) into a C-ABI shared library that Python loads
+with ctypes.  Flags that matter for parity:
+  -fmad=false            no FMA contraction in device code (numpy rounds every op)
+  -ffp-contract=off      same for the host C++ (interpolation weights)
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIBDIR = os.path.join(HERE, "_lib")
+LIB = os.path.join(LIBDIR, "libamr_b200.so")
+INCLUDE = os.path.abspath(os.path.join(HERE, "..", "include"))
+SOURCES = ["amr_kernels.cu", "amr_mesh.cpp"]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(INCLUDE, "amr_b200.h")]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    os.makedirs(LIBDIR, exist_ok=True)
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-shared",
+           "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off,-O2",
+           "-I", INCLUDE, "-o", LIB + ".tmp",
+           *[os.path.join(CSRC, s) for s in SOURCES], "-lgomp"]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({' '.join(cmd)}):\n{proc.stdout}\n{proc.stderr}")
+    if verbose:
+        sys.stderr.write(proc.stderr)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

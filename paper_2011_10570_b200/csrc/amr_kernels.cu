@@ -1,0 +1,590 @@
+// amr_kernels.cu — sm_100a kernels of the B200 LTS/GTS wave solver.
+//
+// Hot path: amr_stage.  One CTA owns one leaf tile (ppo^D computed nodes,
+// (ppo-1)^D owned when interior).  Per RK stage it
+//   1. builds the tile's stage input on the stencil cross in shared memory:
+//      for every cross point the unzip entry is a copy of one zip node, a
+//      sorted interpolation row, or zero (outside the domain), and every zip
+//      node read is first turned into the reader's stage source — verbatim
+//      u + sum_j dt a_sj K_j, or, at LTS level interfaces, the stage-transfer
+//      product M K (and the virtual substep for non-eligible coarse sources);
+//      (Engine._stage_source + Mesh.unzip, stepper.py:274-314, mesh.py:413-420)
+//   2. evaluates the 4th-order RHS (biased rows and radiative overwrite at
+//      physical faces; linear, sin or cubic source) only at the nodes the
+//      leaf owns and writes K_s for them contiguously (wave.py:147-201 and the
+//      zip of stepper.py:422-429);
+//   3. on the last stage also does the RK combine u_new = u + sum dt w_s K_s
+//      into the other u buffer (record rotation u_pre <- u_curr without a
+//      copy: the live buffer of a leaf is the parity of its step count).
+//
+// Arithmetic follows the reference bit for bit: -fmad=false for the whole
+// file, numpy's operation order, the reference's Fornberg weight arrays, and
+// fma() only where the reference goes through OpenBLAS dgemm (np.tensordot at
+// stepper.py:264,305 — an ascending-k FMA chain on the generating host).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/amr_b200.h"
+
+extern "C" void amr_set_error_internal(const char* msg);
+
+namespace {
+
+int cuda_fail(cudaError_t e, const char* what) {
+  amr_set_error_internal((std::string(what) + ": " + cudaGetErrorString(e)).c_str());
+  return AMR_ECUDA;
+}
+
+constexpr int cpow(int b, int e) { return e == 0 ? 1 : b * cpow(b, e - 1); }
+
+template <int DIM, int PPO>
+struct Tile {
+  static constexpr int PAD = 2;
+  static constexpr int NP = PPO + 2 * PAD;
+  static constexpr int NI = cpow(PPO, DIM);
+  static constexpr int NF = cpow(PPO, DIM - 1);
+  static constexpr int NE = NI + DIM * 2 * PAD * NF;
+  static constexpr int NS = cpow(NP, DIM);
+  static constexpr int THREADS = DIM == 3 ? 256 : 128;
+};
+
+// smem cell of cross entry e (same enumeration as cross_entry_local in amr_mesh.cpp)
+template <int DIM, int PPO>
+__device__ __forceinline__ int cross_cell(int e) {
+  using T = Tile<DIM, PPO>;
+  int loc[3];
+  if (e < T::NI) {
+    int r = e;
+#pragma unroll
+    for (int d = DIM - 1; d >= 0; --d) {
+      loc[d] = T::PAD + r % PPO;
+      r /= PPO;
+    }
+  } else {
+    int r = e - T::NI;
+    int axis = r / (2 * T::PAD * T::NF);
+    r %= 2 * T::PAD * T::NF;
+    int layer = r / T::NF;
+    int within = r % T::NF;
+    int lp = layer < T::PAD ? layer : PPO + layer;
+#pragma unroll
+    for (int d = DIM - 1; d >= 0; --d) {
+      if (d == axis) continue;
+      loc[d] = T::PAD + within % PPO;
+      within /= PPO;
+    }
+    loc[axis] = lp;
+  }
+  int c = 0;
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) c = c * T::NP + loc[d];
+  return c;
+}
+
+__device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
+
+// --------------------------------------------------------------------------
+// stage source of one zip node as seen by a reader of cadence level lr
+// --------------------------------------------------------------------------
+template <bool LTS>
+__device__ __forceinline__ double2 stage_source(const AmrStageParams& P, const double2* __restrict__ U0,
+                                                const double2* __restrict__ U1,
+                                                const double2* __restrict__ K, int64_t n, int g, int s,
+                                                int lr, const AmrSliceCoef* __restrict__ C) {
+  const int p = P.n_stages;
+  if (!LTS) {
+    const double2* U = P.gts_cur ? U1 : U0;
+    double2 u = ld2(U + g);
+    double2 y = make_double2(0.0 + u.x, 0.0 + u.y);
+    for (int j = 0; j < s; ++j) {
+      double c = P.g_cstage[s][j];
+      if (c != 0.0) {
+        double2 k = ld2(K + j * n + g);
+        y.x = y.x + c * k.x;
+        y.y = y.y + c * k.y;
+      }
+    }
+    return y;
+  }
+  const int ls = P.node_cadence[g];
+  const int mode = C->mode[lr][ls];
+  const int cur = C->cur[ls];
+  const double2* Uc = cur ? U1 : U0;
+  if (mode == 0) {  // eligible, same step size: verbatim (stepper.py:290-296)
+    double2 u = ld2(Uc + g);
+    double2 y = make_double2(0.0 + u.x, 0.0 + u.y);
+    for (int j = 0; j < s; ++j) {
+      double c = C->cstage[lr][s][j];
+      if (c != 0.0) {
+        double2 k = ld2(K + j * n + g);
+        y.x = y.x + c * k.x;
+        y.y = y.y + c * k.y;
+      }
+    }
+    return y;
+  }
+  double2 kk[AMR_MAXP];
+  const int nk = (mode == 1) ? s : p;  // delta=0 transfer is lower triangular
+  for (int k = 0; k < nk; ++k) kk[k] = ld2(K + k * n + g);
+  double2 y;
+  if (mode == 1) {
+    y = ld2(Uc + g);
+  } else {  // virtual substep from u_pre (stepper.py:256-270)
+    const double2* Up = cur ? U0 : U1;
+    y = ld2(Up + g);
+    const double(*Mv)[AMR_MAXP] = C->Mv[lr][ls];
+    for (int i = 0; i < p; ++i) {
+      double c = C->dtw[lr][ls][i];
+      if (c == 0.0) continue;
+      double ax = 0.0, ay = 0.0;
+      for (int k = 0; k <= i; ++k) {
+        ax = fma(Mv[i][k], kk[k].x, ax);
+        ay = fma(Mv[i][k], kk[k].y, ay);
+      }
+      y.x = y.x + c * ax;
+      y.y = y.y + c * ay;
+    }
+  }
+  const double(*M)[AMR_MAXP] = C->M[lr][ls];
+  for (int j = 0; j < s; ++j) {
+    double c = C->cstage[lr][s][j];
+    if (c == 0.0) continue;
+    int kmax = (mode == 1) ? j : p - 1;
+    double ax = 0.0, ay = 0.0;
+    for (int k = 0; k <= kmax; ++k) {
+      ax = fma(M[j][k], kk[k].x, ax);
+      ay = fma(M[j][k], kk[k].y, ay);
+    }
+    y.x = y.x + c * ax;
+    y.y = y.y + c * ay;
+  }
+  return y;
+}
+
+// --------------------------------------------------------------------------
+// RHS at one interior point (wave.py:57-201), generic over the data accessor
+// --------------------------------------------------------------------------
+// Stencil weights are read straight from the by-value kernel parameter block
+// (constant bank, compile-time indices after unrolling).
+using Weights = AmrStageParams;
+
+// derivative along one axis: centred, or the biased row near a physical face
+// (derivative_axis, wave.py:67-109).  get(o) returns the value at offset o.
+template <class Get>
+__device__ __forceinline__ double deriv(const Get& get, int order, int pos, int n, bool lo, bool hi,
+                                        const Weights& W, double hp, bool pow2, double inv_hp) {
+  double t;
+  if (order == 2) {
+    if (lo && pos == 0) {
+      t = W.d2e0[0] * get(0);
+#pragma unroll
+      for (int k = 1; k < 6; ++k) t = t + W.d2e0[k] * get(k);
+    } else if (lo && pos == 1) {
+      t = W.d2e1[0] * get(-1);
+#pragma unroll
+      for (int k = 1; k < 6; ++k) t = t + W.d2e1[k] * get(k - 1);
+    } else if (hi && pos == n - 1) {
+      t = W.d2e0[0] * get(0);
+#pragma unroll
+      for (int k = 1; k < 6; ++k) t = t + W.d2e0[k] * get(-k);
+    } else if (hi && pos == n - 2) {
+      t = W.d2e1[0] * get(1);
+#pragma unroll
+      for (int k = 1; k < 6; ++k) t = t + W.d2e1[k] * get(1 - k);
+    } else {
+      t = W.d2c[0] * get(-2);
+#pragma unroll
+      for (int k = 1; k < 5; ++k) t = t + W.d2c[k] * get(k - 2);
+    }
+  } else {
+    if (lo && pos == 0) {
+      t = W.d1e0[0] * get(0);
+#pragma unroll
+      for (int k = 1; k < 5; ++k) t = t + W.d1e0[k] * get(k);
+    } else if (lo && pos == 1) {
+      t = W.d1e1[0] * get(-1);
+#pragma unroll
+      for (int k = 1; k < 5; ++k) t = t + W.d1e1[k] * get(k - 1);
+    } else if (hi && pos == n - 1) {
+      t = (-W.d1e0[0]) * get(0);
+#pragma unroll
+      for (int k = 1; k < 5; ++k) t = t + (-W.d1e0[k]) * get(-k);
+    } else if (hi && pos == n - 2) {
+      t = (-W.d1e1[0]) * get(1);
+#pragma unroll
+      for (int k = 1; k < 5; ++k) t = t + (-W.d1e1[k]) * get(1 - k);
+    } else {
+      t = W.d1c[0] * get(-2);
+#pragma unroll
+      for (int k = 1; k < 5; ++k) t = t + W.d1c[k] * get(k - 2);
+    }
+  }
+  return pow2 ? t * inv_hp : t / hp;
+}
+
+struct RhsConst {
+  double h, h2, inv_h2;
+  bool pow2;
+  double r_eps, r_eps2;
+  double k_chi, k_phi, f0_chi, f0_phi;
+  int nonlinear;
+};
+
+// Acc: at(var, axis, offset) -> value; pos[d] interior index, n interior extent
+template <int DIM, class Acc>
+__device__ __forceinline__ double2 rhs_point(const Acc& acc, const int* pos, int n, int faces,
+                                             const double* x, const Weights& W, const RhsConst& R) {
+  double lap = 0.0;
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) {
+    auto get = [&](int o) { return acc.at(0, d, o); };
+    double t = deriv(get, 2, pos[d], n, faces & (1 << (2 * d)), faces & (2 << (2 * d)), W, R.h2, R.pow2,
+                     R.inv_h2);
+    lap = (d == 0) ? t : lap + t;
+  }
+  const double chi = acc.at(0, 0, 0);
+  const double phi = acc.at(1, 0, 0);
+  double dchi = phi, dphi = lap;
+  bool on_face = false;
+#pragma unroll
+  for (int d = 0; d < DIM; ++d)
+    on_face |= (((faces >> (2 * d)) & 1) && pos[d] == 0) || (((faces >> (2 * d + 1)) & 1) && pos[d] == n - 1);
+  if (R.nonlinear && !on_face) {
+    if (R.nonlinear == 1) {
+      double r2 = x[0] * x[0];
+#pragma unroll
+      for (int d = 1; d < DIM; ++d) r2 = r2 + x[d] * x[d];
+      double r2_reg = r2 > R.r_eps2 ? r2 : R.r_eps2;
+      dphi = dphi - sin(2.0 * chi) / r2_reg;
+    } else {
+      dphi = dphi - (chi * chi) * chi;
+    }
+  }
+  if (on_face) {  // radiative rows (wave.py:173-201)
+    double r2 = x[0] * x[0];
+#pragma unroll
+    for (int d = 1; d < DIM; ++d) r2 = r2 + x[d] * x[d];
+    double r = sqrt(r2);
+    r = r > R.r_eps ? r : R.r_eps;
+    double rad[2];
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      double a = 0.0;
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) {
+        auto get = [&](int o) { return acc.at(v, d, o); };
+        double g = deriv(get, 1, pos[d], n, faces & (1 << (2 * d)), faces & (2 << (2 * d)), W, R.h, false, 0.0);
+        double term = x[d] * g;
+        a = (d == 0) ? term : a + term;
+      }
+      rad[v] = a / r;
+    }
+    dchi = rad[0] - R.k_chi * (chi - R.f0_chi);
+    dphi = rad[1] - R.k_phi * (phi - R.f0_phi);
+  }
+  return make_double2(dchi, dphi);
+}
+
+template <int DIM, int PPO>
+struct SmemAcc {
+  const double2* sv;
+  int cell;
+  __device__ __forceinline__ double at(int v, int d, int o) const {
+    constexpr int NP = Tile<DIM, PPO>::NP;
+    int stride = (DIM == 3) ? (d == 0 ? NP * NP : (d == 1 ? NP : 1)) : (d == 0 ? NP : 1);
+    double2 q = sv[cell + o * stride];
+    return v == 0 ? q.x : q.y;
+  }
+};
+
+// --------------------------------------------------------------------------
+// the stage kernel
+// --------------------------------------------------------------------------
+template <int DIM, int PPO, bool LTS>
+__global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS)
+    stage_kernel(const AmrStageParams P) {
+  using T = Tile<DIM, PPO>;
+  __shared__ double2 sv[T::NS];
+  __shared__ short s_own[T::NI];
+  const int leaf = P.tile_ids[blockIdx.x];
+  const int32_t* __restrict__ tab = P.tile_table + (int64_t)leaf * T::NE;
+  const int64_t g0 = P.leaf_start[leaf];
+  const int64_t g1 = P.leaf_start[leaf + 1];
+  const int lvl = P.leaf_level[leaf];
+  const int cad = P.leaf_cadence[leaf];
+  const int s = P.stage;
+  const int64_t n = P.n_nodes;
+  const double2* U0 = reinterpret_cast<const double2*>(P.U0);
+  const double2* U1 = reinterpret_cast<const double2*>(P.U1);
+  const double2* K = reinterpret_cast<const double2*>(P.K);
+  const AmrSliceCoef* C = P.coef;
+
+  for (int e = threadIdx.x; e < T::NE; e += T::THREADS) {
+    const int ent = __ldg(tab + e);
+    double2 y;
+    if (ent >= 0) {
+      double2 v = stage_source<LTS>(P, U0, U1, K, n, ent, s, cad, C);
+      y = make_double2(0.0 + v.x, 0.0 + v.y);  // copy row: 0 + 1.0*src
+      if (e < T::NI && ent >= g0 && ent < g1) s_own[ent - g0] = (short)e;
+    } else if (ent == -1) {
+      y = make_double2(0.0, 0.0);
+    } else {
+      const int row = -ent - 2;
+      const int64_t k0 = __ldg(P.interp_ptr + row), k1 = __ldg(P.interp_ptr + row + 1);
+      y = make_double2(0.0, 0.0);
+      for (int64_t k = k0; k < k1; ++k) {
+        const int g = __ldg(P.interp_gid + k);
+        const double w = __ldg(P.interp_w + k);
+        double2 v = stage_source<LTS>(P, U0, U1, K, n, g, s, cad, C);
+        y.x = y.x + w * v.x;
+        y.y = y.y + w * v.y;
+      }
+    }
+    sv[cross_cell<DIM, PPO>(e)] = y;
+  }
+  __syncthreads();
+
+  const Weights& W = P;
+  RhsConst R;
+  R.h = P.h[lvl];
+  R.h2 = P.h2[lvl];
+  R.inv_h2 = P.inv_h2[lvl];
+  R.pow2 = P.h2_pow2[lvl] != 0;
+  R.r_eps = P.r_eps;
+  R.r_eps2 = P.r_eps2;
+  R.k_chi = P.k_chi;
+  R.k_phi = P.k_phi;
+  R.f0_chi = P.f0_chi;
+  R.f0_phi = P.f0_phi;
+  R.nonlinear = P.nonlinear;
+  int faces = 0;
+  const int64_t side = (int64_t)1 << (P.max_depth - lvl);
+  const int64_t spacing = side;  // lattice spacing of this level (finest lattice units)
+  int32_t anc[3];
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) {
+    anc[d] = P.leaf_anchor[leaf * 3 + d];
+    if (anc[d] == 0) faces |= 1 << (2 * d);
+    if (anc[d] + side == ((int64_t)1 << P.max_depth)) faces |= 2 << (2 * d);
+  }
+  const int scale = PPO - 1;
+  const int p = P.n_stages;
+  const bool last = (s == p - 1);
+  const int cur = LTS ? C->cur[cad] : P.gts_cur;
+  double2* Unew = reinterpret_cast<double2*>(cur ? P.U0 : P.U1);
+  const double2* Ucur = cur ? U1 : U0;
+  double2* Ks = reinterpret_cast<double2*>(P.K) + (int64_t)s * n;
+
+  const int n_own = (int)(g1 - g0);
+  for (int k = threadIdx.x; k < n_own; k += T::THREADS) {
+    const int q = s_own[k];
+    int pos[3];
+    int r = q;
+#pragma unroll
+    for (int d = DIM - 1; d >= 0; --d) {
+      pos[d] = r % PPO;
+      r /= PPO;
+    }
+    int cell = 0;
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) cell = cell * T::NP + (pos[d] + T::PAD);
+    double x[3];
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) {
+      int64_t lat = (int64_t)anc[d] * scale + spacing * pos[d];
+      x[d] = P.lo[d] + ((double)lat / (double)P.top_nodes) * P.extent[d];
+    }
+    SmemAcc<DIM, PPO> acc{sv, cell};
+    double2 ks = rhs_point<DIM>(acc, pos, PPO, faces, x, W, R);
+    const int64_t g = g0 + k;
+    if (!last) {
+      Ks[g] = ks;
+    } else {
+      if (LTS) Ks[g] = ks;
+      double2 u = ld2(Ucur + g);
+      double2 un = make_double2(0.0 + u.x, 0.0 + u.y);
+      for (int j = 0; j < p; ++j) {
+        double c = LTS ? C->comb[cad][j] : P.g_comb[j];
+        if (c == 0.0) continue;
+        double2 kj = (j == s) ? ks : ld2(K + (int64_t)j * n + g);
+        un.x = un.x + c * kj.x;
+        un.y = un.y + c * kj.y;
+      }
+      Unew[g] = un;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// Mesh.unzip over CSR rows
+// --------------------------------------------------------------------------
+__global__ void gather_rows_kernel(int64_t n_rows, const int64_t* __restrict__ ptr,
+                                   const int64_t* __restrict__ col, const double* __restrict__ val, int nv,
+                                   const double* __restrict__ z, int64_t zs, double* __restrict__ out,
+                                   int64_t os) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_rows * nv) return;
+  int64_t r = t % n_rows;
+  int v = (int)(t / n_rows);
+  double acc = 0.0;
+  for (int64_t k = ptr[r]; k < ptr[r + 1]; ++k) acc = acc + val[k] * z[v * zs + col[k]];
+  out[v * os + r] = acc;
+}
+
+// --------------------------------------------------------------------------
+// wave_rhs on one padded block (API path)
+// --------------------------------------------------------------------------
+template <int DIM>
+struct GlobalAcc {
+  const double* y;
+  int np, pad, cell;
+  int64_t var_stride;
+  __device__ __forceinline__ double at(int v, int d, int o) const {
+    int stride = (DIM == 3) ? (d == 0 ? np * np : (d == 1 ? np : 1)) : (d == 0 ? np : 1);
+    return y[v * var_stride + cell + o * stride];
+  }
+};
+
+template <int DIM>
+__global__ void block_rhs_kernel(int n, int pad, const double* __restrict__ y, double* __restrict__ out,
+                                 RhsConst R, const double* __restrict__ coords, int faces,
+                                 const AmrStageParams P) {
+  int64_t total = 1;
+  for (int d = 0; d < DIM; ++d) total *= n;
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  int pos[3];
+  int64_t r = t;
+  for (int d = DIM - 1; d >= 0; --d) {
+    pos[d] = (int)(r % n);
+    r /= n;
+  }
+  int np = n + 2 * pad;
+  int cell = 0;
+  for (int d = 0; d < DIM; ++d) cell = cell * np + (pos[d] + pad);
+  int64_t vs = 1;
+  for (int d = 0; d < DIM; ++d) vs *= np;
+  double x[3];
+  for (int d = 0; d < DIM; ++d) x[d] = coords[d * n + pos[d]];
+  const Weights& W = P;
+  GlobalAcc<DIM> acc{y, np, pad, cell, vs};
+  double2 v = rhs_point<DIM>(acc, pos, n, faces, x, W, R);
+  out[t] = v.x;
+  out[total + t] = v.y;
+}
+
+__global__ void pack_kernel(int64_t n_ranges, const int64_t* __restrict__ start,
+                            const int64_t* __restrict__ len, const int64_t* __restrict__ off, int width,
+                            const double* __restrict__ src, double* __restrict__ buf, int64_t total,
+                            bool unpack) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  int64_t node = t / width, c = t % width;
+  // binary search the range holding `node` (off = exclusive prefix of len)
+  int64_t lo = 0, hi = n_ranges - 1;
+  while (lo < hi) {
+    int64_t mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= node) lo = mid; else hi = mid - 1;
+  }
+  int64_t g = start[lo] + (node - off[lo]);
+  if (!unpack) buf[t] = src[g * width + c];
+  else const_cast<double*>(src)[g * width + c] = buf[t];
+}
+
+template <int DIM, int PPO>
+int launch_stage_t(const AmrStageParams* p, cudaStream_t st) {
+  if (p->n_tiles <= 0) return AMR_OK;
+  using T = Tile<DIM, PPO>;
+  if (p->lts)
+    stage_kernel<DIM, PPO, true><<<(unsigned)p->n_tiles, T::THREADS, 0, st>>>(*p);
+  else
+    stage_kernel<DIM, PPO, false><<<(unsigned)p->n_tiles, T::THREADS, 0, st>>>(*p);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? AMR_OK : cuda_fail(e, "amr_stage launch");
+}
+
+}  // namespace
+
+extern "C" int amr_stage(const AmrStageParams* p, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p->pad != 2) return AMR_EINVAL;
+  if (p->n_stages < 1 || p->n_stages > AMR_MAXP || p->stage < 0 || p->stage >= p->n_stages) return AMR_EINVAL;
+  if (p->dim == 2) {
+    if (p->ppo == 5) return launch_stage_t<2, 5>(p, st);
+    if (p->ppo == 7) return launch_stage_t<2, 7>(p, st);
+    if (p->ppo == 9) return launch_stage_t<2, 9>(p, st);
+  } else if (p->dim == 3) {
+    if (p->ppo == 5) return launch_stage_t<3, 5>(p, st);
+    if (p->ppo == 7) return launch_stage_t<3, 7>(p, st);
+    if (p->ppo == 9) return launch_stage_t<3, 9>(p, st);
+  }
+  amr_set_error_internal("amr_stage: unsupported (dim, ppo)");
+  return AMR_EINVAL;
+}
+
+extern "C" int amr_gather_rows(int64_t n_rows, const int64_t* row_ptr, const int64_t* col, const double* val,
+                               int nv, const double* z, int64_t z_stride, double* out, int64_t out_stride,
+                               void* stream) {
+  int64_t total = n_rows * nv;
+  if (total == 0) return AMR_OK;
+  unsigned blocks = (unsigned)((total + 255) / 256);
+  gather_rows_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n_rows, row_ptr, col, val, nv, z, z_stride, out,
+                                                               out_stride);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? AMR_OK : cuda_fail(e, "amr_gather_rows launch");
+}
+
+extern "C" int amr_block_rhs(int dim, int n, int pad, const double* y, double* out, double h, double h2,
+                             const double* coords, double r_eps, int faces, int nonlinear, double k_chi,
+                             double k_phi, double f0_chi, double f0_phi, const AmrStageParams* weights,
+                             void* stream) {
+  RhsConst R;
+  R.h = h;
+  R.h2 = h2;
+  R.inv_h2 = 0.0;
+  R.pow2 = false;
+  R.r_eps = r_eps;
+  R.r_eps2 = weights->r_eps2;
+  R.k_chi = k_chi;
+  R.k_phi = k_phi;
+  R.f0_chi = f0_chi;
+  R.f0_phi = f0_phi;
+  R.nonlinear = nonlinear;
+  int64_t total = 1;
+  for (int d = 0; d < dim; ++d) total *= n;
+  if (total == 0) return AMR_OK;
+  unsigned blocks = (unsigned)((total + 127) / 128);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dim == 2)
+    block_rhs_kernel<2><<<blocks, 128, 0, st>>>(n, pad, y, out, R, coords, faces, *weights);
+  else if (dim == 3)
+    block_rhs_kernel<3><<<blocks, 128, 0, st>>>(n, pad, y, out, R, coords, faces, *weights);
+  else
+    return AMR_EINVAL;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? AMR_OK : cuda_fail(e, "amr_block_rhs launch");
+}
+
+extern "C" int amr_pack_ranges(int64_t n_ranges, const int64_t* range_start, const int64_t* range_len,
+                               const int64_t* range_off, int width, const double* src, double* buf,
+                               int64_t total, void* stream) {
+  if (total <= 0) return AMR_OK;
+  unsigned blocks = (unsigned)((total * width + 255) / 256);
+  pack_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n_ranges, range_start, range_len, range_off, width,
+                                                        src, buf, total * width, false);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? AMR_OK : cuda_fail(e, "amr_pack_ranges launch");
+}
+
+extern "C" int amr_unpack_ranges(int64_t n_ranges, const int64_t* range_start, const int64_t* range_len,
+                                 const int64_t* range_off, int width, const double* buf, double* dst,
+                                 int64_t total, void* stream) {
+  if (total <= 0) return AMR_OK;
+  unsigned blocks = (unsigned)((total * width + 255) / 256);
+  pack_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n_ranges, range_start, range_len, range_off, width,
+                                                        dst, const_cast<double*>(buf), total * width, true);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? AMR_OK : cuda_fail(e, "amr_unpack_ranges launch");
+}

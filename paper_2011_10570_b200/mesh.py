@@ -1,0 +1,424 @@
+"""Block decomposition, node registry and zip/unzip — drop-in for ``amrlts.mesh``.
+
+The registry and every gather table are built by the native mesh builder
+(``amr_mesh_build``, C++).  Two views are exposed:
+
+* the reference's public view — maximal uniform ``blocks`` split at rank cuts,
+  per-block scipy CSR ``gathers``, ``zip_positions``, ``leaf_gids``,
+  ``node_coords`` (built lazily; API/debug only, mesh.py:153-492);
+* the engine's view — one *leaf tile* per leaf (ppo^D nodes + the 2-deep
+  stencil cross), as int32 unzip tables plus shared interpolation rows
+  (``tile_data``).  Leaf tiles reproduce maximal-block results bit for bit
+  because a gather row depends only on the lattice point it samples.
+
+``unzip`` runs on the GPU (``amr_gather_rows``); there is no CPU gather.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _native
+from .octree import LinearOctree, OctKey
+from .partition import ExchangePlan, PartitionMap, build_exchange_plan
+
+C = _native.C
+
+
+@dataclass(frozen=True)
+class Domain:
+    lo: tuple[float, ...]
+    hi: tuple[float, ...]
+
+    def extent(self, d: int) -> float:
+        return self.hi[d] - self.lo[d]
+
+
+@dataclass(frozen=True)
+class Block:
+    """Uniform patch: a root octant whose descendant leaves share ``leaf_level`` (mesh.py:48-84)."""
+
+    index: int
+    root: OctKey
+    leaf_level: int
+    leaf_range: tuple[int, int]
+    points_per_octant: int
+    pad: int
+    owner_rank: int
+
+    @property
+    def dim(self) -> int:
+        return self.root.dim
+
+    @property
+    def interior_n(self) -> int:
+        return (self.points_per_octant - 1) * (1 << (self.leaf_level - self.root.level)) + 1
+
+    @property
+    def interior_points(self) -> int:
+        return self.interior_n ** self.dim
+
+    @property
+    def padded_n(self) -> int:
+        return self.interior_n + 2 * self.pad
+
+    @property
+    def padded_shape(self) -> tuple[int, ...]:
+        return (self.padded_n,) * self.dim
+
+    @property
+    def interior_slices(self) -> tuple[slice, ...]:
+        return (slice(self.pad, self.pad + self.interior_n),) * self.dim
+
+
+def decompose_blocks(tree: LinearOctree, points_per_octant: int = 7, pad: int = 2,
+                     pmap: PartitionMap | None = None) -> list[Block]:
+    """Maximal uniform blocks split at rank cuts (mesh.py:87-135), native recursion."""
+    owners = pmap.owners(len(tree.leaves)) if pmap is not None else np.zeros(len(tree.leaves), dtype=int)
+    return _blocks_from_native(_NativeMesh(tree, points_per_octant, 2, owners, registry=False), tree,
+                               points_per_octant, pad)
+
+
+class _NativeMesh:
+    """Owning handle around AmrMesh*."""
+
+    def __init__(self, tree: LinearOctree, ppo: int, pad: int, owners, registry: bool = True):
+        anchors, levels = tree.arrays()
+        self.lib = _native.lib()
+        own = np.ascontiguousarray(owners, dtype=np.int32)
+        self.h = self.lib.amr_mesh_build(tree.dim, tree.max_depth, ppo, pad, len(levels),
+                                         _native.ptr(anchors, C.c_int32), _native.ptr(levels, C.c_int32),
+                                         _native.ptr(own, C.c_int32), 0)
+        if not self.h:
+            raise ValueError(_native.last_error())
+
+    def __del__(self):
+        h, self.h = getattr(self, "h", None), None
+        if h:
+            self.lib.amr_mesh_free(h)
+
+
+def _blocks_from_native(nm: _NativeMesh, tree, ppo, pad) -> list[Block]:
+    L = nm.lib
+    nb = L.amr_mesh_n_blocks(nm.h)
+    dim = tree.dim
+    ra = np.empty((nb, dim), dtype=np.int32)
+    rl = np.empty(nb, dtype=np.int32)
+    ll = np.empty(nb, dtype=np.int32)
+    lr = np.empty((nb, 2), dtype=np.int64)
+    ow = np.empty(nb, dtype=np.int32)
+    _native.check(L.amr_mesh_blocks(nm.h, _native.ptr(ra, C.c_int32), _native.ptr(rl, C.c_int32),
+                                    _native.ptr(ll, C.c_int32), _native.ptr(lr, C.c_int64),
+                                    _native.ptr(ow, C.c_int32)), "amr_mesh_blocks")
+    return [Block(index=i, root=OctKey(tuple(int(x) for x in ra[i]), int(rl[i]), tree.max_depth),
+                  leaf_level=int(ll[i]), leaf_range=(int(lr[i, 0]), int(lr[i, 1])),
+                  points_per_octant=ppo, pad=pad, owner_rank=int(ow[i]))
+            for i in range(nb)]
+
+
+class Mesh:
+    """Node registry, gather/scatter plans and synchronization maps (mesh.py:153-492)."""
+
+    def __init__(self, tree: LinearOctree, points_per_octant: int = 7, pad: int = 2,
+                 pmap: PartitionMap | None = None, domain: Domain | None = None):
+        if not tree.balanced:
+            raise ValueError("mesh construction requires a 2:1 balanced tree")
+        if points_per_octant < 5 or points_per_octant % 2 == 0:
+            raise ValueError("points_per_octant must be odd and >= 5")
+        if pad < 1 or pad > points_per_octant - 1:
+            raise ValueError("pad must be in [1, points_per_octant - 1]")
+        if pad != 2:
+            raise ValueError("the B200 engine implements the reference's 5-point stencil reach: pad must be 2")
+        self.tree = tree
+        self.dim = tree.dim
+        self.L = tree.max_depth
+        self.ppo = points_per_octant
+        self.pad = pad
+        self.scale = points_per_octant - 1
+        self.top_nodes = self.scale << self.L
+        if (self.top_nodes + 1) ** self.dim >= 2**62:
+            raise ValueError("max_depth too large for the node lattice encoding")
+        if domain is None:
+            domain = Domain((0.0,) * self.dim, (float(1 << self.L),) * self.dim)
+        self.domain = domain
+        if pmap is None:
+            w = np.ones(len(tree.leaves))
+            pmap = PartitionMap([(0, len(tree.leaves))], w, np.array([float(len(tree.leaves))]))
+        self.pmap = pmap
+        owners = pmap.owners(len(tree.leaves))
+        self._nm = _NativeMesh(tree, points_per_octant, pad, owners)
+        L = self._nm.lib
+        self.blocks = _blocks_from_native(self._nm, tree, points_per_octant, pad)
+        n_leaves = len(tree.leaves)
+        self.leaf_block = np.empty(n_leaves, dtype=int)
+        for b in self.blocks:
+            self.leaf_block[b.leaf_range[0]: b.leaf_range[1]] = b.index
+        self.n_nodes = int(L.amr_mesh_n_nodes(self._nm.h))
+        starts = np.empty(n_leaves + 1, dtype=np.int64)
+        _native.check(L.amr_mesh_leaf_starts(self._nm.h, _native.ptr(starts, C.c_int64)), "leaf_starts")
+        self.leaf_starts = starts
+        self.leaf_slices = np.stack([starts[:-1], starts[1:]], axis=1)
+        self._leaf_gids = None
+        self._node_coords = None
+        self._zip_positions = None
+        self._gathers = None
+        self._block_read = None
+        self._tile = None
+        self._plan: ExchangePlan | None = None
+        self._unzip_dev = None
+
+    # -- registry views --------------------------------------------------------
+    @property
+    def leaf_gids(self) -> np.ndarray:
+        if self._leaf_gids is None:
+            g = np.empty((len(self.tree.leaves), self.ppo ** self.dim), dtype=np.int32)
+            _native.check(self._nm.lib.amr_mesh_leaf_gids(self._nm.h, _native.ptr(g, C.c_int32)), "leaf_gids")
+            self._leaf_gids = g.astype(np.int64)
+        return self._leaf_gids
+
+    @property
+    def node_coords(self) -> np.ndarray:
+        if self._node_coords is None:
+            c = np.empty((self.n_nodes, self.dim), dtype=np.int32)
+            _native.check(self._nm.lib.amr_mesh_node_coords(self._nm.h, _native.ptr(c, C.c_int32)), "node_coords")
+            self._node_coords = c.astype(np.int64)
+        return self._node_coords
+
+    def leaf_spacing(self, level: int) -> int:
+        return 1 << (self.L - level)
+
+    def _leaf_points(self, key: OctKey) -> np.ndarray:
+        s = self.leaf_spacing(key.level)
+        axes = [a * self.scale + s * np.arange(self.ppo) for a in key.anchor]
+        grid = np.meshgrid(*axes, indexing="ij")
+        return np.stack([g.ravel() for g in grid], axis=-1).astype(np.int64)
+
+    def _block_org(self, b: Block) -> np.ndarray:
+        s = self.leaf_spacing(b.leaf_level)
+        return np.array(b.root.anchor, dtype=np.int64) * self.scale - b.pad * s
+
+    @property
+    def zip_positions(self) -> list[np.ndarray]:
+        """Per leaf: flat padded-block positions of its owned nodes (mesh.py:270-277)."""
+        if self._zip_positions is None:
+            gids = self.leaf_gids
+            out = []
+            for i, key in enumerate(self.tree.leaves):
+                a, e = self.leaf_slices[i]
+                owned = (gids[i] >= a) & (gids[i] < e)
+                pts = self._leaf_points(key)[owned]
+                b = self.blocks[self.leaf_block[i]]
+                rel = (pts - self._block_org(b)) // self.leaf_spacing(b.leaf_level)
+                out.append(np.ravel_multi_index(rel.T, b.padded_shape).astype(np.int64))
+            self._zip_positions = out
+        return self._zip_positions
+
+    def lookup_gids(self, codes: np.ndarray) -> np.ndarray:
+        m = self.top_nodes + 1
+        coords = self.node_coords
+        all_codes = coords[:, 0].copy()
+        for d in range(1, self.dim):
+            all_codes = all_codes * m + coords[:, d]
+        order = np.argsort(all_codes, kind="stable")
+        sc = all_codes[order]
+        codes = np.asarray(codes, dtype=np.int64)
+        pos = np.clip(np.searchsorted(sc, codes), 0, max(len(sc) - 1, 0))
+        hit = sc[pos] == codes if len(sc) else np.zeros(codes.shape, dtype=bool)
+        return np.where(hit, order[pos], -1)
+
+    # -- gathers ------------------------------------------------------------------
+    def _block_csr(self, b: int):
+        L = self._nm.lib
+        rows, nnz = C.c_int64(0), C.c_int64(0)
+        _native.check(L.amr_mesh_block_gather(self._nm.h, b, C.byref(rows), C.byref(nnz), None, None, None),
+                      "block_gather")
+        ptr = np.empty(rows.value + 1, dtype=np.int64)
+        col = np.empty(nnz.value, dtype=np.int64)
+        val = np.empty(nnz.value, dtype=np.float64)
+        _native.check(L.amr_mesh_block_gather(self._nm.h, b, C.byref(rows), C.byref(nnz),
+                                              _native.ptr(ptr, C.c_int64), _native.ptr(col, C.c_int64),
+                                              _native.ptr(val, C.c_double)), "block_gather")
+        return ptr, col, val
+
+    @property
+    def gathers(self):
+        """Per-block scipy CSR (padded points x n_nodes), rows sorted by gid."""
+        if self._gathers is None:
+            import scipy.sparse as sp
+
+            out = []
+            for b in self.blocks:
+                ptr, col, val = self._block_csr(b.index)
+                out.append(sp.csr_matrix((val, col, ptr), shape=(len(ptr) - 1, self.n_nodes)))
+            self._gathers = out
+        return self._gathers
+
+    def _read_sets(self):
+        if self._block_read is None:
+            starts = self.leaf_slices[:, 0]
+            reads = []
+            for b in self.blocks:
+                _, col, _ = self._block_csr(b.index)
+                support = np.unique(col)
+                reads.append(np.unique(np.searchsorted(starts, support, side="right") - 1))
+            self._block_read = reads
+        return self._block_read
+
+    def leaf_node_slice(self, leaf: int) -> tuple[int, int]:
+        a, b = self.leaf_slices[leaf]
+        return int(a), int(b)
+
+    def block_read_leaves(self, block_index: int) -> np.ndarray:
+        return self._read_sets()[block_index]
+
+    def zeros_zip(self, nvars: int = 1) -> np.ndarray:
+        return np.zeros((nvars, self.n_nodes))
+
+    def unzip(self, zip_values: np.ndarray) -> list[np.ndarray]:
+        """Padded per-block arrays gathered from the zipped field, on the GPU."""
+        import torch
+
+        z = np.atleast_2d(np.asarray(zip_values, dtype=np.float64))
+        nv = z.shape[0]
+        dev = torch.device("cuda")
+        if self._unzip_dev is None:
+            ptrs, cols, vals, offs = [np.zeros(1, dtype=np.int64)], [], [], [0]
+            base = 0
+            for b in self.blocks:
+                ptr, col, val = self._block_csr(b.index)
+                ptrs.append(ptr[1:] + base)
+                base += len(col)
+                cols.append(col)
+                vals.append(val)
+                offs.append(offs[-1] + len(ptr) - 1)
+            self._unzip_dev = (
+                torch.from_numpy(np.concatenate(ptrs)).to(dev),
+                torch.from_numpy(np.concatenate(cols) if cols else np.zeros(0, np.int64)).to(dev),
+                torch.from_numpy(np.concatenate(vals) if vals else np.zeros(0)).to(dev),
+                offs,
+            )
+        ptr_d, col_d, val_d, offs = self._unzip_dev
+        zd = torch.from_numpy(np.ascontiguousarray(z)).to(dev)
+        n_rows = offs[-1]
+        out = torch.empty((nv, n_rows), dtype=torch.float64, device=dev)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        _native.check(self._nm.lib.amr_gather_rows(n_rows, ptr_d.data_ptr(), col_d.data_ptr(), val_d.data_ptr(),
+                                                   nv, zd.data_ptr(), self.n_nodes, out.data_ptr(), n_rows,
+                                                   stream), "amr_gather_rows")
+        host = out.cpu().numpy()
+        return [np.ascontiguousarray(host[:, offs[i]:offs[i + 1]].reshape(nv, *b.padded_shape))
+                for i, b in enumerate(self.blocks)]
+
+    def zip(self, block_arrays: Sequence[np.ndarray]) -> np.ndarray:
+        """Zipped field from block interiors, owners win (mesh.py:422-432)."""
+        nvars = block_arrays[0].shape[0]
+        out = np.empty((nvars, self.n_nodes))
+        zp = self.zip_positions
+        for i in range(len(self.tree.leaves)):
+            a, b = self.leaf_slices[i]
+            if b == a:
+                continue
+            arr = block_arrays[self.leaf_block[i]].reshape(nvars, -1)
+            out[:, a:b] = arr[:, zp[i]]
+        return out
+
+    # -- engine view ---------------------------------------------------------------
+    def tile_data(self) -> dict:
+        """Leaf-tile unzip tables for the stage kernel (see include/amr_b200.h)."""
+        if self._tile is None:
+            L = self._nm.lib
+            n = len(self.tree.leaves)
+            E = int(L.amr_tile_entries(self.dim, self.ppo))
+            table = np.empty((n, E), dtype=np.int32)
+            _native.check(L.amr_mesh_tile_table(self._nm.h, _native.ptr(table, C.c_int32)), "tile_table")
+            nr = int(L.amr_mesh_interp_rows(self._nm.h))
+            nz = int(L.amr_mesh_interp_nnz(self._nm.h))
+            iptr = np.empty(nr + 1, dtype=np.int64)
+            igid = np.empty(max(nz, 1), dtype=np.int32)
+            iw = np.empty(max(nz, 1), dtype=np.float64)
+            _native.check(L.amr_mesh_interp_csr(self._nm.h, _native.ptr(iptr, C.c_int64),
+                                                _native.ptr(igid, C.c_int32), _native.ptr(iw, C.c_double)),
+                          "interp_csr")
+            anchors, levels = self.tree.arrays()
+            a3 = np.zeros((n, 3), dtype=np.int32)
+            a3[:, : self.dim] = anchors
+            self._tile = dict(table=table, entries=E, interp_ptr=iptr, interp_gid=igid, interp_w=iw,
+                              anchor3=a3, level=levels.astype(np.int32), starts=self.leaf_starts)
+        return self._tile
+
+    # -- sync maps -------------------------------------------------------------------
+    def exchange_plan(self) -> ExchangePlan:
+        if self._plan is None:
+            self._plan = build_exchange_plan(self, self.pmap)
+        return self._plan
+
+    def level_blocks(self, min_level: int) -> set[int]:
+        return {b.index for b in self.blocks if b.leaf_level >= min_level}
+
+    def build_sync_maps(self) -> tuple[ExchangePlan, list[ExchangePlan]]:
+        full = self.exchange_plan()
+        l_max = max(b.leaf_level for b in self.blocks)
+        l_min = min(b.leaf_level for b in self.blocks)
+        return full, [full.restrict(self.level_blocks(l_max - k)) for k in range(l_max - l_min + 1)]
+
+    # -- physical coordinates ----------------------------------------------------------
+    def node_physical(self) -> np.ndarray:
+        out = np.empty((self.n_nodes, self.dim))
+        nc = self.node_coords
+        for d in range(self.dim):
+            out[:, d] = self.domain.lo[d] + (nc[:, d] / self.top_nodes) * self.domain.extent(d)
+        return out
+
+    def block_axes(self, block: Block) -> list[np.ndarray]:
+        s = self.leaf_spacing(block.leaf_level)
+        org = self._block_org(block)
+        return [self.domain.lo[d] + ((org[d] + s * np.arange(block.padded_n)) / self.top_nodes) * self.domain.extent(d)
+                for d in range(self.dim)]
+
+    def level_spacing(self, level: int) -> float:
+        return self.domain.extent(0) * self.leaf_spacing(level) / self.top_nodes
+
+    def block_spacing(self, block: Block) -> float:
+        return self.level_spacing(block.leaf_level)
+
+    def finest_spacing(self) -> float:
+        return min(self.block_spacing(b) for b in self.blocks)
+
+    def block_domain_faces(self, block: Block) -> list[tuple[int, int]]:
+        out = []
+        side = block.root.side
+        for d in range(self.dim):
+            if block.root.anchor[d] == 0:
+                out.append((d, 0))
+            if block.root.anchor[d] + side == (1 << self.L):
+                out.append((d, 1))
+        return out
+
+
+def write_block_vtk(mesh: Mesh, block: Block, values: np.ndarray, name: str = "field") -> str:
+    """Legacy-VTK ASCII rectilinear grid of one block's interior (mesh.py:500-525)."""
+    axes = mesh.block_axes(block)
+    g, n = block.pad, block.interior_n
+    inner = [ax[g: g + n] for ax in axes]
+    if mesh.dim == 2:
+        inner.append(np.zeros(1))
+    dims = [len(a) for a in inner]
+    lines = ["# vtk DataFile Version 2.0", f"block {block.index}", "ASCII", "DATASET RECTILINEAR_GRID",
+             f"DIMENSIONS {dims[0]} {dims[1]} {dims[2]}"]
+    for label, ax in zip(("X", "Y", "Z"), inner):
+        lines.append(f"{label}_COORDINATES {len(ax)} double")
+        lines.append(" ".join(f"{v:.17g}" for v in ax))
+    interior = values[block.interior_slices]
+    lines += [f"POINT_DATA {interior.size}", f"SCALARS {name} double", "LOOKUP_TABLE default"]
+    lines.extend(f"{v:.17g}" for v in interior.transpose(*range(mesh.dim - 1, -1, -1)).ravel())
+    return "\n".join(lines) + "\n"
+
+
+def field_csv_rows(mesh: Mesh, block_arrays: Sequence[np.ndarray], var: int = 0):
+    """Rows ``block_id,i,j[,k],value`` over block interiors (mesh.py:528-533)."""
+    for b in mesh.blocks:
+        interior = block_arrays[b.index][var][b.interior_slices]
+        for idx in np.ndindex(*interior.shape):
+            yield (b.index, *idx, interior[idx])

@@ -1,0 +1,89 @@
+"""GPU parity against goldens produced by the unmodified reference Engine.
+
+Tolerances (BASELINE.json north_star): relative L-inf <= 1e-12 after one
+step / round, <= 1e-10 at the final time.  The kernels follow the reference's
+operation order, so linear and cubic runs are expected to be bit-exact; the
+sin source differs by libm-vs-CUDA ulps and is held to the tolerance only.
+"""
+import numpy as np
+import pytest
+
+from conftest import compare_field, golden
+from helpers import config_mesh
+
+from paper_2011_10570_b200.configs import CONFIGS
+from paper_2011_10570_b200.mesh import Domain, Mesh
+from paper_2011_10570_b200.octree import LinearOctree, SfcOrdering
+from paper_2011_10570_b200.stepper import Engine
+from paper_2011_10570_b200.wave import gaussian_pulse
+
+pytestmark = pytest.mark.gpu
+
+RUNS = {  # tag -> (tableau, mode, nonlinear)
+    "gts_rk4": ("rk4", "gts", False), "lts_rk4": ("rk4", "lts", False),
+    "lts_cubic": ("rk4", "lts", "cubic"), "gts_cubic": ("rk4", "gts", "cubic"),
+    "lts_sin": ("rk4", "lts", "sin"), "lts_rk3": ("rk3", "lts", False),
+    "gts_rk3": ("rk3", "gts", False), "lts_rk2": ("rk2", "lts", False), "lts_euler": ("euler", "lts", False),
+}
+
+
+def _checkpoints(gd, prefix, tag):
+    out = []
+    for k in gd.files:
+        if k.startswith(f"{prefix}{tag}_i"):
+            stem = k[len(prefix) + len(tag) + 2:].split("__")[0]
+            if stem.isdigit():
+                out.append(int(stem))
+    return sorted(set(out))
+
+
+def _run_case(mesh, chi0, gd, prefix, tag, results):
+    tab, mode, nl = RUNS[tag]
+    eng = Engine(mesh, tableau=tab, cfl=0.25, mode=mode, nonlinear=nl)
+    eng.initialize(chi0)
+    assert eng.dt_fine == float(gd[f"{prefix}{tag}_dt_fine"])
+    for cp in _checkpoints(gd, prefix, tag):
+        eng.run_to(cp)
+        exact, rel = compare_field(eng.current_zip(), gd, f"{prefix}{tag}_i{cp}")
+        results.append((tag, cp, exact, rel))
+    return eng
+
+
+def _assert_results(results, final_tol=1e-10, first_tol=1e-12):
+    for tag, cp, exact, rel in results:
+        tol = first_tol if cp <= 8 else final_tol
+        assert rel <= tol, (tag, cp, rel)
+        if "sin" not in tag:
+            assert exact, f"{tag} at slice {cp} not bit-exact (rel {rel:.3e})"
+
+
+@pytest.mark.parametrize("tag", ["gts_rk4", "lts_rk4", "lts_cubic", "gts_cubic", "lts_sin", "lts_rk3"])
+def test_cfg1_fields_match_reference(cuda, tag):
+    gd = golden("cfg1")
+    mesh = config_mesh("cfg1")
+    results = []
+    _run_case(mesh, CONFIGS["cfg1"].chi0(), gd, "", tag, results)
+    print(results)
+    _assert_results(results)
+
+
+@pytest.mark.parametrize("tag", ["gts_rk4", "lts_rk4", "lts_cubic"])
+def test_mini3d_fields_match_reference(cuda, tag):
+    gd = golden("mini3d")
+    mesh = config_mesh("mini3d")
+    results = []
+    _run_case(mesh, CONFIGS["mini3d"].chi0(), gd, "", tag, results)
+    print(results)
+    _assert_results(results)
+
+
+@pytest.mark.parametrize("tag", ["lts_rk3", "gts_rk3", "lts_rk4", "lts_rk2", "lts_euler", "lts_sin", "lts_cubic"])
+def test_ball_dom2_fields_match_reference(cuda, tag):
+    """Reference-test geometry: [-10,10]^2, ppo 5 (non-dyadic h: true divisions)."""
+    gd = golden("small")
+    tree = LinearOctree.from_arrays(gd["ball_anchor"], gd["ball_level"], 2, 4, SfcOrdering("morton", 2, 4), True)
+    mesh = Mesh(tree, points_per_octant=5, pad=2, domain=Domain((-10.0, -10.0), (10.0, 10.0)))
+    results = []
+    _run_case(mesh, gaussian_pulse((0.0, 0.0), 0.8, 1.0), gd, "ball_", tag, results)
+    print(results)
+    _assert_results(results)
