@@ -377,10 +377,14 @@ class Engine:
         return M
 
     def _slice_coef(self, i: int):
-        """Device AmrSliceCoef for slice i (depends on i only through i mod round)."""
+        """Device AmrSliceCoef for slice i.
+
+        It depends on i only through (i mod round, round parity): the coarsest
+        cadence steps once per round, so its live-buffer parity flips every round."""
         import torch
 
-        key = i % self.schedule.slices_per_round
+        R = self.schedule.slices_per_round
+        key = (i % R, (i // R) & 1)
         t = self._coef_cache.get(key)
         if t is not None:
             return t
