@@ -440,7 +440,9 @@ static void emit_block(OraMesh* m, const int32_t* node, int nlevel, int64_t a, i
   }
 }
 
-/* decompose_blocks recursion (mesh.py:115-131), Morton child order */
+/* decompose_blocks recursion (mesh.py:115-131).  Children are taken in the
+ * tree's SFC order: leaves of one child are contiguous along any SFC, so the
+ * children are the maximal runs of leaves sharing the child digit. */
 static void decompose(OraMesh* m, const int32_t* node, int nlevel, int64_t a, int64_t b) {
   int lvl = m->level[a], uniform = 1;
   for (int64_t i = a; i < b; ++i)
@@ -449,23 +451,19 @@ static void decompose(OraMesh* m, const int32_t* node, int nlevel, int64_t a, in
     emit_block(m, node, nlevel, a, b);
     return;
   }
-  int32_t half = 1 << (m->L - nlevel - 1);
+  int sh = m->L - (nlevel + 1);
   int64_t pos = a;
-  for (int code = 0; code < (1 << m->dim); ++code) {
+  while (pos < b) {
     int32_t ch[3];
-    for (int d = 0; d < m->dim; ++d) ch[d] = node[d] + (((code >> d) & 1) * half);
-    int32_t cs = half;
+    for (int d = 0; d < m->dim; ++d) ch[d] = (m->anchor[pos * m->dim + d] >> sh) << sh;
     int64_t end = pos;
     while (end < b) {
-      int inside = m->level[end] >= nlevel + 1;
-      for (int d = 0; d < m->dim; ++d) {
-        int32_t x = m->anchor[end * m->dim + d];
-        inside &= (ch[d] <= x && x < ch[d] + cs);
-      }
+      int inside = 1;
+      for (int d = 0; d < m->dim; ++d) inside &= ((m->anchor[end * m->dim + d] >> sh) << sh) == ch[d];
       if (!inside) break;
       ++end;
     }
-    if (end > pos) decompose(m, ch, nlevel + 1, pos, end);
+    decompose(m, ch, nlevel + 1, pos, end);
     pos = end;
   }
 }
