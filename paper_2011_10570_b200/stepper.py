@@ -240,7 +240,7 @@ class Engine:
         self._K = torch.zeros((self.p, n, 2), dtype=torch.float64, device=dev)
         self._node_cad_t = self._d["node_cad"].long()
         self._prm = self._make_params()
-        self._exchange = GhostExchange(self) if self._dist is not None else None
+        self._exchange = _EngineExchange(self) if self._dist is not None else None
 
     # -- setup -------------------------------------------------------------------------
     def _promoted_cadence(self, levels: list[int]) -> list[int]:
@@ -510,59 +510,67 @@ def compare_round(lts: Engine, gts: Engine) -> float:
 
 
 class GhostExchange:
-    """Ghost-leaf transport between ranks over torch.distributed (NCCL on GPUs).
+    """Ghost-leaf transport between ranks over torch.distributed (NCCL on GPUs,
+    gloo in the CPU tests).
 
     The reference ships whole leaf records after every stage and step
-    (stepper.py:318-361, partition.py:182-207).  Here the record fields that
-    changed are shipped: K_s of the leaves that just ran stage s, and their
-    new u after the step; t0/dt_units follow from the schedule and u_pre is
-    the other parity buffer the receiver already holds.  Which leaves go to
-    which rank is the reference's exchange plan (block gather footprints)."""
+    (stepper.py:318-361, partition.py:182-207).  Here only the record fields
+    that changed move: K_s of the leaves that just ran stage s, and their new
+    u after the step; t0/dt_units follow from the schedule and u_pre is the
+    other parity buffer the receiver already holds.  Which leaves go to which
+    rank is the reference's exchange plan (block gather footprints); since
+    every rank keeps the global zip layout, a shipment is a set of contiguous
+    gid ranges gathered into one buffer per peer."""
 
-    def __init__(self, engine: Engine):
-        import torch
-
-        self.eng = engine
-        self.group = engine._dist
-        self.rank = engine.rank
-        plan = engine.full_plan
-        cad = engine._leaf_cadence
-        starts = engine.mesh.leaf_starts
+    def __init__(self, plan: ExchangePlan, leaf_cadence: np.ndarray, leaf_starts: np.ndarray, rank: int,
+                 group=None, device=None):
+        self.group = group
+        self.rank = rank
+        self.cad = np.asarray(leaf_cadence)
+        self.starts = np.asarray(leaf_starts)
+        self.device = device
         self.send, self.recv = {}, {}
         for (s, r), items in plan.entries.items():
             leaves = np.array([e.leaf for e in items], dtype=np.int64)
-            if s == self.rank:
+            if s == rank:
                 self.send[r] = leaves
-            if r == self.rank:
+            if r == rank:
                 self.recv[s] = leaves
-        dev = engine.device
-
-        def index_for(leaves, min_cad):
-            sel = leaves[cad[leaves] >= min_cad]
-            if len(sel) == 0:
-                return None
-            idx = np.concatenate([np.arange(starts[l], starts[l + 1]) for l in sel])
-            return torch.from_numpy(idx).to(dev)
-
+        self.peers = sorted(set(self.send) | set(self.recv))
         self._idx = {}
-        for c in sorted(set(engine.cadence)):
-            for peer, leaves in self.send.items():
-                self._idx[("s", peer, c)] = index_for(leaves, c)
-            for peer, leaves in self.recv.items():
-                self._idx[("r", peer, c)] = index_for(leaves, c)
 
-    def _swap(self, tensor, min_cad: int) -> None:
+    @classmethod
+    def for_engine(cls, eng: "Engine") -> "GhostExchange":
+        return cls(eng.full_plan, eng._leaf_cadence, eng.mesh.leaf_starts, eng.rank, eng._dist, eng.device)
+
+    def _index(self, kind, peer, sel_key, select):
+        import torch
+
+        key = (kind, peer, sel_key)
+        if key not in self._idx:
+            leaves = (self.send if kind == "s" else self.recv).get(peer)
+            idx = None
+            if leaves is not None:
+                sel = leaves[select(self.cad[leaves])]
+                if len(sel):
+                    idx = torch.from_numpy(np.concatenate(
+                        [np.arange(self.starts[l], self.starts[l + 1]) for l in sel])).to(self.device)
+            self._idx[key] = idx
+        return self._idx[key]
+
+    def swap(self, tensor, sel_key, select) -> None:
+        """Ship rows of the selected leaves owned here to every peer that reads them."""
         import torch
         import torch.distributed as dist
 
         ops, bufs = [], []
-        for peer in sorted(set(self.send) | set(self.recv)):
-            si = self._idx.get(("s", peer, min_cad))
-            ri = self._idx.get(("r", peer, min_cad))
+        for peer in self.peers:
+            si = self._index("s", peer, sel_key, select)
+            ri = self._index("r", peer, sel_key, select)
             if si is not None:
                 ops.append(dist.P2POp(dist.isend, tensor.index_select(0, si).contiguous(), peer, self.group))
             if ri is not None:
-                rb = torch.empty((len(ri), tensor.shape[1]), dtype=tensor.dtype, device=tensor.device)
+                rb = torch.empty((len(ri),) + tuple(tensor.shape[1:]), dtype=tensor.dtype, device=tensor.device)
                 ops.append(dist.P2POp(dist.irecv, rb, peer, self.group))
                 bufs.append((ri, rb))
         if ops:
@@ -570,51 +578,29 @@ class GhostExchange:
                 w.wait()
         for ri, rb in bufs:
             tensor.index_copy_(0, ri, rb)
+
+    def swap_from_cadence(self, tensor, min_cad: int) -> None:
+        self.swap(tensor, ("ge", min_cad), lambda c: c >= min_cad)
+
+    def swap_cadence(self, tensor, cad: int) -> None:
+        self.swap(tensor, ("eq", cad), lambda c: c == cad)
+
+
+class _EngineExchange:
+    """Engine hooks: K_s after each stage, the new u after the step."""
+
+    def __init__(self, eng: Engine):
+        self.eng = eng
+        self.gx = GhostExchange.for_engine(eng)
 
     def after_stage(self, i: int, s: int, elig: list[int]) -> None:
         if elig:
             t0 = time.perf_counter()
-            self._swap(self.eng._K[s], min(elig))
+            self.gx.swap_from_cadence(self.eng._K[s], min(elig))
             self.eng.counters.phases["comm"] += time.perf_counter() - t0
 
     def after_step(self, i: int, elig: list[int]) -> None:
-        if not elig:
-            return
         t0 = time.perf_counter()
-        # the buffer each eligible cadence just wrote (parity after the step)
-        for c in elig:
-            buf = self.eng._U[self.eng._cur_parity(i + 1, c)]
-            self._swap_exact(buf, c)
+        for c in elig:  # each cadence wrote the buffer of its new parity
+            self.gx.swap_cadence(self.eng._U[self.eng._cur_parity(i + 1, c)], c)
         self.eng.counters.phases["comm"] += time.perf_counter() - t0
-
-    def _swap_exact(self, tensor, cad: int) -> None:
-        """Ship only leaves of exactly cadence ``cad`` (their u buffer parity is shared)."""
-        import torch
-        import torch.distributed as dist
-
-        key = ("exact", cad)
-        if key not in self._idx:
-            cadv = self.eng._leaf_cadence
-            starts = self.eng.mesh.leaf_starts
-            for kind, table in (("s", self.send), ("r", self.recv)):
-                for peer, leaves in table.items():
-                    sel = leaves[cadv[leaves] == cad]
-                    self._idx[(kind + "x", peer, cad)] = (
-                        torch.from_numpy(np.concatenate([np.arange(starts[l], starts[l + 1]) for l in sel])).to(
-                            self.eng.device) if len(sel) else None)
-            self._idx[key] = True
-        ops, bufs = [], []
-        for peer in sorted(set(self.send) | set(self.recv)):
-            si = self._idx.get(("sx", peer, cad))
-            ri = self._idx.get(("rx", peer, cad))
-            if si is not None:
-                ops.append(dist.P2POp(dist.isend, tensor.index_select(0, si).contiguous(), peer, self.group))
-            if ri is not None:
-                rb = torch.empty((len(ri), tensor.shape[1]), dtype=tensor.dtype, device=tensor.device)
-                ops.append(dist.P2POp(dist.irecv, rb, peer, self.group))
-                bufs.append((ri, rb))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
-        for ri, rb in bufs:
-            tensor.index_copy_(0, ri, rb)
