@@ -154,7 +154,8 @@ def time_rounds(eng, steps, torch, dist, per_launch=False):
             launches.append((e0, e1, int(P.n_tiles)))
             return rc
 
-        eng._lib = type("L", (), {"amr_stage": staticmethod(timed)})()
+        eng._lib = type("L", (), {"amr_stage": staticmethod(timed),
+                                  "amr_interp": staticmethod(L.amr_interp)})()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     start.record(stream)

@@ -75,7 +75,8 @@ int amr_mesh_node_coords(const AmrMesh* m, int32_t* coords);
 /* Leaf-tile unzip tables: per leaf, amr_tile_entries(dim,ppo) int32 entries
  * over the stencil cross (ppo^dim interior + 2*dim*pad*ppo^(dim-1) face halo).
  * entry >= 0: copy of zip node `entry`; -1: outside the domain (zero row);
- * <= -2: interpolation row (-entry-2) of the CSR below. */
+ * <= -2: interpolation row (-entry-2) of the CSR below (the engine remaps
+ * these to interpolation nodes, one per (row, reader cadence)). */
 int64_t amr_tile_entries(int dim, int ppo);
 int amr_mesh_tile_table(const AmrMesh* m, int32_t* table);
 int64_t amr_mesh_interp_rows(const AmrMesh* m);
@@ -128,6 +129,17 @@ typedef struct {
   const int32_t* leaf_cadence; /* [n_leaves] time level (== level for LTS; promoted for single-stage) */
   const int64_t* leaf_start;   /* [n_leaves+1] */
   const uint8_t* node_cadence; /* [n_nodes] cadence of the owning leaf (LTS) */
+  const uint8_t* tile_src_cad; /* [n_leaves][entries] cadence of each copy entry's source (LTS) */
+  int64_t n_chunks;            /* interpolation chunks of this launch (prefix; one CTA each) */
+  const int64_t* chunk_in;     /* [n_chunks_total+1] first interpolation node of each chunk */
+  const int64_t* in_tap;       /* [n_interp_total+1] first tap of each interpolation node */
+  const int32_t* in_cad;       /* [n_interp_total] reader cadence of each interpolation node */
+  const int32_t* tap_gid;      /* [n_taps] zip node of each tap, CSR (ascending gid) order */
+  const uint16_t* tap_w;       /* [n_taps] index into wtab */
+  const double* wtab;          /* distinct interpolation weights */
+  double* yh;                  /* [n_interp_total][2] interpolated stage inputs */
+  int n_vt;                    /* verbatim stage-source terms at this stage (a[s][j] != 0) */
+  int vt_j[AMR_MAXP];          /* their j */
   double* U0;                  /* [n_nodes][2] interleaved (chi, phi) */
   double* U1;
   double* K;                   /* [n_stages][n_nodes][2] */
@@ -154,6 +166,14 @@ typedef struct {
  * gathers[b].dot + wave_rhs + the K/state scatter (stepper.py:274-314,
  * 395-453). */
 int amr_stage(const AmrStageParams* p, void* stream);
+
+/* Interpolation pre-pass of a stage: yh[i] = 0 + sum_k w_k * src(g_k) over
+ * the taps of each interpolation node (a hanging point's row, mesh.py:316-351,
+ * per reader cadence), src = the reader's stage source.  One CTA per chunk of
+ * <= 2048 taps: products in parallel, sums in tap (ascending gid) order.
+ * Must run before amr_stage of the same stage; table entries <= -2 then read
+ * yh[-entry-2]. */
+int amr_interp(const AmrStageParams* p, void* stream);
 
 /* Mesh.unzip (mesh.py:413-420): out[v][r] = 0 + sum_k w_k * z[v][col_k] over
  * CSR rows (ascending col), z/out in (nv, n) layout. */

@@ -44,6 +44,11 @@ class AmrStageParams(C.Structure):
         ("interp_ptr", _vp), ("interp_gid", _vp), ("interp_w", _vp),
         ("leaf_anchor", _vp), ("leaf_level", _vp), ("leaf_cadence", _vp), ("leaf_start", _vp),
         ("node_cadence", _vp),
+        ("tile_src_cad", _vp),
+        ("n_chunks", C.c_int64),
+        ("chunk_in", _vp), ("in_tap", _vp), ("in_cad", _vp), ("tap_gid", _vp), ("tap_w", _vp), ("wtab", _vp),
+        ("yh", _vp),
+        ("n_vt", C.c_int), ("vt_j", C.c_int * AMR_MAXP),
         ("U0", _vp), ("U1", _vp), ("K", _vp),
         ("coef", _vp),
         ("g_cstage", (C.c_double * AMR_MAXP) * AMR_MAXP),
@@ -84,6 +89,7 @@ SIGNATURES = {
     "amr_mesh_blocks": ([_vp, _i32p, _i32p, _i32p, _i64p, _i32p], C.c_int),
     "amr_mesh_block_gather": ([_vp, C.c_int64, _i64p, _i64p, _i64p, _i64p, _f64p], C.c_int),
     "amr_stage": ([C.POINTER(AmrStageParams), _vp], C.c_int),
+    "amr_interp": ([C.POINTER(AmrStageParams), _vp], C.c_int),
     "amr_gather_rows": ([C.c_int64, _vp, _vp, _vp, C.c_int, _vp, C.c_int64, _vp, C.c_int64, _vp], C.c_int),
     "amr_block_rhs": ([C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_double, C.c_double, _vp, C.c_double,
                        C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,

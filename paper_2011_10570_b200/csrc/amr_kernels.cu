@@ -92,7 +92,7 @@ template <bool LTS>
 __device__ __forceinline__ double2 stage_source(const AmrStageParams& P, const double2* __restrict__ U0,
                                                 const double2* __restrict__ U1,
                                                 const double2* __restrict__ K, int64_t n, int g, int s,
-                                                int lr, const AmrSliceCoef* __restrict__ C) {
+                                                int lr, int ls, const AmrSliceCoef* __restrict__ C) {
   const int p = P.n_stages;
   if (!LTS) {
     const double2* U = P.gts_cur ? U1 : U0;
@@ -108,7 +108,6 @@ __device__ __forceinline__ double2 stage_source(const AmrStageParams& P, const d
     }
     return y;
   }
-  const int ls = P.node_cadence[g];
   const int mode = C->mode[lr][ls];
   const int cur = C->cur[ls];
   const double2* Uc = cur ? U1 : U0;
@@ -127,7 +126,8 @@ __device__ __forceinline__ double2 stage_source(const AmrStageParams& P, const d
   }
   double2 kk[AMR_MAXP];
   const int nk = (mode == 1) ? s : p;  // delta=0 transfer is lower triangular
-  for (int k = 0; k < nk; ++k) kk[k] = ld2(K + k * n + g);
+#pragma unroll
+  for (int k = 0; k < AMR_MAXP; ++k) kk[k] = (k < nk) ? ld2(K + k * n + g) : make_double2(0.0, 0.0);
   double2 y;
   if (mode == 1) {
     y = ld2(Uc + g);
@@ -135,10 +135,13 @@ __device__ __forceinline__ double2 stage_source(const AmrStageParams& P, const d
     const double2* Up = cur ? U0 : U1;
     y = ld2(Up + g);
     const double(*Mv)[AMR_MAXP] = C->Mv[lr][ls];
-    for (int i = 0; i < p; ++i) {
+#pragma unroll
+    for (int i = 0; i < AMR_MAXP; ++i) {
+      if (i >= p) break;
       double c = C->dtw[lr][ls][i];
       if (c == 0.0) continue;
       double ax = 0.0, ay = 0.0;
+#pragma unroll
       for (int k = 0; k <= i; ++k) {
         ax = fma(Mv[i][k], kk[k].x, ax);
         ay = fma(Mv[i][k], kk[k].y, ay);
@@ -148,12 +151,16 @@ __device__ __forceinline__ double2 stage_source(const AmrStageParams& P, const d
     }
   }
   const double(*M)[AMR_MAXP] = C->M[lr][ls];
-  for (int j = 0; j < s; ++j) {
+#pragma unroll
+  for (int j = 0; j < AMR_MAXP; ++j) {
+    if (j >= s) break;
     double c = C->cstage[lr][s][j];
     if (c == 0.0) continue;
-    int kmax = (mode == 1) ? j : p - 1;
+    const int kmax = (mode == 1) ? j : p - 1;
     double ax = 0.0, ay = 0.0;
-    for (int k = 0; k <= kmax; ++k) {
+#pragma unroll
+    for (int k = 0; k < AMR_MAXP; ++k) {
+      if (k > kmax) break;
       ax = fma(M[j][k], kk[k].x, ax);
       ay = fma(M[j][k], kk[k].y, ay);
     }
@@ -300,16 +307,70 @@ struct SmemAcc {
 };
 
 // --------------------------------------------------------------------------
+// interpolation pre-pass: one warp per (row, reader cadence) "interp node".
+// Lanes form the tap products w_k * src(g_k) in parallel (each rounded, as
+// numpy/scipy do), then two lanes add them in CSR (ascending gid) order from
+// 0.0 — bit-identical to the reference's csr_matvecs row sum.
+// --------------------------------------------------------------------------
+constexpr int INTERP_CHUNK = 2048;  // taps per block (products staged in smem)
+
+template <bool LTS>
+__global__ void __launch_bounds__(256) interp_kernel(const AmrStageParams P) {
+  __shared__ double2 prod[INTERP_CHUNK];
+  const int64_t in0 = __ldg(P.chunk_in + blockIdx.x), in1 = __ldg(P.chunk_in + blockIdx.x + 1);
+  const int64_t t0 = __ldg(P.in_tap + in0), t1 = __ldg(P.in_tap + in1);
+  const int lr = LTS ? __ldg(P.in_cad + in0) : 0;  // a chunk never mixes reader cadences
+  const double2* U0 = reinterpret_cast<const double2*>(P.U0);
+  const double2* U1 = reinterpret_cast<const double2*>(P.U1);
+  const double2* K = reinterpret_cast<const double2*>(P.K);
+  const int ntap = (int)(t1 - t0);
+  // phase A: every tap product in parallel (8 independent taps per thread per batch)
+  constexpr int B = 8;
+  for (int base = threadIdx.x; base < ntap; base += 256 * B) {
+    int g[B];
+    double w[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int k = base + u * 256;
+      g[u] = k < ntap ? __ldg(P.tap_gid + t0 + k) : -1;
+      w[u] = k < ntap ? __ldg(P.wtab + __ldg(P.tap_w + t0 + k)) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      if (g[u] < 0) continue;
+      const int ls = LTS ? P.node_cadence[g[u]] : 0;
+      const double2 v = stage_source<LTS>(P, U0, U1, K, P.n_nodes, g[u], P.stage, lr, ls, P.coef);
+      prod[base + u * 256] = make_double2(w[u] * v.x, w[u] * v.y);
+    }
+  }
+  __syncthreads();
+  // phase B: each interpolation node sums its products in CSR order from 0
+  double2* yh = reinterpret_cast<double2*>(P.yh);
+  for (int64_t i = in0 + threadIdx.x; i < in1; i += 256) {
+    const int a = (int)(__ldg(P.in_tap + i) - t0), e = (int)(__ldg(P.in_tap + i + 1) - t0);
+    double sx = 0.0, sy = 0.0;
+    for (int k = a; k < e; ++k) {
+      const double2 q = prod[k];
+      sx = sx + q.x;
+      sy = sy + q.y;
+    }
+    yh[i] = make_double2(sx, sy);
+  }
+}
+
+// --------------------------------------------------------------------------
 // the stage kernel
 // --------------------------------------------------------------------------
-template <int DIM, int PPO, bool LTS>
+template <int DIM, int PPO, bool LTS, int NT>
 __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS)
     stage_kernel(const AmrStageParams P) {
   using T = Tile<DIM, PPO>;
+  constexpr int EPT = (T::NE + T::THREADS - 1) / T::THREADS;
   __shared__ double2 sv[T::NS];
   __shared__ short s_own[T::NI];
   const int leaf = P.tile_ids[blockIdx.x];
   const int32_t* __restrict__ tab = P.tile_table + (int64_t)leaf * T::NE;
+  const uint8_t* __restrict__ side = LTS ? P.tile_src_cad + (int64_t)leaf * T::NE : nullptr;
   const int64_t g0 = P.leaf_start[leaf];
   const int64_t g1 = P.leaf_start[leaf + 1];
   const int lvl = P.leaf_level[leaf];
@@ -319,33 +380,65 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS)
   const double2* U0 = reinterpret_cast<const double2*>(P.U0);
   const double2* U1 = reinterpret_cast<const double2*>(P.U1);
   const double2* K = reinterpret_cast<const double2*>(P.K);
+  const double2* YH = reinterpret_cast<const double2*>(P.yh);
   const AmrSliceCoef* C = P.coef;
+  // verbatim stage-source terms of this stage: y = (0 + u) + sum_t c_t K_{j_t}
+  int js[NT > 0 ? NT : 1];
+  double cs[NT > 0 ? NT : 1];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    js[t] = P.vt_j[t];
+    cs[t] = LTS ? C->cstage[cad][s][js[t]] : P.g_cstage[s][js[t]];
+  }
+  const int cur = LTS ? C->cur[cad] : P.gts_cur;
+  const double2* Ucur = cur ? U1 : U0;
 
-  for (int e = threadIdx.x; e < T::NE; e += T::THREADS) {
-    const int ent = __ldg(tab + e);
-    double2 y;
-    if (ent >= 0) {
-      double2 v = stage_source<LTS>(P, U0, U1, K, n, ent, s, cad, C);
-      y = make_double2(0.0 + v.x, 0.0 + v.y);  // copy row: 0 + 1.0*src
-      if (e < T::NI && ent >= g0 && ent < g1) s_own[ent - g0] = (short)e;
-    } else if (ent == -1) {
-      y = make_double2(0.0, 0.0);
-    } else {
-      const int row = -ent - 2;
-      const int64_t k0 = __ldg(P.interp_ptr + row), k1 = __ldg(P.interp_ptr + row + 1);
-      y = make_double2(0.0, 0.0);
-      for (int64_t k = k0; k < k1; ++k) {
-        const int g = __ldg(P.interp_gid + k);
-        const double w = __ldg(P.interp_w + k);
-        double2 v = stage_source<LTS>(P, U0, U1, K, n, g, s, cad, C);
-        y.x = y.x + w * v.x;
-        y.y = y.y + w * v.y;
-      }
+  // ---- phase 1: all table entries of this thread first (coalesced), then all
+  //      data loads (independent, many in flight), then combine into smem
+  int ent[EPT];
+  bool fast[EPT];
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const int e = threadIdx.x + i * T::THREADS;
+    ent[i] = (e < T::NE) ? __ldg(tab + e) : -1;
+    fast[i] = ent[i] >= 0;
+    if (LTS && e < T::NE && fast[i]) fast[i] = C->mode[cad][side[e]] == 0;
+  }
+  double2 uv[EPT], kv[EPT][NT > 0 ? NT : 1];
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    uv[i] = make_double2(0.0, 0.0);
+    if (fast[i]) {
+      uv[i] = ld2(Ucur + ent[i]);
+#pragma unroll
+      for (int t = 0; t < NT; ++t) kv[i][t] = ld2(K + (int64_t)js[t] * n + ent[i]);
+    } else if (ent[i] <= -2) {
+      uv[i] = ld2(YH + (-ent[i] - 2));
     }
+  }
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const int e = threadIdx.x + i * T::THREADS;
+    if (e >= T::NE) continue;
+    double2 y = uv[i];  // zero row or precomputed interpolation row
+    if (fast[i]) {
+      y = make_double2(0.0 + uv[i].x, 0.0 + uv[i].y);
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        y.x = y.x + cs[t] * kv[i][t].x;
+        y.y = y.y + cs[t] * kv[i][t].y;
+      }
+      y = make_double2(0.0 + y.x, 0.0 + y.y);  // copy row: 0 + 1.0 * src
+    } else if (LTS && ent[i] >= 0) {
+      double2 v = stage_source<LTS>(P, U0, U1, K, n, ent[i], s, cad, side[e], C);
+      y = make_double2(0.0 + v.x, 0.0 + v.y);
+    }
+    if (e < T::NI && ent[i] >= g0 && ent[i] < g1) s_own[ent[i] - g0] = (short)e;
     sv[cross_cell<DIM, PPO>(e)] = y;
   }
   __syncthreads();
 
+  // ---- phase 2: RHS at the owned nodes, K_s (and the RK combine) out
   const Weights& W = P;
   RhsConst R;
   R.h = P.h[lvl];
@@ -360,23 +453,19 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS)
   R.f0_phi = P.f0_phi;
   R.nonlinear = P.nonlinear;
   int faces = 0;
-  const int64_t side = (int64_t)1 << (P.max_depth - lvl);
-  const int64_t spacing = side;  // lattice spacing of this level (finest lattice units)
+  const int64_t side_len = (int64_t)1 << (P.max_depth - lvl);
   int32_t anc[3];
 #pragma unroll
   for (int d = 0; d < DIM; ++d) {
     anc[d] = P.leaf_anchor[leaf * 3 + d];
     if (anc[d] == 0) faces |= 1 << (2 * d);
-    if (anc[d] + side == ((int64_t)1 << P.max_depth)) faces |= 2 << (2 * d);
+    if (anc[d] + side_len == ((int64_t)1 << P.max_depth)) faces |= 2 << (2 * d);
   }
-  const int scale = PPO - 1;
+  constexpr int scale = PPO - 1;
   const int p = P.n_stages;
   const bool last = (s == p - 1);
-  const int cur = LTS ? C->cur[cad] : P.gts_cur;
   double2* Unew = reinterpret_cast<double2*>(cur ? P.U0 : P.U1);
-  const double2* Ucur = cur ? U1 : U0;
   double2* Ks = reinterpret_cast<double2*>(P.K) + (int64_t)s * n;
-
   const int n_own = (int)(g1 - g0);
   for (int k = threadIdx.x; k < n_own; k += T::THREADS) {
     const int q = s_own[k];
@@ -393,22 +482,22 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS)
     double x[3];
 #pragma unroll
     for (int d = 0; d < DIM; ++d) {
-      int64_t lat = (int64_t)anc[d] * scale + spacing * pos[d];
+      const int64_t lat = (int64_t)anc[d] * scale + side_len * pos[d];
       x[d] = P.lo[d] + ((double)lat / (double)P.top_nodes) * P.extent[d];
     }
     SmemAcc<DIM, PPO> acc{sv, cell};
-    double2 ks = rhs_point<DIM>(acc, pos, PPO, faces, x, W, R);
+    const double2 ks = rhs_point<DIM>(acc, pos, PPO, faces, x, W, R);
     const int64_t g = g0 + k;
     if (!last) {
       Ks[g] = ks;
     } else {
       if (LTS) Ks[g] = ks;
-      double2 u = ld2(Ucur + g);
+      const double2 u = ld2(Ucur + g);
       double2 un = make_double2(0.0 + u.x, 0.0 + u.y);
       for (int j = 0; j < p; ++j) {
-        double c = LTS ? C->comb[cad][j] : P.g_comb[j];
+        const double c = LTS ? C->comb[cad][j] : P.g_comb[j];
         if (c == 0.0) continue;
-        double2 kj = (j == s) ? ks : ld2(K + (int64_t)j * n + g);
+        const double2 kj = (j == s) ? ks : ld2(K + (int64_t)j * n + g);
         un.x = un.x + c * kj.x;
         un.y = un.y + c * kj.y;
       }
@@ -493,14 +582,25 @@ __global__ void pack_kernel(int64_t n_ranges, const int64_t* __restrict__ start,
   else const_cast<double*>(src)[g * width + c] = buf[t];
 }
 
+template <int DIM, int PPO, bool LTS>
+int launch_stage_nt(const AmrStageParams* p, cudaStream_t st) {
+  using T = Tile<DIM, PPO>;
+  const unsigned grid = (unsigned)p->n_tiles;
+  switch (p->n_vt) {
+    case 0: stage_kernel<DIM, PPO, LTS, 0><<<grid, T::THREADS, 0, st>>>(*p); break;
+    case 1: stage_kernel<DIM, PPO, LTS, 1><<<grid, T::THREADS, 0, st>>>(*p); break;
+    case 2: stage_kernel<DIM, PPO, LTS, 2><<<grid, T::THREADS, 0, st>>>(*p); break;
+    case 3: stage_kernel<DIM, PPO, LTS, 3><<<grid, T::THREADS, 0, st>>>(*p); break;
+    default: return AMR_EINVAL;
+  }
+  return AMR_OK;
+}
+
 template <int DIM, int PPO>
 int launch_stage_t(const AmrStageParams* p, cudaStream_t st) {
   if (p->n_tiles <= 0) return AMR_OK;
-  using T = Tile<DIM, PPO>;
-  if (p->lts)
-    stage_kernel<DIM, PPO, true><<<(unsigned)p->n_tiles, T::THREADS, 0, st>>>(*p);
-  else
-    stage_kernel<DIM, PPO, false><<<(unsigned)p->n_tiles, T::THREADS, 0, st>>>(*p);
+  int rc = p->lts ? launch_stage_nt<DIM, PPO, true>(p, st) : launch_stage_nt<DIM, PPO, false>(p, st);
+  if (rc) return rc;
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? AMR_OK : cuda_fail(e, "amr_stage launch");
 }
@@ -522,6 +622,17 @@ extern "C" int amr_stage(const AmrStageParams* p, void* stream) {
   }
   amr_set_error_internal("amr_stage: unsupported (dim, ppo)");
   return AMR_EINVAL;
+}
+
+extern "C" int amr_interp(const AmrStageParams* p, void* stream) {
+  if (p->n_chunks <= 0) return AMR_OK;
+  const unsigned grid = (unsigned)p->n_chunks;
+  if (p->lts)
+    interp_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(*p);
+  else
+    interp_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(*p);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? AMR_OK : cuda_fail(e, "amr_interp launch");
 }
 
 extern "C" int amr_gather_rows(int64_t n_rows, const int64_t* row_ptr, const int64_t* col, const double* val,

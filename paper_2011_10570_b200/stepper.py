@@ -230,15 +230,30 @@ class Engine:
         tiles = mine[order].astype(np.int32)
         tcad = leaf_cad[tiles]
         self._prefix = {c: int(np.sum(tcad >= c)) for c in range(self.l_max + 1)}
+        table, in_row, in_cad = self._interp_nodes(td["table"], tiles, leaf_cad)
+        ip = self._interp_program(td, in_row, in_cad)
+        self._chunk_prefix = {c: int(np.sum(ip["chunk_cad"] >= c)) for c in range(self.l_max + 1)}
+        lts_kernel = mode == "lts" or any(c != self.l_max for c in cadence)
+        if lts_kernel:
+            side = np.zeros(table.shape, dtype=np.uint8)
+            cp = table >= 0
+            side[cp] = node_cad[table[cp]]
+        else:
+            side = np.zeros(1, dtype=np.uint8)
         dev = self.device
         T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
-        self._d = dict(tiles=T(tiles), table=T(td["table"]), iptr=T(td["interp_ptr"]), igid=T(td["interp_gid"]),
+        self._d = dict(tiles=T(tiles), table=T(table), iptr=T(td["interp_ptr"]), igid=T(td["interp_gid"]),
                        iw=T(td["interp_w"]), anchor=T(td["anchor3"]), level=T(td["level"]), cadence=T(leaf_cad),
-                       starts=T(td["starts"]), node_cad=T(node_cad))
+                       starts=T(td["starts"]), node_cad=T(node_cad), side=T(side),
+                       chunk_in=T(ip["chunk_in"]), in_tap=T(ip["in_tap"]),
+                       in_cad=T(in_cad if len(in_cad) else np.zeros(1, np.int32)),
+                       tap_gid=T(ip["tap_gid"]), tap_w=T(ip["tap_w"]), wtab=T(ip["wtab"]))
+        self._yh = torch.zeros((max(len(in_row), 1), 2), dtype=torch.float64, device=dev)
         n = mesh.n_nodes
         self._U = [torch.zeros((n, 2), dtype=torch.float64, device=dev) for _ in range(2)]
         self._K = torch.zeros((self.p, n, 2), dtype=torch.float64, device=dev)
         self._node_cad_t = self._d["node_cad"].long()
+        self._vt = [[j for j in range(s_) if self.tab.a[s_][j] != 0.0] for s_ in range(self.p)]
         self._prm = self._make_params()
         self._exchange = _EngineExchange(self) if self._dist is not None else None
 
@@ -260,11 +275,67 @@ class Engine:
                     cadence[i] = max(cadence[i], levels[j])
         return cadence
 
+    @staticmethod
+    def _interp_nodes(table: np.ndarray, tiles: np.ndarray, leaf_cad: np.ndarray):
+        """Deduplicate hanging-point rows into interpolation nodes, one per (row,
+        reader cadence), ordered by cadence (finest first) so that the nodes of
+        the eligible readers of any slice are a prefix; remap the table."""
+        table = table.copy()
+        sub = table[tiles]
+        hang = sub <= -2
+        if not hang.any():
+            return table, np.zeros(0, np.int32), np.zeros(0, np.int32)
+        rows = (-sub[hang] - 2).astype(np.int64)
+        cads = np.broadcast_to(leaf_cad[tiles][:, None], sub.shape)[hang].astype(np.int64)
+        key = (31 - cads) * (1 << 32) + rows
+        uniq, inv = np.unique(key, return_inverse=True)
+        in_cad = (31 - (uniq >> 32)).astype(np.int32)
+        in_row = (uniq & 0xFFFFFFFF).astype(np.int32)
+        sub[hang] = (-(inv + 2)).astype(np.int32)
+        table[tiles] = sub
+        return table, in_row, in_cad
+
+    CHUNK = 2048  # taps per interpolation CTA (INTERP_CHUNK in amr_kernels.cu)
+
+    @classmethod
+    def _interp_program(cls, td: dict, in_row: np.ndarray, in_cad: np.ndarray) -> dict:
+        """Flatten the interpolation nodes' taps (CSR order) with 16-bit weight
+        ids, and cut them into CTA chunks of <= CHUNK taps that never straddle
+        a node or a reader cadence."""
+        ptr, gid, w = td["interp_ptr"], td["interp_gid"], td["interp_w"]
+        counts = (ptr[in_row + 1] - ptr[in_row]).astype(np.int64) if len(in_row) else np.zeros(0, np.int64)
+        in_tap = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        idx = np.repeat(ptr[in_row] - in_tap[:-1], counts) + np.arange(in_tap[-1]) if len(in_row) else \
+            np.zeros(0, np.int64)
+        wtab, tap_w = np.unique(w[idx], return_inverse=True) if len(idx) else (np.zeros(1), np.zeros(0, np.int64))
+        if len(wtab) > 65535:
+            raise ValueError("more than 65535 distinct interpolation weights")
+        if len(counts) and counts.max() > cls.CHUNK:
+            raise ValueError("interpolation row longer than one chunk")
+        bounds, cads = [0], []
+        acc = 0
+        for i, (c, cad) in enumerate(zip(counts.tolist(), in_cad.tolist())):
+            if i > bounds[-1] and (acc + c > cls.CHUNK or cad != cads[-1]):
+                bounds.append(i)
+                acc = 0
+            if len(cads) < len(bounds):
+                cads.append(cad)
+            acc += c
+        if len(counts):
+            bounds.append(len(counts))
+        else:
+            cads = []
+        return dict(in_tap=in_tap, tap_gid=gid[idx].astype(np.int32) if len(idx) else np.zeros(1, np.int32),
+                    tap_w=tap_w.astype(np.uint16) if len(idx) else np.zeros(1, np.uint16),
+                    wtab=wtab.astype(np.float64), chunk_in=np.array(bounds, dtype=np.int64),
+                    chunk_cad=np.array(cads, dtype=np.int64))
+
     def _make_params(self) -> _native.AmrStageParams:
         m = self.mesh
         P = _native.AmrStageParams()
         P.dim, P.ppo, P.pad = m.dim, m.ppo, m.pad
         P.lts = 1 if self.mode == "lts" or any(c != self.l_max for c in self.cadence) else 0
+        P.n_chunks = 0
         P.n_stages = self.p
         P.nonlinear = self._nl
         P.n_nodes = m.n_nodes
@@ -274,6 +345,10 @@ class Engine:
         P.leaf_anchor, P.leaf_level = d["anchor"].data_ptr(), d["level"].data_ptr()
         P.leaf_cadence, P.leaf_start = d["cadence"].data_ptr(), d["starts"].data_ptr()
         P.node_cadence = d["node_cad"].data_ptr()
+        P.tile_src_cad = d["side"].data_ptr()
+        P.chunk_in, P.in_tap, P.in_cad = d["chunk_in"].data_ptr(), d["in_tap"].data_ptr(), d["in_cad"].data_ptr()
+        P.tap_gid, P.tap_w, P.wtab = d["tap_gid"].data_ptr(), d["tap_w"].data_ptr(), d["wtab"].data_ptr()
+        P.yh = self._yh.data_ptr()
         P.U0, P.U1, P.K = self._U[0].data_ptr(), self._U[1].data_ptr(), self._K.data_ptr()
         for s in range(self.p):
             for j in range(self.p):
@@ -445,6 +520,7 @@ class Engine:
         n_tiles = self._prefix[min(elig)] if elig else 0
         P = self._prm
         P.n_tiles = n_tiles
+        P.n_chunks = self._chunk_prefix[min(elig)] if elig else 0
         if P.lts:
             P.coef = self._slice_coef(i).data_ptr()
         else:
@@ -453,9 +529,17 @@ class Engine:
         t0 = time.perf_counter()
         for s in range(self.p):
             P.stage = s
-            rc = self._lib.amr_stage(C.byref(P), stream)
-            if rc:
-                _native.check(rc, "amr_stage")
+            vt = self._vt[s]
+            P.n_vt = len(vt)
+            for t, j in enumerate(vt):
+                P.vt_j[t] = j
+            if n_tiles:
+                rc = self._lib.amr_interp(C.byref(P), stream)
+                if rc:
+                    _native.check(rc, "amr_interp")
+                rc = self._lib.amr_stage(C.byref(P), stream)
+                if rc:
+                    _native.check(rc, "amr_stage")
             if self._exchange is not None:
                 self._exchange.after_stage(i, s, elig)
         if self._exchange is not None:
@@ -483,7 +567,7 @@ class Engine:
             self.advance_slice()
 
     def launches_per_slice(self, i: int) -> int:
-        return self.p if self._eligible_cadences(i) else 0
+        return 2 * self.p if self._eligible_cadences(i) else 0
 
     def close(self):
         self._exchange = None
