@@ -127,7 +127,7 @@ def units_per_round(eng, rank_only=True):
     for i in range(eng.schedule.slices_per_round):
         el = eng._eligible_cadences(i)
         total += eng.p * sum(by_cad.get(c, 0) for c in el)
-        launches += eng.p if el else 0
+        launches += 2 * eng.p if el else 0
     return total, launches
 
 

@@ -120,7 +120,7 @@ typedef struct {
   int64_t n_tiles;
   int64_t n_nodes;
   const int32_t* tile_ids;     /* leaf per CTA */
-  const int32_t* tile_table;   /* [n_leaves][entries] */
+  const int32_t* tile_table;   /* [n_tiles][entries], row t = tile t of the launch order */
   const int64_t* interp_ptr;
   const int32_t* interp_gid;
   const double* interp_w;
@@ -129,14 +129,17 @@ typedef struct {
   const int32_t* leaf_cadence; /* [n_leaves] time level (== level for LTS; promoted for single-stage) */
   const int64_t* leaf_start;   /* [n_leaves+1] */
   const uint8_t* node_cadence; /* [n_nodes] cadence of the owning leaf (LTS) */
-  const uint8_t* tile_src_cad; /* [n_leaves][entries] cadence of each copy entry's source (LTS) */
+  const uint8_t* tile_src_cad; /* [n_tiles][entries] cadence of each copy entry's source (LTS) */
   int64_t n_chunks;            /* interpolation chunks of this launch (prefix; one CTA each) */
   const int64_t* chunk_in;     /* [n_chunks_total+1] first interpolation node of each chunk */
-  const int64_t* in_tap;       /* [n_interp_total+1] first tap of each interpolation node */
+  const int32_t* chunk_cad;    /* [n_chunks_total] reader cadence of each chunk */
+  const int64_t* in_tap;       /* [n_interp_total][2] [first, end) tap of each interpolation node */
   const int32_t* in_cad;       /* [n_interp_total] reader cadence of each interpolation node */
-  const int32_t* tap_gid;      /* [n_taps] zip node of each tap, CSR (ascending gid) order */
+  const int32_t* tap_gid;      /* [n_chunks*2048] zip node of each tap, CSR (ascending gid) order; chunk b
+                                  starts at b*2048, padded with -1 */
   const uint16_t* tap_w;       /* [n_taps] index into wtab */
   const double* wtab;          /* distinct interpolation weights */
+  int64_t n_wtab;
   double* yh;                  /* [n_interp_total][2] interpolated stage inputs */
   int n_vt;                    /* verbatim stage-source terms at this stage (a[s][j] != 0) */
   int vt_j[AMR_MAXP];          /* their j */

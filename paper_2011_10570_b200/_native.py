@@ -46,7 +46,7 @@ class AmrStageParams(C.Structure):
         ("node_cadence", _vp),
         ("tile_src_cad", _vp),
         ("n_chunks", C.c_int64),
-        ("chunk_in", _vp), ("in_tap", _vp), ("in_cad", _vp), ("tap_gid", _vp), ("tap_w", _vp), ("wtab", _vp),
+        ("chunk_in", _vp), ("chunk_cad", _vp), ("in_tap", _vp), ("in_cad", _vp), ("tap_gid", _vp), ("tap_w", _vp), ("wtab", _vp), ("n_wtab", C.c_int64),
         ("yh", _vp),
         ("n_vt", C.c_int), ("vt_j", C.c_int * AMR_MAXP),
         ("U0", _vp), ("U1", _vp), ("K", _vp),

@@ -88,6 +88,71 @@ __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
 // --------------------------------------------------------------------------
 // stage source of one zip node as seen by a reader of cadence level lr
 // --------------------------------------------------------------------------
+__device__ __forceinline__ double2 lts_source(const double2* __restrict__ U0, const double2* __restrict__ U1,
+                                              const double2* __restrict__ K, int64_t n, int p, int g, int s, int lr,
+                                              int ls, const AmrSliceCoef* __restrict__ C) {
+  const int mode = C->mode[lr][ls];
+  const int cur = C->cur[ls];
+  const double2* Uc = cur ? U1 : U0;
+  if (mode == 0) {  // eligible, same step size: verbatim (stepper.py:290-296)
+    double2 u = ld2(Uc + g);
+    double2 y = make_double2(0.0 + u.x, 0.0 + u.y);
+    for (int j = 0; j < s; ++j) {
+      double c = C->cstage[lr][s][j];
+      if (c != 0.0) {
+        double2 k = ld2(K + j * n + g);
+        y.x = y.x + c * k.x;
+        y.y = y.y + c * k.y;
+      }
+    }
+    return y;
+  }
+  double2 kk[AMR_MAXP];
+  const int nk = (mode == 1) ? s : p;  // delta=0 transfer is lower triangular
+#pragma unroll
+  for (int k = 0; k < AMR_MAXP; ++k) kk[k] = (k < nk) ? ld2(K + k * n + g) : make_double2(0.0, 0.0);
+  double2 y;
+  if (mode == 1) {
+    y = ld2(Uc + g);
+  } else {  // virtual substep from u_pre (stepper.py:256-270)
+    const double2* Up = cur ? U0 : U1;
+    y = ld2(Up + g);
+    const double(*Mv)[AMR_MAXP] = C->Mv[lr][ls];
+#pragma unroll
+    for (int i = 0; i < AMR_MAXP; ++i) {
+      if (i >= p) break;
+      double c = C->dtw[lr][ls][i];
+      if (c == 0.0) continue;
+      double ax = 0.0, ay = 0.0;
+#pragma unroll
+      for (int k = 0; k <= i; ++k) {
+        ax = fma(Mv[i][k], kk[k].x, ax);
+        ay = fma(Mv[i][k], kk[k].y, ay);
+      }
+      y.x = y.x + c * ax;
+      y.y = y.y + c * ay;
+    }
+  }
+  const double(*M)[AMR_MAXP] = C->M[lr][ls];
+#pragma unroll
+  for (int j = 0; j < AMR_MAXP; ++j) {
+    if (j >= s) break;
+    double c = C->cstage[lr][s][j];
+    if (c == 0.0) continue;
+    const int kmax = (mode == 1) ? j : p - 1;
+    double ax = 0.0, ay = 0.0;
+#pragma unroll
+    for (int k = 0; k < AMR_MAXP; ++k) {
+      if (k > kmax) break;
+      ax = fma(M[j][k], kk[k].x, ax);
+      ay = fma(M[j][k], kk[k].y, ay);
+    }
+    y.x = y.x + c * ax;
+    y.y = y.y + c * ay;
+  }
+  return y;
+}
+
 template <bool LTS>
 __device__ __forceinline__ double2 stage_source(const AmrStageParams& P, const double2* __restrict__ U0,
                                                 const double2* __restrict__ U1,
@@ -317,13 +382,19 @@ constexpr int INTERP_CHUNK = 2048;  // taps per block (products staged in smem)
 template <bool LTS>
 __global__ void __launch_bounds__(256) interp_kernel(const AmrStageParams P) {
   __shared__ double2 prod[INTERP_CHUNK];
+  __shared__ double wsm[256];
+  const bool wsmall = P.n_wtab <= 256;
+  if (wsmall)
+    for (int i = threadIdx.x; i < P.n_wtab; i += blockDim.x) wsm[i] = P.wtab[i];
+  __syncthreads();
+  // taps of chunk b live at [b*CHUNK, b*CHUNK + CHUNK), padded with gid -1
+  const int64_t t0 = (int64_t)blockIdx.x * INTERP_CHUNK;
   const int64_t in0 = __ldg(P.chunk_in + blockIdx.x), in1 = __ldg(P.chunk_in + blockIdx.x + 1);
-  const int64_t t0 = __ldg(P.in_tap + in0), t1 = __ldg(P.in_tap + in1);
-  const int lr = LTS ? __ldg(P.in_cad + in0) : 0;  // a chunk never mixes reader cadences
+  const int lr = LTS ? __ldg(P.chunk_cad + blockIdx.x) : 0;  // a chunk never mixes reader cadences
   const double2* U0 = reinterpret_cast<const double2*>(P.U0);
   const double2* U1 = reinterpret_cast<const double2*>(P.U1);
   const double2* K = reinterpret_cast<const double2*>(P.K);
-  const int ntap = (int)(t1 - t0);
+  constexpr int ntap = INTERP_CHUNK;
   // phase A: every tap product in parallel (8 independent taps per thread per batch)
   constexpr int B = 8;
   for (int base = threadIdx.x; base < ntap; base += 256 * B) {
@@ -332,8 +403,9 @@ __global__ void __launch_bounds__(256) interp_kernel(const AmrStageParams P) {
 #pragma unroll
     for (int u = 0; u < B; ++u) {
       const int k = base + u * 256;
-      g[u] = k < ntap ? __ldg(P.tap_gid + t0 + k) : -1;
-      w[u] = k < ntap ? __ldg(P.wtab + __ldg(P.tap_w + t0 + k)) : 0.0;
+      g[u] = __ldg(P.tap_gid + t0 + k);
+      const int wi = __ldg(P.tap_w + t0 + k);
+      w[u] = wsmall ? wsm[wi] : __ldg(P.wtab + wi);
     }
 #pragma unroll
     for (int u = 0; u < B; ++u) {
@@ -347,7 +419,7 @@ __global__ void __launch_bounds__(256) interp_kernel(const AmrStageParams P) {
   // phase B: each interpolation node sums its products in CSR order from 0
   double2* yh = reinterpret_cast<double2*>(P.yh);
   for (int64_t i = in0 + threadIdx.x; i < in1; i += 256) {
-    const int a = (int)(__ldg(P.in_tap + i) - t0), e = (int)(__ldg(P.in_tap + i + 1) - t0);
+    const int a = (int)(__ldg(P.in_tap + 2 * i) - t0), e = (int)(__ldg(P.in_tap + 2 * i + 1) - t0);
     double sx = 0.0, sy = 0.0;
     for (int k = a; k < e; ++k) {
       const double2 q = prod[k];
@@ -359,56 +431,71 @@ __global__ void __launch_bounds__(256) interp_kernel(const AmrStageParams P) {
 }
 
 // --------------------------------------------------------------------------
-// the stage kernel
+// the stage kernel: one CTA per leaf tile.  Tables are stored in launch
+// (tile) order, so the table load does not wait for the tile's leaf id.
 // --------------------------------------------------------------------------
+
+// interface source (LTS, reader and source step sizes or times differ): out
+// of line so the verbatim hot path keeps its register budget.
+__device__ __noinline__ double2 iface_source(const double2* __restrict__ U0, const double2* __restrict__ U1,
+                                             const double2* __restrict__ K, int64_t n, int p, int g, int s, int lr,
+                                             int ls, const AmrSliceCoef* __restrict__ C) {
+  return lts_source(U0, U1, K, n, p, g, s, lr, ls, C);
+}
+
 template <int DIM, int PPO, bool LTS, int NT>
-__global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS)
+__global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, 3)
     stage_kernel(const AmrStageParams P) {
   using T = Tile<DIM, PPO>;
   constexpr int EPT = (T::NE + T::THREADS - 1) / T::THREADS;
+  constexpr int NK = NT > 0 ? NT : 1;
   __shared__ double2 sv[T::NS];
   __shared__ short s_own[T::NI];
-  const int leaf = P.tile_ids[blockIdx.x];
-  const int32_t* __restrict__ tab = P.tile_table + (int64_t)leaf * T::NE;
-  const uint8_t* __restrict__ side = LTS ? P.tile_src_cad + (int64_t)leaf * T::NE : nullptr;
+  const int64_t tile = blockIdx.x;
+  const int32_t* __restrict__ tab = P.tile_table + tile * T::NE;
+  const uint8_t* __restrict__ side = LTS ? P.tile_src_cad + tile * T::NE : nullptr;
+  // phase 1a: table entries (independent of the leaf-id load below)
+  int ent[EPT];
+  uint8_t sc[EPT];
+#pragma unroll
+  for (int i = 0; i < EPT; ++i) {
+    const int e = threadIdx.x + i * T::THREADS;
+    ent[i] = (e < T::NE) ? __ldg(tab + e) : -1;
+    sc[i] = (LTS && e < T::NE) ? __ldg(side + e) : 0;
+  }
+  const int leaf = P.tile_ids[tile];
   const int64_t g0 = P.leaf_start[leaf];
   const int64_t g1 = P.leaf_start[leaf + 1];
   const int lvl = P.leaf_level[leaf];
   const int cad = P.leaf_cadence[leaf];
   const int s = P.stage;
   const int64_t n = P.n_nodes;
+  const int p = P.n_stages;
   const double2* U0 = reinterpret_cast<const double2*>(P.U0);
   const double2* U1 = reinterpret_cast<const double2*>(P.U1);
   const double2* K = reinterpret_cast<const double2*>(P.K);
   const double2* YH = reinterpret_cast<const double2*>(P.yh);
   const AmrSliceCoef* C = P.coef;
-  // verbatim stage-source terms of this stage: y = (0 + u) + sum_t c_t K_{j_t}
-  int js[NT > 0 ? NT : 1];
-  double cs[NT > 0 ? NT : 1];
+  int js[NK];
+  double cs[NK];
 #pragma unroll
-  for (int t = 0; t < NT; ++t) {
-    js[t] = P.vt_j[t];
-    cs[t] = LTS ? C->cstage[cad][s][js[t]] : P.g_cstage[s][js[t]];
+  for (int t = 0; t < NK; ++t) {
+    js[t] = t < NT ? P.vt_j[t] : 0;
+    cs[t] = t < NT ? (LTS ? C->cstage[cad][s][js[t]] : P.g_cstage[s][js[t]]) : 0.0;
   }
   const int cur = LTS ? C->cur[cad] : P.gts_cur;
   const double2* Ucur = cur ? U1 : U0;
 
-  // ---- phase 1: all table entries of this thread first (coalesced), then all
-  //      data loads (independent, many in flight), then combine into smem
-  int ent[EPT];
-  bool fast[EPT];
+  // phase 1b: every data load of this thread in flight at once
+  uint32_t fast = 0;
+  double2 uv[EPT], kv[EPT][NK];
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
-    const int e = threadIdx.x + i * T::THREADS;
-    ent[i] = (e < T::NE) ? __ldg(tab + e) : -1;
-    fast[i] = ent[i] >= 0;
-    if (LTS && e < T::NE && fast[i]) fast[i] = C->mode[cad][side[e]] == 0;
-  }
-  double2 uv[EPT], kv[EPT][NT > 0 ? NT : 1];
-#pragma unroll
-  for (int i = 0; i < EPT; ++i) {
+    bool f = ent[i] >= 0;
+    if (LTS && f) f = C->mode[cad][sc[i]] == 0;
+    fast |= (uint32_t)f << i;
     uv[i] = make_double2(0.0, 0.0);
-    if (fast[i]) {
+    if (f) {
       uv[i] = ld2(Ucur + ent[i]);
 #pragma unroll
       for (int t = 0; t < NT; ++t) kv[i][t] = ld2(K + (int64_t)js[t] * n + ent[i]);
@@ -416,12 +503,13 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS)
       uv[i] = ld2(YH + (-ent[i] - 2));
     }
   }
+  // phase 1c: stage inputs -> smem
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
     const int e = threadIdx.x + i * T::THREADS;
     if (e >= T::NE) continue;
-    double2 y = uv[i];  // zero row or precomputed interpolation row
-    if (fast[i]) {
+    double2 y = uv[i];  // zero row or precomputed interpolation node
+    if (fast >> i & 1) {
       y = make_double2(0.0 + uv[i].x, 0.0 + uv[i].y);
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
@@ -430,7 +518,7 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS)
       }
       y = make_double2(0.0 + y.x, 0.0 + y.y);  // copy row: 0 + 1.0 * src
     } else if (LTS && ent[i] >= 0) {
-      double2 v = stage_source<LTS>(P, U0, U1, K, n, ent[i], s, cad, side[e], C);
+      const double2 v = iface_source(U0, U1, K, n, p, ent[i], s, cad, sc[i], C);
       y = make_double2(0.0 + v.x, 0.0 + v.y);
     }
     if (e < T::NI && ent[i] >= g0 && ent[i] < g1) s_own[ent[i] - g0] = (short)e;
@@ -438,7 +526,7 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS)
   }
   __syncthreads();
 
-  // ---- phase 2: RHS at the owned nodes, K_s (and the RK combine) out
+  // phase 2: RHS at the owned nodes, K_s (and the RK combine) out
   const Weights& W = P;
   RhsConst R;
   R.h = P.h[lvl];
@@ -462,7 +550,6 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS)
     if (anc[d] + side_len == ((int64_t)1 << P.max_depth)) faces |= 2 << (2 * d);
   }
   constexpr int scale = PPO - 1;
-  const int p = P.n_stages;
   const bool last = (s == p - 1);
   double2* Unew = reinterpret_cast<double2*>(cur ? P.U0 : P.U1);
   double2* Ks = reinterpret_cast<double2*>(P.K) + (int64_t)s * n;
@@ -582,18 +669,33 @@ __global__ void pack_kernel(int64_t n_ranges, const int64_t* __restrict__ start,
   else const_cast<double*>(src)[g * width + c] = buf[t];
 }
 
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int DIM, int PPO, bool LTS, int NT>
+int launch_stage_one(const AmrStageParams* p, cudaStream_t st) {
+  using T = Tile<DIM, PPO>;
+  stage_kernel<DIM, PPO, LTS, NT><<<(unsigned)p->n_tiles, T::THREADS, 0, st>>>(*p);
+  return AMR_OK;
+}
+
 template <int DIM, int PPO, bool LTS>
 int launch_stage_nt(const AmrStageParams* p, cudaStream_t st) {
-  using T = Tile<DIM, PPO>;
-  const unsigned grid = (unsigned)p->n_tiles;
   switch (p->n_vt) {
-    case 0: stage_kernel<DIM, PPO, LTS, 0><<<grid, T::THREADS, 0, st>>>(*p); break;
-    case 1: stage_kernel<DIM, PPO, LTS, 1><<<grid, T::THREADS, 0, st>>>(*p); break;
-    case 2: stage_kernel<DIM, PPO, LTS, 2><<<grid, T::THREADS, 0, st>>>(*p); break;
-    case 3: stage_kernel<DIM, PPO, LTS, 3><<<grid, T::THREADS, 0, st>>>(*p); break;
+    case 0: return launch_stage_one<DIM, PPO, LTS, 0>(p, st);
+    case 1: return launch_stage_one<DIM, PPO, LTS, 1>(p, st);
+    case 2: return launch_stage_one<DIM, PPO, LTS, 2>(p, st);
+    case 3: return launch_stage_one<DIM, PPO, LTS, 3>(p, st);
     default: return AMR_EINVAL;
   }
-  return AMR_OK;
 }
 
 template <int DIM, int PPO>

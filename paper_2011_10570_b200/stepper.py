@@ -232,7 +232,9 @@ class Engine:
         self._prefix = {c: int(np.sum(tcad >= c)) for c in range(self.l_max + 1)}
         table, in_row, in_cad = self._interp_nodes(td["table"], tiles, leaf_cad)
         ip = self._interp_program(td, in_row, in_cad)
-        self._chunk_prefix = {c: int(np.sum(ip["chunk_cad"] >= c)) for c in range(self.l_max + 1)}
+        ccad = ip["chunk_cad"][: ip["n_chunks"]]
+        self._chunk_prefix = {c: int(np.sum(ccad >= c)) for c in range(self.l_max + 1)}
+        table = table[tiles]  # launch (tile) order
         lts_kernel = mode == "lts" or any(c != self.l_max for c in cadence)
         if lts_kernel:
             side = np.zeros(table.shape, dtype=np.uint8)
@@ -245,7 +247,7 @@ class Engine:
         self._d = dict(tiles=T(tiles), table=T(table), iptr=T(td["interp_ptr"]), igid=T(td["interp_gid"]),
                        iw=T(td["interp_w"]), anchor=T(td["anchor3"]), level=T(td["level"]), cadence=T(leaf_cad),
                        starts=T(td["starts"]), node_cad=T(node_cad), side=T(side),
-                       chunk_in=T(ip["chunk_in"]), in_tap=T(ip["in_tap"]),
+                       chunk_in=T(ip["chunk_in"]), chunk_cad=T(ip["chunk_cad"]), in_tap=T(ip["in_tap"]),
                        in_cad=T(in_cad if len(in_cad) else np.zeros(1, np.int32)),
                        tap_gid=T(ip["tap_gid"]), tap_w=T(ip["tap_w"]), wtab=T(ip["wtab"]))
         self._yh = torch.zeros((max(len(in_row), 1), 2), dtype=torch.float64, device=dev)
@@ -299,36 +301,47 @@ class Engine:
 
     @classmethod
     def _interp_program(cls, td: dict, in_row: np.ndarray, in_cad: np.ndarray) -> dict:
-        """Flatten the interpolation nodes' taps (CSR order) with 16-bit weight
-        ids, and cut them into CTA chunks of <= CHUNK taps that never straddle
-        a node or a reader cadence."""
+        """Flatten the interpolation nodes' taps (CSR order, 16-bit weight ids)
+        into CTA chunks of CHUNK taps: chunk b occupies [b*CHUNK, (b+1)*CHUNK)
+        (padded with gid -1), never splits a node and never mixes reader
+        cadences, so a CTA finds its taps without a dependent lookup."""
         ptr, gid, w = td["interp_ptr"], td["interp_gid"], td["interp_w"]
-        counts = (ptr[in_row + 1] - ptr[in_row]).astype(np.int64) if len(in_row) else np.zeros(0, np.int64)
-        in_tap = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-        idx = np.repeat(ptr[in_row] - in_tap[:-1], counts) + np.arange(in_tap[-1]) if len(in_row) else \
-            np.zeros(0, np.int64)
-        wtab, tap_w = np.unique(w[idx], return_inverse=True) if len(idx) else (np.zeros(1), np.zeros(0, np.int64))
-        if len(wtab) > 65535:
-            raise ValueError("more than 65535 distinct interpolation weights")
-        if len(counts) and counts.max() > cls.CHUNK:
+        n_in = len(in_row)
+        counts = (ptr[in_row + 1] - ptr[in_row]).astype(np.int64) if n_in else np.zeros(0, np.int64)
+        if n_in and counts.max() > cls.CHUNK:
             raise ValueError("interpolation row longer than one chunk")
-        bounds, cads = [0], []
-        acc = 0
+        # greedy chunking (sequential by construction)
+        chunk_of = np.empty(n_in, dtype=np.int64)
+        pos_in_chunk = np.empty(n_in, dtype=np.int64)
+        bounds, cads = [], []
+        acc, cur_cad, ch = 0, None, -1
         for i, (c, cad) in enumerate(zip(counts.tolist(), in_cad.tolist())):
-            if i > bounds[-1] and (acc + c > cls.CHUNK or cad != cads[-1]):
+            if ch < 0 or acc + c > cls.CHUNK or cad != cur_cad:
+                ch += 1
                 bounds.append(i)
-                acc = 0
-            if len(cads) < len(bounds):
                 cads.append(cad)
+                acc, cur_cad = 0, cad
+            chunk_of[i] = ch
+            pos_in_chunk[i] = acc
             acc += c
-        if len(counts):
-            bounds.append(len(counts))
-        else:
-            cads = []
-        return dict(in_tap=in_tap, tap_gid=gid[idx].astype(np.int32) if len(idx) else np.zeros(1, np.int32),
-                    tap_w=tap_w.astype(np.uint16) if len(idx) else np.zeros(1, np.uint16),
-                    wtab=wtab.astype(np.float64), chunk_in=np.array(bounds, dtype=np.int64),
-                    chunk_cad=np.array(cads, dtype=np.int64))
+        n_chunks = ch + 1
+        bounds.append(n_in)
+        start = chunk_of * cls.CHUNK + pos_in_chunk
+        in_tap = np.stack([start, start + counts], axis=1).reshape(-1) if n_in else np.zeros(2, np.int64)
+        tap_gid = np.full(max(n_chunks, 1) * cls.CHUNK, -1, dtype=np.int32)
+        tap_w = np.zeros(max(n_chunks, 1) * cls.CHUNK, dtype=np.uint16)
+        wtab = np.zeros(1)
+        if n_in:
+            src_idx = np.repeat(ptr[in_row], counts) + (np.arange(counts.sum()) - np.repeat(np.cumsum(counts) - counts, counts))
+            dst_idx = np.repeat(start, counts) + (np.arange(counts.sum()) - np.repeat(np.cumsum(counts) - counts, counts))
+            wtab, widx = np.unique(w[src_idx], return_inverse=True)
+            if len(wtab) > 65535:
+                raise ValueError("more than 65535 distinct interpolation weights")
+            tap_gid[dst_idx] = gid[src_idx]
+            tap_w[dst_idx] = widx.astype(np.uint16)
+        return dict(in_tap=in_tap.astype(np.int64), tap_gid=tap_gid, tap_w=tap_w, wtab=wtab.astype(np.float64),
+                    chunk_in=np.array(bounds if n_in else [0, 0], dtype=np.int64),
+                    chunk_cad=np.array(cads if n_in else [0], dtype=np.int32), n_chunks=n_chunks if n_in else 0)
 
     def _make_params(self) -> _native.AmrStageParams:
         m = self.mesh
@@ -347,7 +360,9 @@ class Engine:
         P.node_cadence = d["node_cad"].data_ptr()
         P.tile_src_cad = d["side"].data_ptr()
         P.chunk_in, P.in_tap, P.in_cad = d["chunk_in"].data_ptr(), d["in_tap"].data_ptr(), d["in_cad"].data_ptr()
+        P.chunk_cad = d["chunk_cad"].data_ptr()
         P.tap_gid, P.tap_w, P.wtab = d["tap_gid"].data_ptr(), d["tap_w"].data_ptr(), d["wtab"].data_ptr()
+        P.n_wtab = int(d["wtab"].numel())
         P.yh = self._yh.data_ptr()
         P.U0, P.U1, P.K = self._U[0].data_ptr(), self._U[1].data_ptr(), self._K.data_ptr()
         for s in range(self.p):

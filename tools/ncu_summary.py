@@ -19,7 +19,8 @@ def main(path):
     print("|---|---|---|---|---|---|---|---|---|---|---|---|")
     for n, r in enumerate(rows[2:]):
         name = r[idx["Kernel Name"]]
-        short = ("interp_lts" if "ILb1E" in name else "interp_gts") if "interp" in name else ("stage" + ("_lts" if "ELb1E" in name else "_gts")) if "stage" in name else name[:20]
+        lts = ("true" in name) or ("ELb1E" in name) or ("ILb1E" in name)
+        short = ("interp" if "interp" in name else "stage") + ("_lts" if lts else "_gts")
         def g(m, scale=1.0):
             try:
                 return float(r[idx[m]]) * scale
