@@ -94,6 +94,12 @@ int amr_mesh_blocks(const AmrMesh* m, int32_t* root_anchor, int32_t* root_level,
 int amr_mesh_block_gather(AmrMesh* m, int64_t block, int64_t* rows, int64_t* nnz,
                           int64_t* row_ptr, int64_t* col, double* val);
 
+/* Greedy packing of interpolation nodes (counts[i] taps, reader cadence
+ * cads[i]) into chunks of <= `chunk` taps that never split a node or mix
+ * cadences; returns the number of chunks (-1 on error). */
+int64_t amr_pack_chunks(int64_t n, const int64_t* counts, const int32_t* cads, int64_t chunk,
+                        int64_t* chunk_of, int64_t* pos_in_chunk);
+
 /* --------------------------------------------------------------- kernels -- */
 
 /* Per-slice LTS coefficient block (device memory, built by the host from

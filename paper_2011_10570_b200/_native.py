@@ -88,6 +88,7 @@ SIGNATURES = {
     "amr_mesh_n_blocks": ([_vp], C.c_int64),
     "amr_mesh_blocks": ([_vp, _i32p, _i32p, _i32p, _i64p, _i32p], C.c_int),
     "amr_mesh_block_gather": ([_vp, C.c_int64, _i64p, _i64p, _i64p, _i64p, _f64p], C.c_int),
+    "amr_pack_chunks": ([C.c_int64, _i64p, _i32p, C.c_int64, _i64p, _i64p], C.c_int64),
     "amr_stage": ([C.POINTER(AmrStageParams), _vp], C.c_int),
     "amr_interp": ([C.POINTER(AmrStageParams), _vp], C.c_int),
     "amr_gather_rows": ([C.c_int64, _vp, _vp, _vp, C.c_int, _vp, C.c_int64, _vp, C.c_int64, _vp], C.c_int),

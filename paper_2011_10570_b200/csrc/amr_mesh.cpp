@@ -20,6 +20,9 @@
 
 #include <omp.h>
 
+#include <chrono>
+#include <cstdlib>
+
 #include <algorithm>
 #include <array>
 #include <cmath>
@@ -221,7 +224,8 @@ struct AmrMesh {
   std::vector<int64_t> iptr{0};
   std::vector<int32_t> igid;
   std::vector<double> iw;
-  std::unordered_map<int64_t, int32_t> row_of_code;
+  std::unordered_map<int64_t, int32_t> row_of_code;  // rows added after the build (API gathers)
+  std::vector<int64_t> hang_codes;                    // sorted codes of the build's rows (row id = index)
   std::unordered_map<int64_t, Row> memo;
   std::vector<AmrBlock> blocks;
 
@@ -306,8 +310,11 @@ struct AmrMesh {
     *npts_out = npts;
   }
 
-  // _point_weights (mesh.py:316-351): insertion-ordered sparse row
-  const Row& point_weights(const int64_t* p, int* err) {
+  // _point_weights (mesh.py:316-351): insertion-ordered sparse row.  `memo`
+  // only caches (any memo gives the same rows), so threads may use their own.
+  const Row& point_weights(const int64_t* p, int* err) { return point_weights_m(p, memo, err); }
+
+  const Row& point_weights_m(const int64_t* p, std::unordered_map<int64_t, Row>& memo, int* err) const {
     int64_t code = encode(p);
     auto hit = memo.find(code);
     if (hit != memo.end()) return hit->second;
@@ -357,7 +364,7 @@ struct AmrMesh {
         q[d] = org[d] + (int64_t)(w0[d] + cidx[d]) * s;
       }
       if (w == 0.0) continue;
-      Row sub = point_weights(q, err);  // copy: memo may rehash
+      Row sub = point_weights_m(q, memo, err);  // copy: memo may rehash
       if (*err) break;
       for (auto& gw : sub) {
         bool found = false;
@@ -375,6 +382,8 @@ struct AmrMesh {
 
   int32_t row_for(const int64_t* p, int* err) {
     int64_t code = encode(p);
+    auto hb = std::lower_bound(hang_codes.begin(), hang_codes.end(), code);
+    if (hb != hang_codes.end() && *hb == code) return (int32_t)(hb - hang_codes.begin());
     auto it = row_of_code.find(code);
     if (it != row_of_code.end()) return it->second;
     Row r = point_weights(p, err);
@@ -518,6 +527,15 @@ extern "C" AmrMesh* amr_mesh_build(int dim, int L, int ppo, int pad, int64_t n_l
       }
     }
   }
+  const bool timing = std::getenv("AMR_MESH_TIMING") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto tick = [&](const char* what) {
+    if (!timing) return;
+    auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[amr_mesh_build] %-14s %8.3f s\n", what,
+                 std::chrono::duration<double>(now - t_last).count());
+    t_last = now;
+  };
   const int P = m->per_leaf;
   m->leaf_gids.assign((size_t)n_leaves * P, -1);
   std::vector<int64_t> counts(n_leaves, 0);
@@ -559,6 +577,7 @@ extern "C" AmrMesh* amr_mesh_build(int dim, int L, int ppo, int pad, int64_t n_l
     }
     counts[i] = cnt;
   }
+  tick("ownership");
   if (bad) {
     fail(AMR_EINVAL, "leaf point outside every leaf: tree is not complete");
     delete m;
@@ -597,6 +616,7 @@ extern "C" AmrMesh* amr_mesh_build(int dim, int L, int ppo, int pad, int64_t n_l
       m->leaf_gids[(size_t)i * P + k] = m->leaf_gids[(size_t)o * P + m->local_index(o, p)];
     }
   }
+  tick("gids");
   // tile tables over the stencil cross
   const int64_t E = amr_tile_entries(dim, ppo);
   m->E = E;
@@ -642,19 +662,61 @@ extern "C" AmrMesh* amr_mesh_build(int dim, int L, int ppo, int pad, int64_t n_l
       }
     }
   }
+  tick("tile tables");
+  // unique hanging codes -> rows, computed in parallel with thread-local memos
+  std::vector<std::pair<int64_t, std::array<int64_t, 3>>> hc;
+  for (int t = 0; t < nt; ++t)
+    for (size_t k = 0; k < hang[t].size(); ++k)
+      hc.push_back({m->encode(hang_pt[t][k].data()), hang_pt[t][k]});
+  std::sort(hc.begin(), hc.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  hc.erase(std::unique(hc.begin(), hc.end(), [](const auto& a, const auto& b) { return a.first == b.first; }),
+           hc.end());
+  std::vector<Row> rows(hc.size());
   int err = 0;
-  for (int t = 0; t < nt && !err; ++t)
-    for (size_t k = 0; k < hang[t].size() && !err; ++k) {
-      int32_t row = m->row_for(hang_pt[t][k].data(), &err);
-      m->table[hang[t][k].first] = -2 - row;
+#pragma omp parallel num_threads(nt) reduction(| : err)
+  {
+    std::unordered_map<int64_t, Row> memo;
+#pragma omp for schedule(dynamic, 256)
+    for (int64_t k = 0; k < (int64_t)hc.size(); ++k) {
+      int e = 0;
+      Row r = m->point_weights_m(hc[k].second.data(), memo, &e);
+      if (e) {
+        err |= 1;
+        continue;
+      }
+      std::sort(r.begin(), r.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      rows[k] = std::move(r);
     }
+  }
   if (err) {
     fail(AMR_ESTATE, "lattice point outside the domain during interpolation");
     delete m;
     return nullptr;
   }
+  m->iptr.assign(rows.size() + 1, 0);
+  for (size_t k = 0; k < rows.size(); ++k) m->iptr[k + 1] = m->iptr[k] + (int64_t)rows[k].size();
+  m->igid.resize(m->iptr.back());
+  m->iw.resize(m->iptr.back());
+#pragma omp parallel for schedule(static) num_threads(nt)
+  for (int64_t k = 0; k < (int64_t)rows.size(); ++k)
+    for (size_t j = 0; j < rows[k].size(); ++j) {
+      m->igid[m->iptr[k] + j] = rows[k][j].first;
+      m->iw[m->iptr[k] + j] = rows[k][j].second;
+    }
+  m->hang_codes.resize(hc.size());
+  for (size_t k = 0; k < hc.size(); ++k) m->hang_codes[k] = hc[k].first;
+#pragma omp parallel for schedule(static, 1) num_threads(nt)
+  for (int t = 0; t < nt; ++t)
+    for (size_t k = 0; k < hang[t].size(); ++k) {
+      const int64_t code = m->encode(hang_pt[t][k].data());
+      const auto it = std::lower_bound(hc.begin(), hc.end(), code,
+                                       [](const auto& a, int64_t c) { return a.first < c; });
+      m->table[hang[t][k].first] = -2 - (int32_t)(it - hc.begin());
+    }
+  tick("interp rows");
   int32_t root[3] = {0, 0, 0};
   if (n_leaves > 0) decompose(m, root, 0, 0, n_leaves);
+  tick("blocks");
   return m;
 }
 
@@ -773,4 +835,28 @@ extern "C" int amr_mesh_block_gather(AmrMesh* m, int64_t block, int64_t* rows, i
   *rows = total;
   *nnz = cnt;
   return AMR_OK;
+}
+
+// Greedy packing of interpolation nodes into CTA chunks of <= `chunk` taps that
+// never split a node and never mix reader cadences (host runtime helper for
+// the engine's interpolation program).  Returns the chunk count.
+extern "C" int64_t amr_pack_chunks(int64_t n, const int64_t* counts, const int32_t* cads, int64_t chunk,
+                                   int64_t* chunk_of, int64_t* pos_in_chunk) {
+  int64_t ch = -1, acc = 0;
+  int32_t cur = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (counts[i] > chunk) {
+      fail(AMR_EINVAL, "interpolation row longer than one chunk");
+      return -1;
+    }
+    if (ch < 0 || acc + counts[i] > chunk || cads[i] != cur) {
+      ++ch;
+      acc = 0;
+      cur = cads[i];
+    }
+    chunk_of[i] = ch;
+    pos_in_chunk[i] = acc;
+    acc += counts[i];
+  }
+  return ch + 1;
 }

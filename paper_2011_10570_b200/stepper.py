@@ -310,22 +310,19 @@ class Engine:
         counts = (ptr[in_row + 1] - ptr[in_row]).astype(np.int64) if n_in else np.zeros(0, np.int64)
         if n_in and counts.max() > cls.CHUNK:
             raise ValueError("interpolation row longer than one chunk")
-        # greedy chunking (sequential by construction)
         chunk_of = np.empty(n_in, dtype=np.int64)
         pos_in_chunk = np.empty(n_in, dtype=np.int64)
-        bounds, cads = [], []
-        acc, cur_cad, ch = 0, None, -1
-        for i, (c, cad) in enumerate(zip(counts.tolist(), in_cad.tolist())):
-            if ch < 0 or acc + c > cls.CHUNK or cad != cur_cad:
-                ch += 1
-                bounds.append(i)
-                cads.append(cad)
-                acc, cur_cad = 0, cad
-            chunk_of[i] = ch
-            pos_in_chunk[i] = acc
-            acc += c
-        n_chunks = ch + 1
-        bounds.append(n_in)
+        cads32 = np.ascontiguousarray(in_cad, dtype=np.int32)
+        n_chunks = int(_native.lib().amr_pack_chunks(n_in, _native.ptr(np.ascontiguousarray(counts), C.c_int64),
+                                                      _native.ptr(cads32, C.c_int32), cls.CHUNK,
+                                                      _native.ptr(chunk_of, C.c_int64),
+                                                      _native.ptr(pos_in_chunk, C.c_int64)))
+        if n_chunks < 0:
+            raise ValueError(_native.last_error())
+        first = np.ones(n_in, dtype=bool)
+        first[1:] = chunk_of[1:] != chunk_of[:-1]
+        bounds = np.concatenate([np.nonzero(first)[0], [n_in]]).tolist() if n_in else [0]
+        cads = cads32[first].tolist() if n_in else []
         start = chunk_of * cls.CHUNK + pos_in_chunk
         in_tap = np.stack([start, start + counts], axis=1).reshape(-1) if n_in else np.zeros(2, np.int64)
         tap_gid = np.full(max(n_chunks, 1) * cls.CHUNK, -1, dtype=np.int32)
