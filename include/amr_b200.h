@@ -76,7 +76,7 @@ int amr_mesh_node_coords(const AmrMesh* m, int32_t* coords);
  * over the stencil cross (ppo^dim interior + 2*dim*pad*ppo^(dim-1) face halo).
  * entry >= 0: copy of zip node `entry`; -1: outside the domain (zero row);
  * <= -2: interpolation row (-entry-2) of the CSR below (the engine remaps
- * these to interpolation nodes, one per (row, reader cadence)). */
+ * these to the tile's own interpolation nodes). */
 int64_t amr_tile_entries(int dim, int ppo);
 int amr_mesh_tile_table(const AmrMesh* m, int32_t* table);
 int64_t amr_mesh_interp_rows(const AmrMesh* m);
@@ -136,17 +136,18 @@ typedef struct {
   const int64_t* leaf_start;   /* [n_leaves+1] */
   const uint8_t* node_cadence; /* [n_nodes] cadence of the owning leaf (LTS) */
   const uint8_t* tile_src_cad; /* [n_tiles][entries] cadence of each copy entry's source (LTS) */
-  int64_t n_chunks;            /* interpolation chunks of this launch (prefix; one CTA each) */
-  const int64_t* chunk_in;     /* [n_chunks_total+1] first interpolation node of each chunk */
-  const int32_t* chunk_cad;    /* [n_chunks_total] reader cadence of each chunk */
-  const int64_t* in_tap;       /* [n_interp_total][2] [first, end) tap of each interpolation node */
-  const int32_t* in_cad;       /* [n_interp_total] reader cadence of each interpolation node */
-  const int32_t* tap_gid;      /* [n_chunks*2048] zip node of each tap, CSR (ascending gid) order; chunk b
-                                  starts at b*2048, padded with -1 */
-  const uint16_t* tap_w;       /* [n_taps] index into wtab */
+  /* per-tile interpolation program: the hanging points of each tile (rows of
+   * mesh.py:316-351), summed from a per-tile set of unique source nodes */
+  const int64_t* tile_slot_ptr; /* [n_tiles+1] source slots of tile t: [ptr[t], ptr[t+1]) */
+  const int32_t* slot_gid;     /* zip node of each slot */
+  const uint8_t* slot_cad;     /* cadence of the slot's source leaf (LTS) */
+  const int64_t* tile_in_ptr;  /* [n_tiles+1] interpolation nodes of tile t */
+  const int64_t* in_tap_ptr;   /* [n_in+1] taps of node j, CSR (ascending gid) order */
+  const uint16_t* in_entry;    /* [n_in] cross entry the node fills */
+  const uint32_t* tap;         /* [n_taps] (tile-local slot << 16) | weight id */
   const double* wtab;          /* distinct interpolation weights */
   int64_t n_wtab;
-  double* yh;                  /* [n_interp_total][2] interpolated stage inputs */
+  int max_slots;               /* largest slot set of any tile (dynamic shared memory) */
   int n_vt;                    /* verbatim stage-source terms at this stage (a[s][j] != 0) */
   int vt_j[AMR_MAXP];          /* their j */
   double* U0;                  /* [n_nodes][2] interleaved (chi, phi) */
@@ -170,19 +171,14 @@ typedef struct {
 } AmrStageParams;
 
 /* One RK stage over a prefix of the tile list: fused unzip (spatial + LTS time
- * interpolation) + RHS stencil + zip of K_s; the last stage also fuses the RK
- * combine and record rotation.  Replaces Engine._stage_source +
+ * interpolation, hanging rows summed in ascending-gid order from a per-tile
+ * smem set of source values) + RHS stencil + zip of K_s; the last stage also
+ * fuses the RK combine and record rotation.  Replaces Engine._stage_source +
  * gathers[b].dot + wave_rhs + the K/state scatter (stepper.py:274-314,
  * 395-453). */
 int amr_stage(const AmrStageParams* p, void* stream);
 
-/* Interpolation pre-pass of a stage: yh[i] = 0 + sum_k w_k * src(g_k) over
- * the taps of each interpolation node (a hanging point's row, mesh.py:316-351,
- * per reader cadence), src = the reader's stage source.  One CTA per chunk of
- * <= 2048 taps: products in parallel, sums in tap (ascending gid) order.
- * Must run before amr_stage of the same stage; table entries <= -2 then read
- * yh[-entry-2]. */
-int amr_interp(const AmrStageParams* p, void* stream);
+
 
 /* Mesh.unzip (mesh.py:413-420): out[v][r] = 0 + sum_k w_k * z[v][col_k] over
  * CSR rows (ascending col), z/out in (nv, n) layout. */

@@ -45,9 +45,9 @@ class AmrStageParams(C.Structure):
         ("leaf_anchor", _vp), ("leaf_level", _vp), ("leaf_cadence", _vp), ("leaf_start", _vp),
         ("node_cadence", _vp),
         ("tile_src_cad", _vp),
-        ("n_chunks", C.c_int64),
-        ("chunk_in", _vp), ("chunk_cad", _vp), ("in_tap", _vp), ("in_cad", _vp), ("tap_gid", _vp), ("tap_w", _vp), ("wtab", _vp), ("n_wtab", C.c_int64),
-        ("yh", _vp),
+        ("tile_slot_ptr", _vp), ("slot_gid", _vp), ("slot_cad", _vp), ("tile_in_ptr", _vp),
+        ("in_tap_ptr", _vp), ("in_entry", _vp), ("tap", _vp), ("wtab", _vp), ("n_wtab", C.c_int64),
+        ("max_slots", C.c_int),
         ("n_vt", C.c_int), ("vt_j", C.c_int * AMR_MAXP),
         ("U0", _vp), ("U1", _vp), ("K", _vp),
         ("coef", _vp),
@@ -90,7 +90,6 @@ SIGNATURES = {
     "amr_mesh_block_gather": ([_vp, C.c_int64, _i64p, _i64p, _i64p, _i64p, _f64p], C.c_int),
     "amr_pack_chunks": ([C.c_int64, _i64p, _i32p, C.c_int64, _i64p, _i64p], C.c_int64),
     "amr_stage": ([C.POINTER(AmrStageParams), _vp], C.c_int),
-    "amr_interp": ([C.POINTER(AmrStageParams), _vp], C.c_int),
     "amr_gather_rows": ([C.c_int64, _vp, _vp, _vp, C.c_int, _vp, C.c_int64, _vp, C.c_int64, _vp], C.c_int),
     "amr_block_rhs": ([C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_double, C.c_double, _vp, C.c_double,
                        C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,

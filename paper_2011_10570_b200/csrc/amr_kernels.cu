@@ -372,65 +372,6 @@ struct SmemAcc {
 };
 
 // --------------------------------------------------------------------------
-// interpolation pre-pass: one warp per (row, reader cadence) "interp node".
-// Lanes form the tap products w_k * src(g_k) in parallel (each rounded, as
-// numpy/scipy do), then two lanes add them in CSR (ascending gid) order from
-// 0.0 — bit-identical to the reference's csr_matvecs row sum.
-// --------------------------------------------------------------------------
-constexpr int INTERP_CHUNK = 2048;  // taps per block (products staged in smem)
-
-template <bool LTS>
-__global__ void __launch_bounds__(256) interp_kernel(const AmrStageParams P) {
-  __shared__ double2 prod[INTERP_CHUNK];
-  __shared__ double wsm[256];
-  const bool wsmall = P.n_wtab <= 256;
-  if (wsmall)
-    for (int i = threadIdx.x; i < P.n_wtab; i += blockDim.x) wsm[i] = P.wtab[i];
-  __syncthreads();
-  // taps of chunk b live at [b*CHUNK, b*CHUNK + CHUNK), padded with gid -1
-  const int64_t t0 = (int64_t)blockIdx.x * INTERP_CHUNK;
-  const int64_t in0 = __ldg(P.chunk_in + blockIdx.x), in1 = __ldg(P.chunk_in + blockIdx.x + 1);
-  const int lr = LTS ? __ldg(P.chunk_cad + blockIdx.x) : 0;  // a chunk never mixes reader cadences
-  const double2* U0 = reinterpret_cast<const double2*>(P.U0);
-  const double2* U1 = reinterpret_cast<const double2*>(P.U1);
-  const double2* K = reinterpret_cast<const double2*>(P.K);
-  constexpr int ntap = INTERP_CHUNK;
-  // phase A: every tap product in parallel (8 independent taps per thread per batch)
-  constexpr int B = 8;
-  for (int base = threadIdx.x; base < ntap; base += 256 * B) {
-    int g[B];
-    double w[B];
-#pragma unroll
-    for (int u = 0; u < B; ++u) {
-      const int k = base + u * 256;
-      g[u] = __ldg(P.tap_gid + t0 + k);
-      const int wi = __ldg(P.tap_w + t0 + k);
-      w[u] = wsmall ? wsm[wi] : __ldg(P.wtab + wi);
-    }
-#pragma unroll
-    for (int u = 0; u < B; ++u) {
-      if (g[u] < 0) continue;
-      const int ls = LTS ? P.node_cadence[g[u]] : 0;
-      const double2 v = stage_source<LTS>(P, U0, U1, K, P.n_nodes, g[u], P.stage, lr, ls, P.coef);
-      prod[base + u * 256] = make_double2(w[u] * v.x, w[u] * v.y);
-    }
-  }
-  __syncthreads();
-  // phase B: each interpolation node sums its products in CSR order from 0
-  double2* yh = reinterpret_cast<double2*>(P.yh);
-  for (int64_t i = in0 + threadIdx.x; i < in1; i += 256) {
-    const int a = (int)(__ldg(P.in_tap + 2 * i) - t0), e = (int)(__ldg(P.in_tap + 2 * i + 1) - t0);
-    double sx = 0.0, sy = 0.0;
-    for (int k = a; k < e; ++k) {
-      const double2 q = prod[k];
-      sx = sx + q.x;
-      sy = sy + q.y;
-    }
-    yh[i] = make_double2(sx, sy);
-  }
-}
-
-// --------------------------------------------------------------------------
 // the stage kernel: one CTA per leaf tile.  Tables are stored in launch
 // (tile) order, so the table load does not wait for the tile's leaf id.
 // --------------------------------------------------------------------------
@@ -448,13 +389,16 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, 3)
     stage_kernel(const AmrStageParams P) {
   using T = Tile<DIM, PPO>;
   constexpr int EPT = (T::NE + T::THREADS - 1) / T::THREADS;
+  constexpr int SPT = 2;  // slots per thread issued with the table gathers
   constexpr int NK = NT > 0 ? NT : 1;
   __shared__ double2 sv[T::NS];
   __shared__ short s_own[T::NI];
+  __shared__ double s_w[256];
+  extern __shared__ double2 slotv[];  // [max_slots] stage sources of the tile's tap nodes
   const int64_t tile = blockIdx.x;
   const int32_t* __restrict__ tab = P.tile_table + tile * T::NE;
   const uint8_t* __restrict__ side = LTS ? P.tile_src_cad + tile * T::NE : nullptr;
-  // phase 1a: table entries (independent of the leaf-id load below)
+  // phase 1a: table entries and the tile's slot range (independent of the leaf id)
   int ent[EPT];
   uint8_t sc[EPT];
 #pragma unroll
@@ -463,6 +407,19 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, 3)
     ent[i] = (e < T::NE) ? __ldg(tab + e) : -1;
     sc[i] = (LTS && e < T::NE) ? __ldg(side + e) : 0;
   }
+  const int64_t sl0 = __ldg(P.tile_slot_ptr + tile), sl1 = __ldg(P.tile_slot_ptr + tile + 1);
+  const int nslot = (int)(sl1 - sl0);
+  int sg[SPT];
+  uint8_t scs[SPT];
+#pragma unroll
+  for (int i = 0; i < SPT; ++i) {
+    const int k = threadIdx.x + i * T::THREADS;
+    sg[i] = k < nslot ? __ldg(P.slot_gid + sl0 + k) : -1;
+    scs[i] = (LTS && k < nslot) ? __ldg(P.slot_cad + sl0 + k) : 0;
+  }
+  const bool wsmall = P.n_wtab <= 256;
+  if (wsmall)
+    for (int i = threadIdx.x; i < P.n_wtab; i += T::THREADS) s_w[i] = P.wtab[i];
   const int leaf = P.tile_ids[tile];
   const int64_t g0 = P.leaf_start[leaf];
   const int64_t g1 = P.leaf_start[leaf + 1];
@@ -474,7 +431,6 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, 3)
   const double2* U0 = reinterpret_cast<const double2*>(P.U0);
   const double2* U1 = reinterpret_cast<const double2*>(P.U1);
   const double2* K = reinterpret_cast<const double2*>(P.K);
-  const double2* YH = reinterpret_cast<const double2*>(P.yh);
   const AmrSliceCoef* C = P.coef;
   int js[NK];
   double cs[NK];
@@ -487,28 +443,36 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, 3)
   const double2* Ucur = cur ? U1 : U0;
 
   // phase 1b: every data load of this thread in flight at once
-  uint32_t fast = 0;
-  double2 uv[EPT], kv[EPT][NK];
+  uint32_t fast = 0, sfast = 0;
+  double2 uv[EPT], kv[EPT][NK], su[SPT], sk[SPT][NK];
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
     bool f = ent[i] >= 0;
     if (LTS && f) f = C->mode[cad][sc[i]] == 0;
     fast |= (uint32_t)f << i;
-    uv[i] = make_double2(0.0, 0.0);
     if (f) {
       uv[i] = ld2(Ucur + ent[i]);
 #pragma unroll
       for (int t = 0; t < NT; ++t) kv[i][t] = ld2(K + (int64_t)js[t] * n + ent[i]);
-    } else if (ent[i] <= -2) {
-      uv[i] = ld2(YH + (-ent[i] - 2));
     }
   }
-  // phase 1c: stage inputs -> smem
+#pragma unroll
+  for (int i = 0; i < SPT; ++i) {
+    bool f = sg[i] >= 0;
+    if (LTS && f) f = C->mode[cad][scs[i]] == 0;
+    sfast |= (uint32_t)f << i;
+    if (f) {
+      su[i] = ld2(Ucur + sg[i]);
+#pragma unroll
+      for (int t = 0; t < NT; ++t) sk[i][t] = ld2(K + (int64_t)js[t] * n + sg[i]);
+    }
+  }
+  // phase 1c: copy entries -> stencil input (0 + 1.0*src), slots -> their stage source
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
     const int e = threadIdx.x + i * T::THREADS;
-    if (e >= T::NE) continue;
-    double2 y = uv[i];  // zero row or precomputed interpolation node
+    if (e >= T::NE || ent[i] <= -2) continue;  // interpolation nodes are written in phase 1d
+    double2 y = make_double2(0.0, 0.0);
     if (fast >> i & 1) {
       y = make_double2(0.0 + uv[i].x, 0.0 + uv[i].y);
 #pragma unroll
@@ -516,13 +480,63 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, 3)
         y.x = y.x + cs[t] * kv[i][t].x;
         y.y = y.y + cs[t] * kv[i][t].y;
       }
-      y = make_double2(0.0 + y.x, 0.0 + y.y);  // copy row: 0 + 1.0 * src
+      y = make_double2(0.0 + y.x, 0.0 + y.y);
     } else if (LTS && ent[i] >= 0) {
       const double2 v = iface_source(U0, U1, K, n, p, ent[i], s, cad, sc[i], C);
       y = make_double2(0.0 + v.x, 0.0 + v.y);
     }
     if (e < T::NI && ent[i] >= g0 && ent[i] < g1) s_own[ent[i] - g0] = (short)e;
     sv[cross_cell<DIM, PPO>(e)] = y;
+  }
+#pragma unroll
+  for (int i = 0; i < SPT; ++i) {
+    if (sg[i] < 0) continue;
+    double2 y;
+    if (sfast >> i & 1) {
+      y = make_double2(0.0 + su[i].x, 0.0 + su[i].y);
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        y.x = y.x + cs[t] * sk[i][t].x;
+        y.y = y.y + cs[t] * sk[i][t].y;
+      }
+    } else {
+      y = iface_source(U0, U1, K, n, p, sg[i], s, cad, scs[i], C);
+    }
+    slotv[threadIdx.x + i * T::THREADS] = y;
+  }
+  // slots beyond SPT*THREADS (very large interface tiles)
+  for (int k = threadIdx.x + SPT * T::THREADS; k < nslot; k += T::THREADS) {
+    const int g = __ldg(P.slot_gid + sl0 + k);
+    if (LTS) {
+      slotv[k] = iface_source(U0, U1, K, n, p, g, s, cad, __ldg(P.slot_cad + sl0 + k), C);
+    } else {
+      const double2 u = ld2(Ucur + g);
+      double2 y = make_double2(0.0 + u.x, 0.0 + u.y);
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const double2 kk = ld2(K + (int64_t)js[t] * n + g);
+        y.x = y.x + cs[t] * kk.x;
+        y.y = y.y + cs[t] * kk.y;
+      }
+      slotv[k] = y;
+    }
+  }
+  __syncthreads();
+  // phase 1d: hanging rows: 0 + sum_k w_k src(g_k), ascending gid (mesh.py:316-351, 418)
+  {
+    const int64_t j0 = __ldg(P.tile_in_ptr + tile), j1 = __ldg(P.tile_in_ptr + tile + 1);
+    for (int64_t j = j0 + threadIdx.x; j < j1; j += T::THREADS) {
+      const int64_t k0 = __ldg(P.in_tap_ptr + j), k1 = __ldg(P.in_tap_ptr + j + 1);
+      double ax = 0.0, ay = 0.0;
+      for (int64_t k = k0; k < k1; ++k) {
+        const uint32_t tp = __ldg(P.tap + k);
+        const double w = wsmall ? s_w[tp & 0xFFFF] : __ldg(P.wtab + (tp & 0xFFFF));
+        const double2 v = slotv[tp >> 16];
+        ax = ax + w * v.x;
+        ay = ay + w * v.y;
+      }
+      sv[cross_cell<DIM, PPO>(__ldg(P.in_entry + j))] = make_double2(ax, ay);
+    }
   }
   __syncthreads();
 
@@ -683,7 +697,15 @@ int sm_count() {
 template <int DIM, int PPO, bool LTS, int NT>
 int launch_stage_one(const AmrStageParams* p, cudaStream_t st) {
   using T = Tile<DIM, PPO>;
-  stage_kernel<DIM, PPO, LTS, NT><<<(unsigned)p->n_tiles, T::THREADS, 0, st>>>(*p);
+  const size_t dyn = sizeof(double2) * (size_t)(p->max_slots > 0 ? p->max_slots : 1);
+  static size_t configured = 0;
+  if (dyn > configured) {
+    cudaError_t e = cudaFuncSetAttribute(stage_kernel<DIM, PPO, LTS, NT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(stage_kernel)");
+    configured = dyn;
+  }
+  stage_kernel<DIM, PPO, LTS, NT><<<(unsigned)p->n_tiles, T::THREADS, dyn, st>>>(*p);
   return AMR_OK;
 }
 
@@ -724,17 +746,6 @@ extern "C" int amr_stage(const AmrStageParams* p, void* stream) {
   }
   amr_set_error_internal("amr_stage: unsupported (dim, ppo)");
   return AMR_EINVAL;
-}
-
-extern "C" int amr_interp(const AmrStageParams* p, void* stream) {
-  if (p->n_chunks <= 0) return AMR_OK;
-  const unsigned grid = (unsigned)p->n_chunks;
-  if (p->lts)
-    interp_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(*p);
-  else
-    interp_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(*p);
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? AMR_OK : cuda_fail(e, "amr_interp launch");
 }
 
 extern "C" int amr_gather_rows(int64_t n_rows, const int64_t* row_ptr, const int64_t* col, const double* val,

@@ -230,11 +230,7 @@ class Engine:
         tiles = mine[order].astype(np.int32)
         tcad = leaf_cad[tiles]
         self._prefix = {c: int(np.sum(tcad >= c)) for c in range(self.l_max + 1)}
-        table, in_row, in_cad = self._interp_nodes(td["table"], tiles, leaf_cad)
-        ip = self._interp_program(td, in_row, in_cad)
-        ccad = ip["chunk_cad"][: ip["n_chunks"]]
-        self._chunk_prefix = {c: int(np.sum(ccad >= c)) for c in range(self.l_max + 1)}
-        table = table[tiles]  # launch (tile) order
+        table, prog = self._tile_programs(td, tiles, node_cad)
         lts_kernel = mode == "lts" or any(c != self.l_max for c in cadence)
         if lts_kernel:
             side = np.zeros(table.shape, dtype=np.uint8)
@@ -244,13 +240,10 @@ class Engine:
             side = np.zeros(1, dtype=np.uint8)
         dev = self.device
         T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
-        self._d = dict(tiles=T(tiles), table=T(table), iptr=T(td["interp_ptr"]), igid=T(td["interp_gid"]),
-                       iw=T(td["interp_w"]), anchor=T(td["anchor3"]), level=T(td["level"]), cadence=T(leaf_cad),
-                       starts=T(td["starts"]), node_cad=T(node_cad), side=T(side),
-                       chunk_in=T(ip["chunk_in"]), chunk_cad=T(ip["chunk_cad"]), in_tap=T(ip["in_tap"]),
-                       in_cad=T(in_cad if len(in_cad) else np.zeros(1, np.int32)),
-                       tap_gid=T(ip["tap_gid"]), tap_w=T(ip["tap_w"]), wtab=T(ip["wtab"]))
-        self._yh = torch.zeros((max(len(in_row), 1), 2), dtype=torch.float64, device=dev)
+        self._d = dict(tiles=T(tiles), table=T(table), anchor=T(td["anchor3"]), level=T(td["level"]),
+                       cadence=T(leaf_cad), starts=T(td["starts"]), node_cad=T(node_cad), side=T(side),
+                       **{k: T(v) for k, v in prog.items() if k != "max_slots"})
+        self._max_slots = prog["max_slots"]
         n = mesh.n_nodes
         self._U = [torch.zeros((n, 2), dtype=torch.float64, device=dev) for _ in range(2)]
         self._K = torch.zeros((self.p, n, 2), dtype=torch.float64, device=dev)
@@ -278,89 +271,73 @@ class Engine:
         return cadence
 
     @staticmethod
-    def _interp_nodes(table: np.ndarray, tiles: np.ndarray, leaf_cad: np.ndarray):
-        """Deduplicate hanging-point rows into interpolation nodes, one per (row,
-        reader cadence), ordered by cadence (finest first) so that the nodes of
-        the eligible readers of any slice are a prefix; remap the table."""
-        table = table.copy()
-        sub = table[tiles]
-        hang = sub <= -2
-        if not hang.any():
-            return table, np.zeros(0, np.int32), np.zeros(0, np.int32)
-        rows = (-sub[hang] - 2).astype(np.int64)
-        cads = np.broadcast_to(leaf_cad[tiles][:, None], sub.shape)[hang].astype(np.int64)
-        key = (31 - cads) * (1 << 32) + rows
-        uniq, inv = np.unique(key, return_inverse=True)
-        in_cad = (31 - (uniq >> 32)).astype(np.int32)
-        in_row = (uniq & 0xFFFFFFFF).astype(np.int32)
-        sub[hang] = (-(inv + 2)).astype(np.int32)
-        table[tiles] = sub
-        return table, in_row, in_cad
+    def _tile_programs(td: dict, tiles: np.ndarray, node_cad: np.ndarray):
+        """Tile tables in launch order plus each tile's interpolation program.
 
-    CHUNK = 2048  # taps per interpolation CTA (INTERP_CHUNK in amr_kernels.cu)
-
-    @classmethod
-    def _interp_program(cls, td: dict, in_row: np.ndarray, in_cad: np.ndarray) -> dict:
-        """Flatten the interpolation nodes' taps (CSR order, 16-bit weight ids)
-        into CTA chunks of CHUNK taps: chunk b occupies [b*CHUNK, (b+1)*CHUNK)
-        (padded with gid -1), never splits a node and never mixes reader
-        cadences, so a CTA finds its taps without a dependent lookup."""
+        A tile's hanging points (table entries <= -2, one interpolation row
+        each) become its own interpolation nodes, numbered tile-locally in
+        the table.  Their taps refer to a per-tile set of unique source nodes
+        ("slots") that the kernel gathers once into shared memory; taps keep
+        the row's CSR (ascending gid) order and a 16-bit weight id."""
+        table = td["table"][tiles].copy()
         ptr, gid, w = td["interp_ptr"], td["interp_gid"], td["interp_w"]
-        n_in = len(in_row)
-        counts = (ptr[in_row + 1] - ptr[in_row]).astype(np.int64) if n_in else np.zeros(0, np.int64)
-        if n_in and counts.max() > cls.CHUNK:
-            raise ValueError("interpolation row longer than one chunk")
-        chunk_of = np.empty(n_in, dtype=np.int64)
-        pos_in_chunk = np.empty(n_in, dtype=np.int64)
-        cads32 = np.ascontiguousarray(in_cad, dtype=np.int32)
-        n_chunks = int(_native.lib().amr_pack_chunks(n_in, _native.ptr(np.ascontiguousarray(counts), C.c_int64),
-                                                      _native.ptr(cads32, C.c_int32), cls.CHUNK,
-                                                      _native.ptr(chunk_of, C.c_int64),
-                                                      _native.ptr(pos_in_chunk, C.c_int64)))
-        if n_chunks < 0:
-            raise ValueError(_native.last_error())
-        first = np.ones(n_in, dtype=bool)
-        first[1:] = chunk_of[1:] != chunk_of[:-1]
-        bounds = np.concatenate([np.nonzero(first)[0], [n_in]]).tolist() if n_in else [0]
-        cads = cads32[first].tolist() if n_in else []
-        start = chunk_of * cls.CHUNK + pos_in_chunk
-        in_tap = np.stack([start, start + counts], axis=1).reshape(-1) if n_in else np.zeros(2, np.int64)
-        tap_gid = np.full(max(n_chunks, 1) * cls.CHUNK, -1, dtype=np.int32)
-        tap_w = np.zeros(max(n_chunks, 1) * cls.CHUNK, dtype=np.uint16)
-        wtab = np.zeros(1)
-        if n_in:
-            src_idx = np.repeat(ptr[in_row], counts) + (np.arange(counts.sum()) - np.repeat(np.cumsum(counts) - counts, counts))
-            dst_idx = np.repeat(start, counts) + (np.arange(counts.sum()) - np.repeat(np.cumsum(counts) - counts, counts))
-            wtab, widx = np.unique(w[src_idx], return_inverse=True)
-            if len(wtab) > 65535:
-                raise ValueError("more than 65535 distinct interpolation weights")
-            tap_gid[dst_idx] = gid[src_idx]
-            tap_w[dst_idx] = widx.astype(np.uint16)
-        return dict(in_tap=in_tap.astype(np.int64), tap_gid=tap_gid, tap_w=tap_w, wtab=wtab.astype(np.float64),
-                    chunk_in=np.array(bounds if n_in else [0, 0], dtype=np.int64),
-                    chunk_cad=np.array(cads if n_in else [0], dtype=np.int32), n_chunks=n_chunks if n_in else 0)
+        nt, E = table.shape
+        t_idx, e_idx = np.nonzero(table <= -2)  # row-major: by tile, then entry
+        rows = (-table[t_idx, e_idx] - 2).astype(np.int64)
+        n_in = len(rows)
+        tile_in_ptr = np.zeros(nt + 1, dtype=np.int64)
+        np.cumsum(np.bincount(t_idx, minlength=nt), out=tile_in_ptr[1:])
+        local_in = np.arange(n_in) - tile_in_ptr[t_idx]
+        table[t_idx, e_idx] = (-(local_in + 2)).astype(np.int32)
+        counts = (ptr[rows + 1] - ptr[rows]).astype(np.int64)
+        in_tap_ptr = np.zeros(n_in + 1, dtype=np.int64)
+        np.cumsum(counts, out=in_tap_ptr[1:])
+        n_taps = int(in_tap_ptr[-1])
+        within = np.arange(n_taps) - np.repeat(in_tap_ptr[:-1], counts)
+        src_idx = np.repeat(ptr[rows], counts) + within
+        tap_gid = gid[src_idx].astype(np.int64)
+        tap_tile = np.repeat(t_idx.astype(np.int64), counts)
+        key, inv = np.unique((tap_tile << 32) | tap_gid, return_inverse=True) if n_taps else \
+            (np.zeros(0, np.int64), np.zeros(0, np.int64))
+        slot_tile = key >> 32
+        tile_slot_ptr = np.zeros(nt + 1, dtype=np.int64)
+        np.cumsum(np.bincount(slot_tile, minlength=nt), out=tile_slot_ptr[1:])
+        local_slot = inv - tile_slot_ptr[tap_tile]
+        max_slots = int(np.diff(tile_slot_ptr).max()) if nt else 0
+        if max_slots >= 1 << 16:
+            raise ValueError("more than 65535 interpolation sources in one tile")
+        wtab, widx = np.unique(w[src_idx], return_inverse=True) if n_taps else (np.zeros(1), np.zeros(0, np.int64))
+        if len(wtab) > 1 << 16:
+            raise ValueError("more than 65536 distinct interpolation weights")
+        slot_gid = (key & 0xFFFFFFFF).astype(np.int32)
+        pad = lambda a, dt: a.astype(dt) if len(a) else np.zeros(1, dt)  # noqa: E731
+        prog = dict(tile_slot_ptr=tile_slot_ptr, slot_gid=pad(slot_gid, np.int32),
+                    slot_cad=pad(node_cad[slot_gid] if len(slot_gid) else slot_gid, np.uint8),
+                    tile_in_ptr=tile_in_ptr, in_tap_ptr=in_tap_ptr, in_entry=pad(e_idx, np.uint16),
+                    tap=pad((local_slot << 16) | widx, np.uint32), wtab=wtab.astype(np.float64),
+                    max_slots=max_slots)
+        return table, prog
 
     def _make_params(self) -> _native.AmrStageParams:
         m = self.mesh
         P = _native.AmrStageParams()
         P.dim, P.ppo, P.pad = m.dim, m.ppo, m.pad
         P.lts = 1 if self.mode == "lts" or any(c != self.l_max for c in self.cadence) else 0
-        P.n_chunks = 0
         P.n_stages = self.p
         P.nonlinear = self._nl
         P.n_nodes = m.n_nodes
         d = self._d
         P.tile_ids, P.tile_table = d["tiles"].data_ptr(), d["table"].data_ptr()
-        P.interp_ptr, P.interp_gid, P.interp_w = d["iptr"].data_ptr(), d["igid"].data_ptr(), d["iw"].data_ptr()
         P.leaf_anchor, P.leaf_level = d["anchor"].data_ptr(), d["level"].data_ptr()
         P.leaf_cadence, P.leaf_start = d["cadence"].data_ptr(), d["starts"].data_ptr()
         P.node_cadence = d["node_cad"].data_ptr()
         P.tile_src_cad = d["side"].data_ptr()
-        P.chunk_in, P.in_tap, P.in_cad = d["chunk_in"].data_ptr(), d["in_tap"].data_ptr(), d["in_cad"].data_ptr()
-        P.chunk_cad = d["chunk_cad"].data_ptr()
-        P.tap_gid, P.tap_w, P.wtab = d["tap_gid"].data_ptr(), d["tap_w"].data_ptr(), d["wtab"].data_ptr()
-        P.n_wtab = int(d["wtab"].numel())
-        P.yh = self._yh.data_ptr()
+        P.tile_slot_ptr, P.slot_gid, P.slot_cad = (d["tile_slot_ptr"].data_ptr(), d["slot_gid"].data_ptr(),
+                                                   d["slot_cad"].data_ptr())
+        P.tile_in_ptr, P.in_tap_ptr, P.in_entry = (d["tile_in_ptr"].data_ptr(), d["in_tap_ptr"].data_ptr(),
+                                                   d["in_entry"].data_ptr())
+        P.tap, P.wtab, P.n_wtab = d["tap"].data_ptr(), d["wtab"].data_ptr(), int(d["wtab"].numel())
+        P.max_slots = self._max_slots
         P.U0, P.U1, P.K = self._U[0].data_ptr(), self._U[1].data_ptr(), self._K.data_ptr()
         for s in range(self.p):
             for j in range(self.p):
@@ -532,7 +509,7 @@ class Engine:
         n_tiles = self._prefix[min(elig)] if elig else 0
         P = self._prm
         P.n_tiles = n_tiles
-        P.n_chunks = self._chunk_prefix[min(elig)] if elig else 0
+
         if P.lts:
             P.coef = self._slice_coef(i).data_ptr()
         else:
@@ -546,9 +523,6 @@ class Engine:
             for t, j in enumerate(vt):
                 P.vt_j[t] = j
             if n_tiles:
-                rc = self._lib.amr_interp(C.byref(P), stream)
-                if rc:
-                    _native.check(rc, "amr_interp")
                 rc = self._lib.amr_stage(C.byref(P), stream)
                 if rc:
                     _native.check(rc, "amr_stage")
@@ -579,7 +553,7 @@ class Engine:
             self.advance_slice()
 
     def launches_per_slice(self, i: int) -> int:
-        return 2 * self.p if self._eligible_cadences(i) else 0
+        return self.p if self._eligible_cadences(i) else 0
 
     def close(self):
         self._exchange = None
