@@ -384,6 +384,8 @@ __device__ __noinline__ double2 iface_source(const double2* __restrict__ U0, con
   return lts_source(U0, U1, K, n, p, g, s, lr, ls, C);
 }
 
+constexpr int PROD_CHUNK = 1024;  // tap products staged per pass (16 KB)
+
 template <int DIM, int PPO, bool LTS, int NT>
 __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, 3)
     stage_kernel(const AmrStageParams P) {
@@ -394,7 +396,9 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, 3)
   __shared__ double2 sv[T::NS];
   __shared__ short s_own[T::NI];
   __shared__ double s_w[256];
-  extern __shared__ double2 slotv[];  // [max_slots] stage sources of the tile's tap nodes
+  extern __shared__ double2 dyn_smem[];  // [PROD_CHUNK] tap products, then [max_slots] slot sources
+  double2* prod = dyn_smem;
+  double2* slotv = dyn_smem + PROD_CHUNK;
   const int64_t tile = blockIdx.x;
   const int32_t* __restrict__ tab = P.tile_table + tile * T::NE;
   const uint8_t* __restrict__ side = LTS ? P.tile_src_cad + tile * T::NE : nullptr;
@@ -522,20 +526,64 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, 3)
     }
   }
   __syncthreads();
-  // phase 1d: hanging rows: 0 + sum_k w_k src(g_k), ascending gid (mesh.py:316-351, 418)
+  // phase 1d: hanging rows, y = 0 + sum_k w_k src(g_k) in ascending-gid order
+  // (mesh.py:316-351, scipy csr_matvecs at mesh.py:418).  Taps are processed in
+  // chunks: all threads form the products w_k*src(g_k) in parallel (each
+  // rounded once, as numpy does) into smem, then each row's owner thread
+  // continues its running sum over the chunk in tap order.
   {
+    constexpr int IPT = 3;  // rows per thread held in registers (more: second pass)
     const int64_t j0 = __ldg(P.tile_in_ptr + tile), j1 = __ldg(P.tile_in_ptr + tile + 1);
-    for (int64_t j = j0 + threadIdx.x; j < j1; j += T::THREADS) {
-      const int64_t k0 = __ldg(P.in_tap_ptr + j), k1 = __ldg(P.in_tap_ptr + j + 1);
-      double ax = 0.0, ay = 0.0;
-      for (int64_t k = k0; k < k1; ++k) {
-        const uint32_t tp = __ldg(P.tap + k);
-        const double w = wsmall ? s_w[tp & 0xFFFF] : __ldg(P.wtab + (tp & 0xFFFF));
-        const double2 v = slotv[tp >> 16];
-        ax = ax + w * v.x;
-        ay = ay + w * v.y;
+    const int nin = (int)(j1 - j0);
+    if (nin > 0) {
+      const int64_t tap0 = __ldg(P.in_tap_ptr + j0), tap1 = __ldg(P.in_tap_ptr + j1);
+      double2 acc[IPT];
+      int64_t ka[IPT], kb[IPT];
+#pragma unroll
+      for (int r = 0; r < IPT; ++r) {
+        const int li = threadIdx.x + r * T::THREADS;
+        acc[r] = make_double2(0.0, 0.0);
+        ka[r] = li < nin ? __ldg(P.in_tap_ptr + j0 + li) : 0;
+        kb[r] = li < nin ? __ldg(P.in_tap_ptr + j0 + li + 1) : 0;
       }
-      sv[cross_cell<DIM, PPO>(__ldg(P.in_entry + j))] = make_double2(ax, ay);
+      for (int64_t c0 = tap0; c0 < tap1; c0 += PROD_CHUNK) {
+        const int cn = (int)min((int64_t)PROD_CHUNK, tap1 - c0);
+        for (int k = threadIdx.x; k < cn; k += T::THREADS) {
+          const uint32_t tp = __ldg(P.tap + c0 + k);
+          const double w = wsmall ? s_w[tp & 0xFFFF] : __ldg(P.wtab + (tp & 0xFFFF));
+          const double2 v = slotv[tp >> 16];
+          prod[k] = make_double2(w * v.x, w * v.y);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < IPT; ++r) {
+          const int64_t lo = max(ka[r], c0), hi = min(kb[r], c0 + cn);
+          for (int64_t k = lo; k < hi; ++k) {
+            const double2 q = prod[k - c0];
+            acc[r].x = acc[r].x + q.x;
+            acc[r].y = acc[r].y + q.y;
+          }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int r = 0; r < IPT; ++r) {
+        const int li = threadIdx.x + r * T::THREADS;
+        if (li < nin) sv[cross_cell<DIM, PPO>(__ldg(P.in_entry + j0 + li))] = acc[r];
+      }
+      // rows beyond IPT*THREADS (not seen in the BASELINE meshes): direct sums
+      for (int li = threadIdx.x + IPT * T::THREADS; li < nin; li += T::THREADS) {
+        const int64_t k0 = __ldg(P.in_tap_ptr + j0 + li), k1 = __ldg(P.in_tap_ptr + j0 + li + 1);
+        double ax = 0.0, ay = 0.0;
+        for (int64_t k = k0; k < k1; ++k) {
+          const uint32_t tp = __ldg(P.tap + k);
+          const double w = wsmall ? s_w[tp & 0xFFFF] : __ldg(P.wtab + (tp & 0xFFFF));
+          const double2 v = slotv[tp >> 16];
+          ax = ax + w * v.x;
+          ay = ay + w * v.y;
+        }
+        sv[cross_cell<DIM, PPO>(__ldg(P.in_entry + j0 + li))] = make_double2(ax, ay);
+      }
     }
   }
   __syncthreads();
@@ -697,7 +745,7 @@ int sm_count() {
 template <int DIM, int PPO, bool LTS, int NT>
 int launch_stage_one(const AmrStageParams* p, cudaStream_t st) {
   using T = Tile<DIM, PPO>;
-  const size_t dyn = sizeof(double2) * (size_t)(p->max_slots > 0 ? p->max_slots : 1);
+  const size_t dyn = sizeof(double2) * (size_t)(PROD_CHUNK + (p->max_slots > 0 ? p->max_slots : 1));
   static size_t configured = 0;
   if (dyn > configured) {
     cudaError_t e = cudaFuncSetAttribute(stage_kernel<DIM, PPO, LTS, NT>,
