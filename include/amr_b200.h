@@ -143,6 +143,7 @@ typedef struct {
   const uint8_t* slot_cad;     /* cadence of the slot's source leaf (LTS) */
   const int64_t* tile_in_ptr;  /* [n_tiles+1] interpolation nodes of tile t */
   const int64_t* in_tap_ptr;   /* [n_in+1] taps of node j, CSR (ascending gid) order */
+  const int64_t* tile_tap_ptr; /* [n_tiles+1] taps of tile t (= in_tap_ptr[tile_in_ptr[t]]) */
   const uint16_t* in_entry;    /* [n_in] cross entry the node fills */
   const uint32_t* tap;         /* [n_taps] (tile-local slot << 16) | weight id */
   const double* wtab;          /* distinct interpolation weights */

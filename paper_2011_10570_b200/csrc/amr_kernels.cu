@@ -412,6 +412,16 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, 3)
     sc[i] = (LTS && e < T::NE) ? __ldg(side + e) : 0;
   }
   const int64_t sl0 = __ldg(P.tile_slot_ptr + tile), sl1 = __ldg(P.tile_slot_ptr + tile + 1);
+  const int64_t j0 = __ldg(P.tile_in_ptr + tile), j1 = __ldg(P.tile_in_ptr + tile + 1);
+  const int64_t tap0 = __ldg(P.tile_tap_ptr + tile), tap1 = __ldg(P.tile_tap_ptr + tile + 1);
+  const int nin = (int)(j1 - j0);
+  constexpr int TPT = PROD_CHUNK / T::THREADS;
+  uint32_t tw[TPT];  // tap words of the current chunk
+#pragma unroll
+  for (int u = 0; u < TPT; ++u) {
+    const int64_t k = tap0 + threadIdx.x + u * T::THREADS;
+    tw[u] = k < tap1 ? __ldg(P.tap + k) : 0u;
+  }
   const int nslot = (int)(sl1 - sl0);
   int sg[SPT];
   uint8_t scs[SPT];
@@ -530,60 +540,70 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, 3)
   // (mesh.py:316-351, scipy csr_matvecs at mesh.py:418).  Taps are processed in
   // chunks: all threads form the products w_k*src(g_k) in parallel (each
   // rounded once, as numpy does) into smem, then each row's owner thread
-  // continues its running sum over the chunk in tap order.
-  {
-    constexpr int IPT = 3;  // rows per thread held in registers (more: second pass)
-    const int64_t j0 = __ldg(P.tile_in_ptr + tile), j1 = __ldg(P.tile_in_ptr + tile + 1);
-    const int nin = (int)(j1 - j0);
-    if (nin > 0) {
-      const int64_t tap0 = __ldg(P.in_tap_ptr + j0), tap1 = __ldg(P.in_tap_ptr + j1);
-      double2 acc[IPT];
-      int64_t ka[IPT], kb[IPT];
+  // continues its running sum over the chunk in tap order.  The tap words of
+  // the next chunk are loaded while the current chunk is summed.
+  if (nin > 0) {
+    constexpr int IPT = 3;  // rows per thread held in registers (more: direct pass)
+    double2 acc[IPT];
+    int ka[IPT], kb[IPT];  // row tap ranges relative to tap0
 #pragma unroll
-      for (int r = 0; r < IPT; ++r) {
-        const int li = threadIdx.x + r * T::THREADS;
-        acc[r] = make_double2(0.0, 0.0);
-        ka[r] = li < nin ? __ldg(P.in_tap_ptr + j0 + li) : 0;
-        kb[r] = li < nin ? __ldg(P.in_tap_ptr + j0 + li + 1) : 0;
-      }
-      for (int64_t c0 = tap0; c0 < tap1; c0 += PROD_CHUNK) {
-        const int cn = (int)min((int64_t)PROD_CHUNK, tap1 - c0);
-        for (int k = threadIdx.x; k < cn; k += T::THREADS) {
-          const uint32_t tp = __ldg(P.tap + c0 + k);
+    for (int r = 0; r < IPT; ++r) {
+      const int li = threadIdx.x + r * T::THREADS;
+      acc[r] = make_double2(0.0, 0.0);
+      ka[r] = li < nin ? (int)(__ldg(P.in_tap_ptr + j0 + li) - tap0) : 0;
+      kb[r] = li < nin ? (int)(__ldg(P.in_tap_ptr + j0 + li + 1) - tap0) : 0;
+    }
+    const int ntap = (int)(tap1 - tap0);
+    for (int c0 = 0; c0 < ntap; c0 += PROD_CHUNK) {
+      const int cn = min(PROD_CHUNK, ntap - c0);
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) {
+        const int k = threadIdx.x + u * T::THREADS;
+        if (k < cn) {
+          const uint32_t tp = tw[u];
           const double w = wsmall ? s_w[tp & 0xFFFF] : __ldg(P.wtab + (tp & 0xFFFF));
           const double2 v = slotv[tp >> 16];
           prod[k] = make_double2(w * v.x, w * v.y);
         }
-        __syncthreads();
+      }
+      __syncthreads();
+      // prefetch the next chunk's tap words (in flight during the sums)
+      const int nc0 = c0 + PROD_CHUNK;
 #pragma unroll
-        for (int r = 0; r < IPT; ++r) {
-          const int64_t lo = max(ka[r], c0), hi = min(kb[r], c0 + cn);
-          for (int64_t k = lo; k < hi; ++k) {
-            const double2 q = prod[k - c0];
-            acc[r].x = acc[r].x + q.x;
-            acc[r].y = acc[r].y + q.y;
-          }
-        }
-        __syncthreads();
+      for (int u = 0; u < TPT; ++u) {
+        const int k = nc0 + threadIdx.x + u * T::THREADS;
+        tw[u] = k < ntap ? __ldg(P.tap + tap0 + k) : 0u;
       }
 #pragma unroll
       for (int r = 0; r < IPT; ++r) {
-        const int li = threadIdx.x + r * T::THREADS;
-        if (li < nin) sv[cross_cell<DIM, PPO>(__ldg(P.in_entry + j0 + li))] = acc[r];
-      }
-      // rows beyond IPT*THREADS (not seen in the BASELINE meshes): direct sums
-      for (int li = threadIdx.x + IPT * T::THREADS; li < nin; li += T::THREADS) {
-        const int64_t k0 = __ldg(P.in_tap_ptr + j0 + li), k1 = __ldg(P.in_tap_ptr + j0 + li + 1);
-        double ax = 0.0, ay = 0.0;
-        for (int64_t k = k0; k < k1; ++k) {
-          const uint32_t tp = __ldg(P.tap + k);
-          const double w = wsmall ? s_w[tp & 0xFFFF] : __ldg(P.wtab + (tp & 0xFFFF));
-          const double2 v = slotv[tp >> 16];
-          ax = ax + w * v.x;
-          ay = ay + w * v.y;
+        const int lo = max(ka[r], c0) - c0, hi = min(kb[r], c0 + cn) - c0;
+        double ax = acc[r].x, ay = acc[r].y;
+        for (int k = lo; k < hi; ++k) {
+          const double2 q = prod[k];
+          ax = ax + q.x;
+          ay = ay + q.y;
         }
-        sv[cross_cell<DIM, PPO>(__ldg(P.in_entry + j0 + li))] = make_double2(ax, ay);
+        acc[r] = make_double2(ax, ay);
       }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) {
+      const int li = threadIdx.x + r * T::THREADS;
+      if (li < nin) sv[cross_cell<DIM, PPO>(__ldg(P.in_entry + j0 + li))] = acc[r];
+    }
+    // rows beyond IPT*THREADS (not seen in the BASELINE meshes): direct sums
+    for (int li = threadIdx.x + IPT * T::THREADS; li < nin; li += T::THREADS) {
+      const int64_t k0 = __ldg(P.in_tap_ptr + j0 + li), k1 = __ldg(P.in_tap_ptr + j0 + li + 1);
+      double ax = 0.0, ay = 0.0;
+      for (int64_t k = k0; k < k1; ++k) {
+        const uint32_t tp = __ldg(P.tap + k);
+        const double w = wsmall ? s_w[tp & 0xFFFF] : __ldg(P.wtab + (tp & 0xFFFF));
+        const double2 v = slotv[tp >> 16];
+        ax = ax + w * v.x;
+        ay = ay + w * v.y;
+      }
+      sv[cross_cell<DIM, PPO>(__ldg(P.in_entry + j0 + li))] = make_double2(ax, ay);
     }
   }
   __syncthreads();
@@ -729,17 +749,6 @@ __global__ void pack_kernel(int64_t n_ranges, const int64_t* __restrict__ start,
   int64_t g = start[lo] + (node - off[lo]);
   if (!unpack) buf[t] = src[g * width + c];
   else const_cast<double*>(src)[g * width + c] = buf[t];
-}
-
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
 }
 
 template <int DIM, int PPO, bool LTS, int NT>

@@ -313,7 +313,8 @@ class Engine:
         pad = lambda a, dt: a.astype(dt) if len(a) else np.zeros(1, dt)  # noqa: E731
         prog = dict(tile_slot_ptr=tile_slot_ptr, slot_gid=pad(slot_gid, np.int32),
                     slot_cad=pad(node_cad[slot_gid] if len(slot_gid) else slot_gid, np.uint8),
-                    tile_in_ptr=tile_in_ptr, in_tap_ptr=in_tap_ptr, in_entry=pad(e_idx, np.uint16),
+                    tile_in_ptr=tile_in_ptr, in_tap_ptr=in_tap_ptr, tile_tap_ptr=in_tap_ptr[tile_in_ptr],
+                    in_entry=pad(e_idx, np.uint16),
                     tap=pad((local_slot << 16) | widx, np.uint32), wtab=wtab.astype(np.float64),
                     max_slots=max_slots)
         return table, prog
@@ -336,6 +337,7 @@ class Engine:
                                                    d["slot_cad"].data_ptr())
         P.tile_in_ptr, P.in_tap_ptr, P.in_entry = (d["tile_in_ptr"].data_ptr(), d["in_tap_ptr"].data_ptr(),
                                                    d["in_entry"].data_ptr())
+        P.tile_tap_ptr = d["tile_tap_ptr"].data_ptr()
         P.tap, P.wtab, P.n_wtab = d["tap"].data_ptr(), d["wtab"].data_ptr(), int(d["wtab"].numel())
         P.max_slots = self._max_slots
         P.U0, P.U1, P.K = self._U[0].data_ptr(), self._U[1].data_ptr(), self._K.data_ptr()
