@@ -31,10 +31,13 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile if stale.  AMR_NVCC_FLAGS adds flags (e.g. -DAMR_MIN_BLOCKS=2
+    for tuning experiments)."""
     if not force and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-shared",
+    extra = os.environ.get("AMR_NVCC_FLAGS", "").split()
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-shared", *extra,
            "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off,-O2",
            "-I", INCLUDE, "-o", LIB + ".tmp",
            *[os.path.join(CSRC, s) for s in SOURCES], "-lgomp"]

@@ -384,10 +384,12 @@ __device__ __noinline__ double2 iface_source(const double2* __restrict__ U0, con
   return lts_source(U0, U1, K, n, p, g, s, lr, ls, C);
 }
 
-constexpr int PROD_CHUNK = 1024;  // tap products staged per pass (16 KB)
+#ifndef AMR_MIN_BLOCKS
+#define AMR_MIN_BLOCKS 3  // resident CTAs per SM the register budget is sized for
+#endif
 
 template <int DIM, int PPO, bool LTS, int NT>
-__global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, 3)
+__global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
     stage_kernel(const AmrStageParams P) {
   using T = Tile<DIM, PPO>;
   constexpr int EPT = (T::NE + T::THREADS - 1) / T::THREADS;
@@ -396,9 +398,7 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, 3)
   __shared__ double2 sv[T::NS];
   __shared__ short s_own[T::NI];
   __shared__ double s_w[256];
-  extern __shared__ double2 dyn_smem[];  // [PROD_CHUNK] tap products, then [max_slots] slot sources
-  double2* prod = dyn_smem;
-  double2* slotv = dyn_smem + PROD_CHUNK;
+  extern __shared__ double2 slotv[];  // [max_slots] stage sources of the tile's tap nodes
   const int64_t tile = blockIdx.x;
   const int32_t* __restrict__ tab = P.tile_table + tile * T::NE;
   const uint8_t* __restrict__ side = LTS ? P.tile_src_cad + tile * T::NE : nullptr;
@@ -413,15 +413,8 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, 3)
   }
   const int64_t sl0 = __ldg(P.tile_slot_ptr + tile), sl1 = __ldg(P.tile_slot_ptr + tile + 1);
   const int64_t j0 = __ldg(P.tile_in_ptr + tile), j1 = __ldg(P.tile_in_ptr + tile + 1);
-  const int64_t tap0 = __ldg(P.tile_tap_ptr + tile), tap1 = __ldg(P.tile_tap_ptr + tile + 1);
   const int nin = (int)(j1 - j0);
-  constexpr int TPT = PROD_CHUNK / T::THREADS;
-  uint32_t tw[TPT];  // tap words of the current chunk
-#pragma unroll
-  for (int u = 0; u < TPT; ++u) {
-    const int64_t k = tap0 + threadIdx.x + u * T::THREADS;
-    tw[u] = k < tap1 ? __ldg(P.tap + k) : 0u;
-  }
+
   const int nslot = (int)(sl1 - sl0);
   int sg[SPT];
   uint8_t scs[SPT];
@@ -537,74 +530,27 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, 3)
   }
   __syncthreads();
   // phase 1d: hanging rows, y = 0 + sum_k w_k src(g_k) in ascending-gid order
-  // (mesh.py:316-351, scipy csr_matvecs at mesh.py:418).  Taps are processed in
-  // chunks: all threads form the products w_k*src(g_k) in parallel (each
-  // rounded once, as numpy does) into smem, then each row's owner thread
-  // continues its running sum over the chunk in tap order.  The tap words of
-  // the next chunk are loaded while the current chunk is summed.
-  if (nin > 0) {
-    constexpr int IPT = 3;  // rows per thread held in registers (more: direct pass)
-    double2 acc[IPT];
-    int ka[IPT], kb[IPT];  // row tap ranges relative to tap0
+  // (mesh.py:316-351, scipy csr_matvecs at mesh.py:418): one thread per row;
+  // tap words are fetched 8 at a time (independent, contiguous) so the
+  // running sum only waits on smem.
+  for (int li = threadIdx.x; li < nin; li += T::THREADS) {
+    const int64_t k0 = __ldg(P.in_tap_ptr + j0 + li), k1 = __ldg(P.in_tap_ptr + j0 + li + 1);
+    double ax = 0.0, ay = 0.0;
+    for (int64_t k = k0; k < k1; k += 8) {
+      uint32_t tp[8];
 #pragma unroll
-    for (int r = 0; r < IPT; ++r) {
-      const int li = threadIdx.x + r * T::THREADS;
-      acc[r] = make_double2(0.0, 0.0);
-      ka[r] = li < nin ? (int)(__ldg(P.in_tap_ptr + j0 + li) - tap0) : 0;
-      kb[r] = li < nin ? (int)(__ldg(P.in_tap_ptr + j0 + li + 1) - tap0) : 0;
-    }
-    const int ntap = (int)(tap1 - tap0);
-    for (int c0 = 0; c0 < ntap; c0 += PROD_CHUNK) {
-      const int cn = min(PROD_CHUNK, ntap - c0);
+      for (int u = 0; u < 8; ++u) tp[u] = (k + u < k1) ? __ldg(P.tap + k + u) : 0u;
 #pragma unroll
-      for (int u = 0; u < TPT; ++u) {
-        const int k = threadIdx.x + u * T::THREADS;
-        if (k < cn) {
-          const uint32_t tp = tw[u];
-          const double w = wsmall ? s_w[tp & 0xFFFF] : __ldg(P.wtab + (tp & 0xFFFF));
-          const double2 v = slotv[tp >> 16];
-          prod[k] = make_double2(w * v.x, w * v.y);
+      for (int u = 0; u < 8; ++u) {
+        if (k + u < k1) {
+          const double w = wsmall ? s_w[tp[u] & 0xFFFF] : __ldg(P.wtab + (tp[u] & 0xFFFF));
+          const double2 v = slotv[tp[u] >> 16];
+          ax = ax + w * v.x;
+          ay = ay + w * v.y;
         }
       }
-      __syncthreads();
-      // prefetch the next chunk's tap words (in flight during the sums)
-      const int nc0 = c0 + PROD_CHUNK;
-#pragma unroll
-      for (int u = 0; u < TPT; ++u) {
-        const int k = nc0 + threadIdx.x + u * T::THREADS;
-        tw[u] = k < ntap ? __ldg(P.tap + tap0 + k) : 0u;
-      }
-#pragma unroll
-      for (int r = 0; r < IPT; ++r) {
-        const int lo = max(ka[r], c0) - c0, hi = min(kb[r], c0 + cn) - c0;
-        double ax = acc[r].x, ay = acc[r].y;
-        for (int k = lo; k < hi; ++k) {
-          const double2 q = prod[k];
-          ax = ax + q.x;
-          ay = ay + q.y;
-        }
-        acc[r] = make_double2(ax, ay);
-      }
-      __syncthreads();
     }
-#pragma unroll
-    for (int r = 0; r < IPT; ++r) {
-      const int li = threadIdx.x + r * T::THREADS;
-      if (li < nin) sv[cross_cell<DIM, PPO>(__ldg(P.in_entry + j0 + li))] = acc[r];
-    }
-    // rows beyond IPT*THREADS (not seen in the BASELINE meshes): direct sums
-    for (int li = threadIdx.x + IPT * T::THREADS; li < nin; li += T::THREADS) {
-      const int64_t k0 = __ldg(P.in_tap_ptr + j0 + li), k1 = __ldg(P.in_tap_ptr + j0 + li + 1);
-      double ax = 0.0, ay = 0.0;
-      for (int64_t k = k0; k < k1; ++k) {
-        const uint32_t tp = __ldg(P.tap + k);
-        const double w = wsmall ? s_w[tp & 0xFFFF] : __ldg(P.wtab + (tp & 0xFFFF));
-        const double2 v = slotv[tp >> 16];
-        ax = ax + w * v.x;
-        ay = ay + w * v.y;
-      }
-      sv[cross_cell<DIM, PPO>(__ldg(P.in_entry + j0 + li))] = make_double2(ax, ay);
-    }
+    sv[cross_cell<DIM, PPO>(__ldg(P.in_entry + j0 + li))] = make_double2(ax, ay);
   }
   __syncthreads();
 
@@ -754,7 +700,7 @@ __global__ void pack_kernel(int64_t n_ranges, const int64_t* __restrict__ start,
 template <int DIM, int PPO, bool LTS, int NT>
 int launch_stage_one(const AmrStageParams* p, cudaStream_t st) {
   using T = Tile<DIM, PPO>;
-  const size_t dyn = sizeof(double2) * (size_t)(PROD_CHUNK + (p->max_slots > 0 ? p->max_slots : 1));
+  const size_t dyn = sizeof(double2) * (size_t)(p->max_slots > 0 ? p->max_slots : 1);
   static size_t configured = 0;
   if (dyn > configured) {
     cudaError_t e = cudaFuncSetAttribute(stage_kernel<DIM, PPO, LTS, NT>,
