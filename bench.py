@@ -47,17 +47,21 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """nvidia-smi clock/throttle sampling (100 ms) for the whole run; samples are
+    attributed to the timed windows by timestamp."""
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
         self.lines = []
+        self.windows = []
 
-    def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
+    def start(self):
+        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -70,10 +74,25 @@ class ClockSampler:
 
     def _read(self):
         for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
+            self.lines.append((time.time(), ln.strip()))
 
-    def __exit__(self, *exc):
+    def window(self):
+        """Context manager marking one timed region."""
+        sampler = self
+
+        class _W:
+            def __enter__(self):
+                self.t0 = time.time()
+                return self
+
+            def __exit__(self, *exc):
+                sampler.windows.append((self.t0, time.time()))
+
+        return _W()
+
+    def stop(self):
         if self.proc is not None:
+            time.sleep(0.25)  # let the last window's samples arrive
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -82,22 +101,39 @@ class ClockSampler:
             self.th.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        sm, mx, reasons, n_all = [], None, set(), 0
+        for t, ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
+            if len(parts) < 9:
+                continue
+            n_all += 1
+            # a sample read at t describes the ~100 ms before it
+            if not any(a - 0.05 <= t <= b + 0.15 for a, b in self.windows):
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[4:8]):
+            for nm, v in zip(self.NAMES, parts[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "samples_total": n_all}
+
+
+def _ncu_traffic():
+    """DRAM bytes per stage launch from the committed ncu capture
+    (profiles/traffic.json, written by tools/ncu_traffic.py from one
+    `ncu --set full` run of tools/profile_stage.py on cfg2)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        return float(d["lts_bytes_per_launch"]), (
+            f"ncu dram__bytes_read+write per LTS stage launch ({d['source']}); "
+            f"algorithmic bytes of the same launches: {d['lts_algorithmic_bytes_per_launch']:.3e}")
+    except Exception:
+        return None, "no committed ncu capture"
 
 
 def build_mesh(cfg_name, ranks, mode):
@@ -188,6 +224,7 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     from paper_2011_10570_b200.stepper import Engine
 
+    clk = ClockSampler(local).start()
     t0 = time.time()
     cfg, mesh = build_mesh(args.config, world, "lts")
     t_mesh = time.time() - t0
@@ -201,7 +238,7 @@ def run_ours(args):
         units, launches = units_per_round(eng)
         for _ in range(args.warmup):
             eng.lts_coarse_step() if mode == "lts" else [eng.gts_step() for _ in range(eng.schedule.slices_per_round)]
-        with ClockSampler(local) as clk:
+        with clk.window():
             if mode == "lts":
                 ms, _ = time_rounds(eng, args.steps, torch, dist)
             else:
@@ -230,7 +267,7 @@ def run_ours(args):
             ms_all, units_all = float(tmax[0]), float(tsum[1])
         else:
             ms_all, units_all = ms, float(units)
-        res[mode] = dict(ms=ms_all, units_per_step=units_all, launches_per_step=launches, clocks=clk.summary())
+        res[mode] = dict(ms=ms_all, units_per_step=units_all, launches_per_step=launches)
 
     # roofline: profiling pass (per-launch CUDA events) of the headline engine
     eng = engines["lts"]
@@ -243,6 +280,7 @@ def run_ours(args):
     k_bytes = sum(BYTES_PER_UNIT * cum[n] for _, n in per)
     peak, peak_src = _peaks()
     achieved = k_bytes / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0
+    traffic, traffic_note = _ncu_traffic()
     # same for GTS launches (all tiles)
     geng = engines["gts"]
     _, gper = time_rounds(geng, 1, torch, None if dist is None else dist, per_launch=True)
@@ -257,12 +295,16 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize(dev)
     te0 = time.perf_counter()
+    ew = clk.window()
+    ew.__enter__()
     for _ in range(args.steps):
         eng.load_zip(z_host)
         eng.lts_coarse_step()
         z_out.copy_(eng.current_zip_device(), non_blocking=True)
         torch.cuda.synchronize(dev)
     te = time.perf_counter() - te0
+    ew.__exit__(None, None, None)
+    clk.stop()
     tt = torch.tensor([te], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -298,7 +340,8 @@ def run_ours(args):
         "lts_vs_gts_wall_speedup": gts["ms"] / lts["ms"],
         "lts_gts_equivalent_rate": gts["units_per_step"] * args.steps / (lts["ms"] * 1e-3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note,
+                     "peak_source": peak_src,
                      "kernel": "amr_stage (fused unzip+time-interp+RHS+zip[+combine])",
                      "bytes_per_unit": BYTES_PER_UNIT,
                      "launches": len(per), "kernel_ms_per_round": k_ms,
@@ -306,7 +349,7 @@ def run_ours(args):
         "e2e": {"value": lts["units_per_step"] * args.steps / te, "unit": "updates/s",
                 "h2d_bytes_per_step": int(2 * 8 * mesh.n_nodes), "d2h_bytes_per_step": int(2 * 8 * mesh.n_nodes)},
         "gpu_launches": int(lts["launches_per_step"] * args.steps),
-        "clocks": lts["clocks"],
+        "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(args, rounds=1)

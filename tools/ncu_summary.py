@@ -1,7 +1,14 @@
 """Summarise an ncu report: one row per profiled launch (duration, DRAM bytes, throughput, occupancy)."""
 import csv
 import subprocess
+import re
 import sys
+
+
+def _is_lts(name: str) -> bool:
+    """stage_kernel<DIM, PPO, LTS, NT> as ncu prints it (demangled forms vary)."""
+    m = re.search(r"stage_kernel<\(?\w*\)?(\d+), \(?\w*\)?(\d+), \(?\w*\)?(\w+)", name)
+    return bool(m) and m.group(3) in ("1", "true")
 
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
@@ -19,7 +26,7 @@ def main(path):
     print("|---|---|---|---|---|---|---|---|---|---|---|---|")
     for n, r in enumerate(rows[2:]):
         name = r[idx["Kernel Name"]]
-        lts = ("true" in name) or ("ELb1E" in name) or ("ILb1E" in name)
+        lts = _is_lts(name)
         short = ("interp" if "interp" in name else "stage") + ("_lts" if lts else "_gts")
         def g(m, scale=1.0):
             try:

@@ -1,0 +1,51 @@
+"""Write profiles/traffic.json from an ncu report of tools/profile_stage.py:
+average DRAM bytes (read+write) per LTS stage launch over the profiled LTS
+launches (slices 16 and 17), beside their algorithmic bytes (68 B/unit)."""
+import csv
+import json
+import subprocess
+import re
+import sys
+
+
+def _is_lts(name: str) -> bool:
+    """stage_kernel<DIM, PPO, LTS, NT> as ncu prints it (demangled forms vary)."""
+    m = re.search(r"stage_kernel<\(?\w*\)?(\d+), \(?\w*\)?(\d+), \(?\w*\)?(\w+)", name)
+    return bool(m) and m.group(3) in ("1", "true")
+
+import numpy as np
+
+
+def main(rep, out="profiles/traffic.json"):
+    q = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
+                        "dram__bytes_read.sum,dram__bytes_write.sum,launch__grid_size"],
+                       capture_output=True, text=True).stdout
+    rows = list(csv.reader(q.splitlines()))
+    hdr, units = rows[0], rows[1]
+    i_r, i_w = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+    i_n, i_g = hdr.index("Kernel Name"), hdr.index("launch__grid_size")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    lts = []
+    for r in rows[2:]:
+        if _is_lts(r[i_n]):
+            lts.append((float(r[i_r]) * scale[units[i_r]] + float(r[i_w]) * scale[units[i_w]], int(float(r[i_g]))))
+    # algorithmic bytes: 68 B x owned nodes of the launched tiles (cfg2 mesh)
+    sys.path.insert(0, ".")
+    from bench import build_mesh
+
+    _, mesh = build_mesh("cfg2", 1, "lts")
+    lv = mesh.tree.arrays()[1]
+    counts = np.diff(mesh.leaf_starts)
+    order = np.lexsort((np.arange(len(lv)), -lv))
+    cum = np.concatenate([[0], np.cumsum(counts[order])])
+    alg = [68.0 * cum[g] for _, g in lts]
+    d = {"source": rep.split("/")[-1], "lts_launches": len(lts),
+         "lts_bytes_per_launch": float(np.mean([b for b, _ in lts])),
+         "lts_algorithmic_bytes_per_launch": float(np.mean(alg)),
+         "ratio": float(np.sum([b for b, _ in lts]) / np.sum(alg))}
+    json.dump(d, open(out, "w"), indent=1)
+    print(d)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
