@@ -151,9 +151,9 @@ typedef struct {
   int max_slots;               /* largest slot set of any tile (dynamic shared memory) */
   int n_vt;                    /* verbatim stage-source terms at this stage (a[s][j] != 0) */
   int vt_j[AMR_MAXP];          /* their j */
-  double* U0;                  /* [n_nodes][2] interleaved (chi, phi) */
+  double* U0;                  /* [2][n_nodes]: the reference's zip layout (chi row, phi row) */
   double* U1;
-  double* K;                   /* [n_stages][n_nodes][2] */
+  double* K;                   /* [n_stages][2][n_nodes] */
   const AmrSliceCoef* coef;    /* LTS only (device) */
   /* GTS coefficients */
   double g_cstage[AMR_MAXP][AMR_MAXP];

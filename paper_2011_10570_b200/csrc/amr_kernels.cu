@@ -85,22 +85,30 @@ __device__ __forceinline__ int cross_cell(int e) {
 
 __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
 
+// Fields are SoA, the reference's (nvars, n_nodes) zip layout: var v of node g
+// at base[v*n + g]; stage j of K at K + j*2n.
+__device__ __forceinline__ double2 ld_pair(const double* __restrict__ base, int64_t n, int64_t g) {
+  return make_double2(__ldg(base + g), __ldg(base + n + g));
+}
+
 // --------------------------------------------------------------------------
-// stage source of one zip node as seen by a reader of cadence level lr
+// stage source of one zip node as seen by a reader of cadence lr (LTS):
+// verbatim, delta=0 stage transfer, or virtual substep + transfer
+// (Engine._stage_source / _virtual_state, stepper.py:256-314)
 // --------------------------------------------------------------------------
-__device__ __forceinline__ double2 lts_source(const double2* __restrict__ U0, const double2* __restrict__ U1,
-                                              const double2* __restrict__ K, int64_t n, int p, int g, int s, int lr,
+__device__ __forceinline__ double2 lts_source(const double* __restrict__ U0, const double* __restrict__ U1,
+                                              const double* __restrict__ K, int64_t n, int p, int g, int s, int lr,
                                               int ls, const AmrSliceCoef* __restrict__ C) {
   const int mode = C->mode[lr][ls];
   const int cur = C->cur[ls];
-  const double2* Uc = cur ? U1 : U0;
+  const double* Uc = cur ? U1 : U0;
   if (mode == 0) {  // eligible, same step size: verbatim (stepper.py:290-296)
-    double2 u = ld2(Uc + g);
+    const double2 u = ld_pair(Uc, n, g);
     double2 y = make_double2(0.0 + u.x, 0.0 + u.y);
     for (int j = 0; j < s; ++j) {
-      double c = C->cstage[lr][s][j];
+      const double c = C->cstage[lr][s][j];
       if (c != 0.0) {
-        double2 k = ld2(K + j * n + g);
+        const double2 k = ld_pair(K + (int64_t)j * 2 * n, n, g);
         y.x = y.x + c * k.x;
         y.y = y.y + c * k.y;
       }
@@ -110,18 +118,18 @@ __device__ __forceinline__ double2 lts_source(const double2* __restrict__ U0, co
   double2 kk[AMR_MAXP];
   const int nk = (mode == 1) ? s : p;  // delta=0 transfer is lower triangular
 #pragma unroll
-  for (int k = 0; k < AMR_MAXP; ++k) kk[k] = (k < nk) ? ld2(K + k * n + g) : make_double2(0.0, 0.0);
+  for (int k = 0; k < AMR_MAXP; ++k)
+    kk[k] = (k < nk) ? ld_pair(K + (int64_t)k * 2 * n, n, g) : make_double2(0.0, 0.0);
   double2 y;
   if (mode == 1) {
-    y = ld2(Uc + g);
+    y = ld_pair(Uc, n, g);
   } else {  // virtual substep from u_pre (stepper.py:256-270)
-    const double2* Up = cur ? U0 : U1;
-    y = ld2(Up + g);
+    y = ld_pair(cur ? U0 : U1, n, g);
     const double(*Mv)[AMR_MAXP] = C->Mv[lr][ls];
 #pragma unroll
     for (int i = 0; i < AMR_MAXP; ++i) {
       if (i >= p) break;
-      double c = C->dtw[lr][ls][i];
+      const double c = C->dtw[lr][ls][i];
       if (c == 0.0) continue;
       double ax = 0.0, ay = 0.0;
 #pragma unroll
@@ -137,89 +145,7 @@ __device__ __forceinline__ double2 lts_source(const double2* __restrict__ U0, co
 #pragma unroll
   for (int j = 0; j < AMR_MAXP; ++j) {
     if (j >= s) break;
-    double c = C->cstage[lr][s][j];
-    if (c == 0.0) continue;
-    const int kmax = (mode == 1) ? j : p - 1;
-    double ax = 0.0, ay = 0.0;
-#pragma unroll
-    for (int k = 0; k < AMR_MAXP; ++k) {
-      if (k > kmax) break;
-      ax = fma(M[j][k], kk[k].x, ax);
-      ay = fma(M[j][k], kk[k].y, ay);
-    }
-    y.x = y.x + c * ax;
-    y.y = y.y + c * ay;
-  }
-  return y;
-}
-
-template <bool LTS>
-__device__ __forceinline__ double2 stage_source(const AmrStageParams& P, const double2* __restrict__ U0,
-                                                const double2* __restrict__ U1,
-                                                const double2* __restrict__ K, int64_t n, int g, int s,
-                                                int lr, int ls, const AmrSliceCoef* __restrict__ C) {
-  const int p = P.n_stages;
-  if (!LTS) {
-    const double2* U = P.gts_cur ? U1 : U0;
-    double2 u = ld2(U + g);
-    double2 y = make_double2(0.0 + u.x, 0.0 + u.y);
-    for (int j = 0; j < s; ++j) {
-      double c = P.g_cstage[s][j];
-      if (c != 0.0) {
-        double2 k = ld2(K + j * n + g);
-        y.x = y.x + c * k.x;
-        y.y = y.y + c * k.y;
-      }
-    }
-    return y;
-  }
-  const int mode = C->mode[lr][ls];
-  const int cur = C->cur[ls];
-  const double2* Uc = cur ? U1 : U0;
-  if (mode == 0) {  // eligible, same step size: verbatim (stepper.py:290-296)
-    double2 u = ld2(Uc + g);
-    double2 y = make_double2(0.0 + u.x, 0.0 + u.y);
-    for (int j = 0; j < s; ++j) {
-      double c = C->cstage[lr][s][j];
-      if (c != 0.0) {
-        double2 k = ld2(K + j * n + g);
-        y.x = y.x + c * k.x;
-        y.y = y.y + c * k.y;
-      }
-    }
-    return y;
-  }
-  double2 kk[AMR_MAXP];
-  const int nk = (mode == 1) ? s : p;  // delta=0 transfer is lower triangular
-#pragma unroll
-  for (int k = 0; k < AMR_MAXP; ++k) kk[k] = (k < nk) ? ld2(K + k * n + g) : make_double2(0.0, 0.0);
-  double2 y;
-  if (mode == 1) {
-    y = ld2(Uc + g);
-  } else {  // virtual substep from u_pre (stepper.py:256-270)
-    const double2* Up = cur ? U0 : U1;
-    y = ld2(Up + g);
-    const double(*Mv)[AMR_MAXP] = C->Mv[lr][ls];
-#pragma unroll
-    for (int i = 0; i < AMR_MAXP; ++i) {
-      if (i >= p) break;
-      double c = C->dtw[lr][ls][i];
-      if (c == 0.0) continue;
-      double ax = 0.0, ay = 0.0;
-#pragma unroll
-      for (int k = 0; k <= i; ++k) {
-        ax = fma(Mv[i][k], kk[k].x, ax);
-        ay = fma(Mv[i][k], kk[k].y, ay);
-      }
-      y.x = y.x + c * ax;
-      y.y = y.y + c * ay;
-    }
-  }
-  const double(*M)[AMR_MAXP] = C->M[lr][ls];
-#pragma unroll
-  for (int j = 0; j < AMR_MAXP; ++j) {
-    if (j >= s) break;
-    double c = C->cstage[lr][s][j];
+    const double c = C->cstage[lr][s][j];
     if (c == 0.0) continue;
     const int kmax = (mode == 1) ? j : p - 1;
     double ax = 0.0, ay = 0.0;
@@ -361,13 +287,13 @@ __device__ __forceinline__ double2 rhs_point(const Acc& acc, const int* pos, int
 
 template <int DIM, int PPO>
 struct SmemAcc {
-  const double2* sv;
+  const double* chi;
+  const double* phi;
   int cell;
   __device__ __forceinline__ double at(int v, int d, int o) const {
     constexpr int NP = Tile<DIM, PPO>::NP;
-    int stride = (DIM == 3) ? (d == 0 ? NP * NP : (d == 1 ? NP : 1)) : (d == 0 ? NP : 1);
-    double2 q = sv[cell + o * stride];
-    return v == 0 ? q.x : q.y;
+    const int stride = (DIM == 3) ? (d == 0 ? NP * NP : (d == 1 ? NP : 1)) : (d == 0 ? NP : 1);
+    return (v == 0 ? chi : phi)[cell + o * stride];
   }
 };
 
@@ -378,8 +304,8 @@ struct SmemAcc {
 
 // interface source (LTS, reader and source step sizes or times differ): out
 // of line so the verbatim hot path keeps its register budget.
-__device__ __noinline__ double2 iface_source(const double2* __restrict__ U0, const double2* __restrict__ U1,
-                                             const double2* __restrict__ K, int64_t n, int p, int g, int s, int lr,
+__device__ __noinline__ double2 iface_source(const double* __restrict__ U0, const double* __restrict__ U1,
+                                             const double* __restrict__ K, int64_t n, int p, int g, int s, int lr,
                                              int ls, const AmrSliceCoef* __restrict__ C) {
   return lts_source(U0, U1, K, n, p, g, s, lr, ls, C);
 }
@@ -388,21 +314,32 @@ __device__ __noinline__ double2 iface_source(const double2* __restrict__ U0, con
 #define AMR_MIN_BLOCKS 4  // resident CTAs per SM the register budget is sized for (tuned: 2,3,4 -> 8.0,9.7,10.2 G LTS upd/s)
 #endif
 
+// The stage kernel.  Per tile:
+//  1a  table entries + slot ids (independent of the leaf-id load)
+//  1b  all gathers in flight: chi (u and the K_j of the verbatim source) for
+//      every copy entry and slot; phi only where the stencil needs it (owned
+//      nodes: dchi = phi; every entry of tiles on a physical face: radiative
+//      gradients)
+//  1c  copy rows (0 + 1.0*src) -> smem cross; slot stage sources -> smem
+//  1d  hanging rows: 0 + sum w*src in ascending-gid order -> smem cross
+//  2   RHS at the owned nodes; K_s out (last stage: RK combine into the other u)
 template <int DIM, int PPO, bool LTS, int NT>
 __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
     stage_kernel(const AmrStageParams P) {
   using T = Tile<DIM, PPO>;
   constexpr int EPT = (T::NE + T::THREADS - 1) / T::THREADS;
-  constexpr int SPT = 2;  // slots per thread issued with the table gathers
+  constexpr int EPI = (T::NI + T::THREADS - 1) / T::THREADS;  // entries per thread inside the leaf (e < NI)
+  constexpr int SPT = 2;                                      // slots per thread issued with the gathers
   constexpr int NK = NT > 0 ? NT : 1;
-  __shared__ double2 sv[T::NS];
+  __shared__ double s_chi[T::NS];
+  __shared__ double s_phi[T::NS];
   __shared__ short s_own[T::NI];
   __shared__ double s_w[256];
   extern __shared__ double2 slotv[];  // [max_slots] stage sources of the tile's tap nodes
   const int64_t tile = blockIdx.x;
   const int32_t* __restrict__ tab = P.tile_table + tile * T::NE;
   const uint8_t* __restrict__ side = LTS ? P.tile_src_cad + tile * T::NE : nullptr;
-  // phase 1a: table entries and the tile's slot range (independent of the leaf id)
+  // ---- 1a
   int ent[EPT];
   uint8_t sc[EPT];
 #pragma unroll
@@ -414,7 +351,6 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   const int64_t sl0 = __ldg(P.tile_slot_ptr + tile), sl1 = __ldg(P.tile_slot_ptr + tile + 1);
   const int64_t j0 = __ldg(P.tile_in_ptr + tile), j1 = __ldg(P.tile_in_ptr + tile + 1);
   const int nin = (int)(j1 - j0);
-
   const int nslot = (int)(sl1 - sl0);
   int sg[SPT];
   uint8_t scs[SPT];
@@ -435,10 +371,20 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   const int s = P.stage;
   const int64_t n = P.n_nodes;
   const int p = P.n_stages;
-  const double2* U0 = reinterpret_cast<const double2*>(P.U0);
-  const double2* U1 = reinterpret_cast<const double2*>(P.U1);
-  const double2* K = reinterpret_cast<const double2*>(P.K);
+  const double* U0 = P.U0;
+  const double* U1 = P.U1;
+  const double* K = P.K;
   const AmrSliceCoef* C = P.coef;
+  int faces = 0;
+  const int64_t side_len = (int64_t)1 << (P.max_depth - lvl);
+  int32_t anc[3];
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) {
+    anc[d] = P.leaf_anchor[leaf * 3 + d];
+    if (anc[d] == 0) faces |= 1 << (2 * d);
+    if (anc[d] + side_len == ((int64_t)1 << P.max_depth)) faces |= 2 << (2 * d);
+  }
+  const bool phi_all = faces != 0;  // radiative rows need phi gradients: phi on the whole cross
   int js[NK];
   double cs[NK];
 #pragma unroll
@@ -447,20 +393,26 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
     cs[t] = t < NT ? (LTS ? C->cstage[cad][s][js[t]] : P.g_cstage[s][js[t]]) : 0.0;
   }
   const int cur = LTS ? C->cur[cad] : P.gts_cur;
-  const double2* Ucur = cur ? U1 : U0;
+  const double* Ucur = cur ? U1 : U0;
 
-  // phase 1b: every data load of this thread in flight at once
+  // ---- 1b
   uint32_t fast = 0, sfast = 0;
-  double2 uv[EPT], kv[EPT][NK], su[SPT], sk[SPT][NK];
+  double cu[EPT], ck[EPT][NK], pu[EPI], pk[EPI][NK];
+  double2 su[SPT], sk[SPT][NK];
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
     bool f = ent[i] >= 0;
     if (LTS && f) f = C->mode[cad][sc[i]] == 0;
     fast |= (uint32_t)f << i;
     if (f) {
-      uv[i] = ld2(Ucur + ent[i]);
+      cu[i] = __ldg(Ucur + ent[i]);
 #pragma unroll
-      for (int t = 0; t < NT; ++t) kv[i][t] = ld2(K + (int64_t)js[t] * n + ent[i]);
+      for (int t = 0; t < NT; ++t) ck[i][t] = __ldg(K + (int64_t)js[t] * 2 * n + ent[i]);
+      if (i < EPI && (phi_all || (ent[i] >= g0 && ent[i] < g1))) {
+        pu[i] = __ldg(Ucur + n + ent[i]);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) pk[i][t] = __ldg(K + (int64_t)js[t] * 2 * n + n + ent[i]);
+      }
     }
   }
 #pragma unroll
@@ -469,31 +421,43 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
     if (LTS && f) f = C->mode[cad][scs[i]] == 0;
     sfast |= (uint32_t)f << i;
     if (f) {
-      su[i] = ld2(Ucur + sg[i]);
+      su[i] = ld_pair(Ucur, n, sg[i]);
 #pragma unroll
-      for (int t = 0; t < NT; ++t) sk[i][t] = ld2(K + (int64_t)js[t] * n + sg[i]);
+      for (int t = 0; t < NT; ++t) sk[i][t] = ld_pair(K + (int64_t)js[t] * 2 * n, n, sg[i]);
     }
   }
-  // phase 1c: copy entries -> stencil input (0 + 1.0*src), slots -> their stage source
+  // ---- 1c
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
     const int e = threadIdx.x + i * T::THREADS;
-    if (e >= T::NE || ent[i] <= -2) continue;  // interpolation nodes are written in phase 1d
-    double2 y = make_double2(0.0, 0.0);
+    if (e >= T::NE || ent[i] <= -2) continue;  // hanging rows are written in 1d
+    const int cell = cross_cell<DIM, PPO>(e);
+    const bool own = e < T::NI && ent[i] >= g0 && ent[i] < g1;
+    if (own) s_own[ent[i] - g0] = (short)e;
+    double yc = 0.0, yp = 0.0;
     if (fast >> i & 1) {
-      y = make_double2(0.0 + uv[i].x, 0.0 + uv[i].y);
+      yc = 0.0 + cu[i];
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        y.x = y.x + cs[t] * kv[i][t].x;
-        y.y = y.y + cs[t] * kv[i][t].y;
+      for (int t = 0; t < NT; ++t) yc = yc + cs[t] * ck[i][t];
+      yc = 0.0 + yc;  // copy row: 0 + 1.0*src
+      if (phi_all || own) {
+        if (i < EPI) {
+          yp = 0.0 + pu[i];
+#pragma unroll
+          for (int t = 0; t < NT; ++t) yp = yp + cs[t] * pk[i][t];
+        } else {  // halo phi of a face tile (rare)
+          yp = 0.0 + __ldg(Ucur + n + ent[i]);
+          for (int t = 0; t < NT; ++t) yp = yp + cs[t] * __ldg(K + (int64_t)js[t] * 2 * n + n + ent[i]);
+        }
+        yp = 0.0 + yp;
       }
-      y = make_double2(0.0 + y.x, 0.0 + y.y);
     } else if (LTS && ent[i] >= 0) {
       const double2 v = iface_source(U0, U1, K, n, p, ent[i], s, cad, sc[i], C);
-      y = make_double2(0.0 + v.x, 0.0 + v.y);
+      yc = 0.0 + v.x;
+      yp = 0.0 + v.y;
     }
-    if (e < T::NI && ent[i] >= g0 && ent[i] < g1) s_own[ent[i] - g0] = (short)e;
-    sv[cross_cell<DIM, PPO>(e)] = y;
+    s_chi[cell] = yc;
+    s_phi[cell] = yp;
   }
 #pragma unroll
   for (int i = 0; i < SPT; ++i) {
@@ -511,17 +475,15 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
     }
     slotv[threadIdx.x + i * T::THREADS] = y;
   }
-  // slots beyond SPT*THREADS (very large interface tiles)
-  for (int k = threadIdx.x + SPT * T::THREADS; k < nslot; k += T::THREADS) {
+  for (int k = threadIdx.x + SPT * T::THREADS; k < nslot; k += T::THREADS) {  // very large interface tiles
     const int g = __ldg(P.slot_gid + sl0 + k);
     if (LTS) {
       slotv[k] = iface_source(U0, U1, K, n, p, g, s, cad, __ldg(P.slot_cad + sl0 + k), C);
     } else {
-      const double2 u = ld2(Ucur + g);
-      double2 y = make_double2(0.0 + u.x, 0.0 + u.y);
-#pragma unroll
+      double2 y = ld_pair(Ucur, n, g);
+      y = make_double2(0.0 + y.x, 0.0 + y.y);
       for (int t = 0; t < NT; ++t) {
-        const double2 kk = ld2(K + (int64_t)js[t] * n + g);
+        const double2 kk = ld_pair(K + (int64_t)js[t] * 2 * n, n, g);
         y.x = y.x + cs[t] * kk.x;
         y.y = y.y + cs[t] * kk.y;
       }
@@ -529,10 +491,8 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
     }
   }
   __syncthreads();
-  // phase 1d: hanging rows, y = 0 + sum_k w_k src(g_k) in ascending-gid order
-  // (mesh.py:316-351, scipy csr_matvecs at mesh.py:418): one thread per row;
-  // tap words are fetched 8 at a time (independent, contiguous) so the
-  // running sum only waits on smem.
+  // ---- 1d: hanging rows, 0 + sum_k w_k src(g_k) in ascending-gid order
+  //      (mesh.py:316-351; scipy csr_matvecs, mesh.py:418); tap words 8 at a time
   for (int li = threadIdx.x; li < nin; li += T::THREADS) {
     const int64_t k0 = __ldg(P.in_tap_ptr + j0 + li), k1 = __ldg(P.in_tap_ptr + j0 + li + 1);
     double ax = 0.0, ay = 0.0;
@@ -546,15 +506,17 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
           const double w = wsmall ? s_w[tp[u] & 0xFFFF] : __ldg(P.wtab + (tp[u] & 0xFFFF));
           const double2 v = slotv[tp[u] >> 16];
           ax = ax + w * v.x;
-          ay = ay + w * v.y;
+          if (phi_all) ay = ay + w * v.y;
         }
       }
     }
-    sv[cross_cell<DIM, PPO>(__ldg(P.in_entry + j0 + li))] = make_double2(ax, ay);
+    const int cell = cross_cell<DIM, PPO>(__ldg(P.in_entry + j0 + li));
+    s_chi[cell] = ax;
+    s_phi[cell] = ay;
   }
   __syncthreads();
 
-  // phase 2: RHS at the owned nodes, K_s (and the RK combine) out
+  // ---- 2: RHS at the owned nodes, K_s (and the RK combine) out
   const Weights& W = P;
   RhsConst R;
   R.h = P.h[lvl];
@@ -568,19 +530,10 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   R.f0_chi = P.f0_chi;
   R.f0_phi = P.f0_phi;
   R.nonlinear = P.nonlinear;
-  int faces = 0;
-  const int64_t side_len = (int64_t)1 << (P.max_depth - lvl);
-  int32_t anc[3];
-#pragma unroll
-  for (int d = 0; d < DIM; ++d) {
-    anc[d] = P.leaf_anchor[leaf * 3 + d];
-    if (anc[d] == 0) faces |= 1 << (2 * d);
-    if (anc[d] + side_len == ((int64_t)1 << P.max_depth)) faces |= 2 << (2 * d);
-  }
   constexpr int scale = PPO - 1;
   const bool last = (s == p - 1);
-  double2* Unew = reinterpret_cast<double2*>(cur ? P.U0 : P.U1);
-  double2* Ks = reinterpret_cast<double2*>(P.K) + (int64_t)s * n;
+  double* Unew = cur ? P.U0 : P.U1;
+  double* Ks = P.K + (int64_t)s * 2 * n;
   const int n_own = (int)(g1 - g0);
   for (int k = threadIdx.x; k < n_own; k += T::THREADS) {
     const int q = s_own[k];
@@ -600,23 +553,25 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
       const int64_t lat = (int64_t)anc[d] * scale + side_len * pos[d];
       x[d] = P.lo[d] + ((double)lat / (double)P.top_nodes) * P.extent[d];
     }
-    SmemAcc<DIM, PPO> acc{sv, cell};
+    SmemAcc<DIM, PPO> acc{s_chi, s_phi, cell};
     const double2 ks = rhs_point<DIM>(acc, pos, PPO, faces, x, W, R);
     const int64_t g = g0 + k;
-    if (!last) {
-      Ks[g] = ks;
-    } else {
-      if (LTS) Ks[g] = ks;
-      const double2 u = ld2(Ucur + g);
-      double2 un = make_double2(0.0 + u.x, 0.0 + u.y);
+    if (!last || LTS) {
+      Ks[g] = ks.x;
+      Ks[n + g] = ks.y;
+    }
+    if (last) {
+      double ux = 0.0 + __ldg(Ucur + g), uy = 0.0 + __ldg(Ucur + n + g);
       for (int j = 0; j < p; ++j) {
         const double c = LTS ? C->comb[cad][j] : P.g_comb[j];
         if (c == 0.0) continue;
-        const double2 kj = (j == s) ? ks : ld2(K + (int64_t)j * n + g);
-        un.x = un.x + c * kj.x;
-        un.y = un.y + c * kj.y;
+        const double kx = (j == s) ? ks.x : __ldg(K + (int64_t)j * 2 * n + g);
+        const double ky = (j == s) ? ks.y : __ldg(K + (int64_t)j * 2 * n + n + g);
+        ux = ux + c * kx;
+        uy = uy + c * ky;
       }
-      Unew[g] = un;
+      Unew[g] = ux;
+      Unew[n + g] = uy;
     }
   }
 }

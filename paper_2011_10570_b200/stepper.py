@@ -7,8 +7,8 @@ run the RK stage loop in lockstep, reading neighbours through the stage
 transfer algebra where step sizes or times differ.
 
 B200 design:
-* state lives on the device in zip (gid) order, interleaved (chi, phi):
-  two u buffers and p stage buffers.  A leaf's live buffer is the parity of
+* state lives on the device in the reference's (nvars, n_nodes) zip layout
+  (SoA): two u buffers and p stage buffers.  A leaf's live buffer is the parity of
   its step count, so ``u_pre <- u_curr`` costs nothing, and the record fields
   ``t0``/``dt_units`` are implied by the schedule;
 * tiles are sorted by cadence (finest first), so the eligible set of any
@@ -245,8 +245,9 @@ class Engine:
                        **{k: T(v) for k, v in prog.items() if k != "max_slots"})
         self._max_slots = prog["max_slots"]
         n = mesh.n_nodes
-        self._U = [torch.zeros((n, 2), dtype=torch.float64, device=dev) for _ in range(2)]
-        self._K = torch.zeros((self.p, n, 2), dtype=torch.float64, device=dev)
+        # the reference's (nvars, n_nodes) zip layout, SoA: chi row then phi row
+        self._U = [torch.zeros((2, n), dtype=torch.float64, device=dev) for _ in range(2)]
+        self._K = torch.zeros((self.p, 2, n), dtype=torch.float64, device=dev)
         self._node_cad_t = self._d["node_cad"].long()
         self._vt = [[j for j in range(s_) if self.tab.a[s_][j] != 0.0] for s_ in range(self.p)]
         self._prm = self._make_params()
@@ -403,8 +404,8 @@ class Engine:
             zt = torch.from_numpy(np.ascontiguousarray(z, dtype=np.float64)).to(self.device, non_blocking=True)
         if tuple(zt.shape) != (self.NVARS, self.mesh.n_nodes):
             raise ValueError(f"zip field must be (2, {self.mesh.n_nodes}), got {tuple(zt.shape)}")
-        self._U[0].copy_(zt.t())
-        self._U[1].copy_(self._U[0])
+        self._U[0].copy_(zt)
+        self._U[1].copy_(zt)
         self._K.zero_()
         self.i_fine = 0
 
@@ -422,8 +423,8 @@ class Engine:
 
         i = self.i_fine
         par = torch.tensor([self._cur_parity(i, c) for c in range(self.l_max + 1)], device=self.device)
-        sel = par[self._node_cad_t].bool().unsqueeze(1)
-        return torch.where(sel, self._U[1], self._U[0]).t()
+        sel = par[self._node_cad_t].bool().unsqueeze(0)
+        return torch.where(sel, self._U[1], self._U[0])
 
     def current_zip(self) -> np.ndarray:
         return self.current_zip_device().cpu().numpy()
@@ -631,25 +632,27 @@ class GhostExchange:
         return self._idx[key]
 
     def swap(self, tensor, sel_key, select) -> None:
-        """Ship rows of the selected leaves owned here to every peer that reads them."""
+        """Ship the zip nodes (last axis) of the selected leaves owned here to
+        every peer that reads them."""
         import torch
         import torch.distributed as dist
 
+        ax = tensor.dim() - 1
         ops, bufs = [], []
         for peer in self.peers:
             si = self._index("s", peer, sel_key, select)
             ri = self._index("r", peer, sel_key, select)
             if si is not None:
-                ops.append(dist.P2POp(dist.isend, tensor.index_select(0, si).contiguous(), peer, self.group))
+                ops.append(dist.P2POp(dist.isend, tensor.index_select(ax, si).contiguous(), peer, self.group))
             if ri is not None:
-                rb = torch.empty((len(ri),) + tuple(tensor.shape[1:]), dtype=tensor.dtype, device=tensor.device)
+                rb = torch.empty(tuple(tensor.shape[:-1]) + (len(ri),), dtype=tensor.dtype, device=tensor.device)
                 ops.append(dist.P2POp(dist.irecv, rb, peer, self.group))
                 bufs.append((ri, rb))
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
         for ri, rb in bufs:
-            tensor.index_copy_(0, ri, rb)
+            tensor.index_copy_(ax, ri, rb)
 
     def swap_from_cadence(self, tensor, min_cad: int) -> None:
         self.swap(tensor, ("ge", min_cad), lambda c: c >= min_cad)

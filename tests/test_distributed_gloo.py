@@ -38,14 +38,15 @@ def _worker(rank, world, port, q):
         owners = mesh.pmap.owners(len(mesh.tree.leaves))
         levels = mesh.tree.arrays()[1]
         n = mesh.n_nodes
-        truth = np.stack([np.arange(n, dtype=np.float64), -np.arange(n, dtype=np.float64)], axis=1)
+        truth = np.stack([np.arange(n, dtype=np.float64), -np.arange(n, dtype=np.float64)])  # (2, n) zip layout
         node_owner = np.repeat(owners, np.diff(mesh.leaf_starts))
-        t = torch.full((n, 2), float("nan"), dtype=torch.float64)
+        t = torch.full((2, n), float("nan"), dtype=torch.float64)
         mine = torch.from_numpy(node_owner == rank)
-        t[mine] = torch.from_numpy(truth)[mine]
+        t[:, mine] = torch.from_numpy(truth)[:, mine]
         gx = GhostExchange(mesh.exchange_plan(), levels, mesh.leaf_starts, rank, None, torch.device("cpu"))
         gx.swap_from_cadence(t, int(levels.min()))
-        got = t.numpy()
+        got = t.numpy().T
+        truth = truth.T
         expect_rows = np.zeros(n, dtype=bool)
         expect_rows[node_owner == rank] = True
         for peer, leaves in gx.recv.items():
@@ -54,15 +55,15 @@ def _worker(rank, world, port, q):
         ok_vals = np.array_equal(got[expect_rows], truth[expect_rows])
         ok_rest = bool(np.all(np.isnan(got[~expect_rows])))
         # exact-cadence swap: only finest-level ghosts move
-        t2 = torch.full((n, 2), float("nan"), dtype=torch.float64)
-        t2[mine] = torch.from_numpy(truth)[mine]
+        t2 = torch.full((2, n), float("nan"), dtype=torch.float64)
+        t2[:, mine] = torch.from_numpy(truth.T)[:, mine]
         lmax = int(levels.max())
         gx.swap_cadence(t2, lmax)
         fine_rows = np.zeros(n, dtype=bool)
         for peer, leaves in gx.recv.items():
             for l in leaves[levels[leaves] == lmax]:
                 fine_rows[mesh.leaf_starts[l]:mesh.leaf_starts[l + 1]] = True
-        g2 = t2.numpy()
+        g2 = t2.numpy().T
         ok_fine = np.array_equal(g2[fine_rows], truth[fine_rows]) and bool(
             np.all(np.isnan(g2[~fine_rows & (node_owner != rank)])))
         n_recv = int(sum(len(v) for v in gx.recv.values()))
