@@ -145,7 +145,6 @@ typedef struct {
   const int64_t* in_tap_ptr;   /* [n_in+1] taps of node j, CSR (ascending gid) order */
   const int64_t* tile_tap_ptr; /* [n_tiles+1] taps of tile t (= in_tap_ptr[tile_in_ptr[t]]) */
   const uint16_t* in_entry;    /* [n_in] cross entry the node fills */
-  const uint8_t* tile_hface;   /* [n_tiles] faces (bit 2*axis+side) holding interpolated cells */
   const uint32_t* tap;         /* [n_taps] (tile-local slot << 16) | weight id */
   const double* wtab;          /* distinct interpolation weights */
   int64_t n_wtab;

@@ -83,6 +83,7 @@ __device__ __forceinline__ int cross_cell(int e) {
   return c;
 }
 
+__device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
 
 // Fields are SoA, the reference's (nvars, n_nodes) zip layout: var v of node g
 // at base[v*n + g]; stage j of K at K + j*2n.
@@ -490,10 +491,32 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
     }
   }
   __syncthreads();
-  // ---- 2: RHS at the owned nodes, K_s (and the RK combine) out.  Nodes whose
-  //      stencil cannot reach a hanging cell (hface: faces with interpolated
-  //      cells, within 2 nodes) go first, before the hanging-row sums and their
-  //      barrier; the rest after.
+  // ---- 1d: hanging rows, 0 + sum_k w_k src(g_k) in ascending-gid order
+  //      (mesh.py:316-351; scipy csr_matvecs, mesh.py:418); tap words 8 at a time
+  for (int li = threadIdx.x; li < nin; li += T::THREADS) {
+    const int64_t k0 = __ldg(P.in_tap_ptr + j0 + li), k1 = __ldg(P.in_tap_ptr + j0 + li + 1);
+    double ax = 0.0, ay = 0.0;
+    for (int64_t k = k0; k < k1; k += 8) {
+      uint32_t tp[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) tp[u] = (k + u < k1) ? __ldg(P.tap + k + u) : 0u;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (k + u < k1) {
+          const double w = wsmall ? s_w[tp[u] & 0xFFFF] : __ldg(P.wtab + (tp[u] & 0xFFFF));
+          const double2 v = slotv[tp[u] >> 16];
+          ax = ax + w * v.x;
+          if (phi_all) ay = ay + w * v.y;
+        }
+      }
+    }
+    const int cell = cross_cell<DIM, PPO>(__ldg(P.in_entry + j0 + li));
+    s_chi[cell] = ax;
+    s_phi[cell] = ay;
+  }
+  __syncthreads();
+
+  // ---- 2: RHS at the owned nodes, K_s (and the RK combine) out
   const Weights& W = P;
   RhsConst R;
   R.h = P.h[lvl];
@@ -512,77 +535,43 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   double* Unew = cur ? P.U0 : P.U1;
   double* Ks = P.K + (int64_t)s * 2 * n;
   const int n_own = (int)(g1 - g0);
-  const int hface = nin > 0 ? (int)__ldg(P.tile_hface + tile) : 0;
-  for (int pass = 0; pass < 2; ++pass) {
-    if (pass == 1) {
-      // ---- 1d: hanging rows, 0 + sum_k w_k src(g_k) in ascending-gid order
-      //      (mesh.py:316-351; scipy csr_matvecs, mesh.py:418); tap words 8 at a time
-      for (int li = threadIdx.x; li < nin; li += T::THREADS) {
-        const int64_t k0 = __ldg(P.in_tap_ptr + j0 + li), k1 = __ldg(P.in_tap_ptr + j0 + li + 1);
-        double ax = 0.0, ay = 0.0;
-        for (int64_t k = k0; k < k1; k += 8) {
-          uint32_t tp[8];
+  for (int k = threadIdx.x; k < n_own; k += T::THREADS) {
+    const int q = s_own[k];
+    int pos[3];
+    int r = q;
 #pragma unroll
-          for (int u = 0; u < 8; ++u) tp[u] = (k + u < k1) ? __ldg(P.tap + k + u) : 0u;
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            if (k + u < k1) {
-              const double w = wsmall ? s_w[tp[u] & 0xFFFF] : __ldg(P.wtab + (tp[u] & 0xFFFF));
-              const double2 v = slotv[tp[u] >> 16];
-              ax = ax + w * v.x;
-              if (phi_all) ay = ay + w * v.y;
-            }
-          }
-        }
-        const int cell = cross_cell<DIM, PPO>(__ldg(P.in_entry + j0 + li));
-        s_chi[cell] = ax;
-        s_phi[cell] = ay;
-      }
-      __syncthreads();
+    for (int d = DIM - 1; d >= 0; --d) {
+      pos[d] = r % PPO;
+      r /= PPO;
     }
-    for (int k = threadIdx.x; k < n_own; k += T::THREADS) {
-      const int q = s_own[k];
-      int pos[3];
-      int r = q;
+    int cell = 0;
 #pragma unroll
-      for (int d = DIM - 1; d >= 0; --d) {
-        pos[d] = r % PPO;
-        r /= PPO;
-      }
-      bool dep = false;
+    for (int d = 0; d < DIM; ++d) cell = cell * T::NP + (pos[d] + T::PAD);
+    double x[3];
 #pragma unroll
-      for (int d = 0; d < DIM; ++d)
-        dep |= (((hface >> (2 * d)) & 1) && pos[d] <= 2) || (((hface >> (2 * d + 1)) & 1) && pos[d] >= PPO - 3);
-      if (dep != (pass == 1)) continue;
-      int cell = 0;
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) cell = cell * T::NP + (pos[d] + T::PAD);
-      double x[3];
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        const int64_t lat = (int64_t)anc[d] * scale + side_len * pos[d];
-        x[d] = P.lo[d] + ((double)lat / (double)P.top_nodes) * P.extent[d];
+    for (int d = 0; d < DIM; ++d) {
+      const int64_t lat = (int64_t)anc[d] * scale + side_len * pos[d];
+      x[d] = P.lo[d] + ((double)lat / (double)P.top_nodes) * P.extent[d];
+    }
+    SmemAcc<DIM, PPO> acc{s_chi, s_phi, cell};
+    const double2 ks = rhs_point<DIM>(acc, pos, PPO, faces, x, W, R);
+    const int64_t g = g0 + k;
+    if (!last || LTS) {
+      Ks[g] = ks.x;
+      Ks[n + g] = ks.y;
+    }
+    if (last) {
+      double ux = 0.0 + __ldg(Ucur + g), uy = 0.0 + __ldg(Ucur + n + g);
+      for (int j = 0; j < p; ++j) {
+        const double c = LTS ? C->comb[cad][j] : P.g_comb[j];
+        if (c == 0.0) continue;
+        const double kx = (j == s) ? ks.x : __ldg(K + (int64_t)j * 2 * n + g);
+        const double ky = (j == s) ? ks.y : __ldg(K + (int64_t)j * 2 * n + n + g);
+        ux = ux + c * kx;
+        uy = uy + c * ky;
       }
-      SmemAcc<DIM, PPO> acc{s_chi, s_phi, cell};
-      const double2 ks = rhs_point<DIM>(acc, pos, PPO, faces, x, W, R);
-      const int64_t g = g0 + k;
-      if (!last || LTS) {
-        Ks[g] = ks.x;
-        Ks[n + g] = ks.y;
-      }
-      if (last) {
-        double ux = 0.0 + __ldg(Ucur + g), uy = 0.0 + __ldg(Ucur + n + g);
-        for (int j = 0; j < p; ++j) {
-          const double c = LTS ? C->comb[cad][j] : P.g_comb[j];
-          if (c == 0.0) continue;
-          const double kx = (j == s) ? ks.x : __ldg(K + (int64_t)j * 2 * n + g);
-          const double ky = (j == s) ? ks.y : __ldg(K + (int64_t)j * 2 * n + n + g);
-          ux = ux + c * kx;
-          uy = uy + c * ky;
-        }
-        Unew[g] = ux;
-        Unew[n + g] = uy;
-      }
+      Unew[g] = ux;
+      Unew[n + g] = uy;
     }
   }
 }

@@ -142,34 +142,6 @@ class WorkCounters:
         return out
 
 
-def _cross_local(e: np.ndarray, dim: int, ppo: int, pad: int = 2) -> np.ndarray:
-    """Padded local coordinates of stencil-cross entries (the enumeration of
-    cross_entry_local in amr_mesh.cpp / cross_cell in amr_kernels.cu)."""
-    e = np.asarray(e, dtype=np.int64)
-    NI, NF = ppo ** dim, ppo ** (dim - 1)
-    loc = np.zeros((len(e), dim), dtype=np.int64)
-    inner = e < NI
-    r = e[inner].copy()
-    for d in range(dim - 1, -1, -1):
-        loc[inner, d] = pad + r % ppo
-        r //= ppo
-    h = ~inner
-    r = e[h] - NI
-    axis = r // (2 * pad * NF)
-    r = r % (2 * pad * NF)
-    layer = r // NF
-    within = r % NF
-    lp = np.where(layer < pad, layer, ppo + layer)
-    sub = np.zeros((len(r), dim), dtype=np.int64)
-    for d in range(dim - 1, -1, -1):
-        others = axis != d
-        sub[others, d] = pad + within[others] % ppo
-        within = np.where(others, within // ppo, within)
-    sub[np.arange(len(r)), axis] = lp
-    loc[h] = sub
-    return loc
-
-
 def _pow2_exact(x: float) -> bool:
     m, _ = np.frexp(x)
     return x > 0 and m == 0.5
@@ -339,20 +311,11 @@ class Engine:
         if len(wtab) > 1 << 16:
             raise ValueError("more than 65536 distinct interpolation weights")
         slot_gid = (key & 0xFFFFFFFF).astype(np.int32)
-        # faces of each tile that hold interpolated cells (kernel: nodes within 2 of them wait for 1d)
-        hface = np.zeros(nt, dtype=np.uint8)
-        if n_in:
-            loc = _cross_local(e_idx, td["dim"], td["ppo"]) - 2  # interior coords of each hanging cell
-            for d in range(td["dim"]):
-                lo = loc[:, d] <= 0
-                hi = loc[:, d] >= td["ppo"] - 1
-                np.bitwise_or.at(hface, t_idx[lo], np.uint8(1 << (2 * d)))
-                np.bitwise_or.at(hface, t_idx[hi], np.uint8(2 << (2 * d)))
         pad = lambda a, dt: a.astype(dt) if len(a) else np.zeros(1, dt)  # noqa: E731
         prog = dict(tile_slot_ptr=tile_slot_ptr, slot_gid=pad(slot_gid, np.int32),
                     slot_cad=pad(node_cad[slot_gid] if len(slot_gid) else slot_gid, np.uint8),
                     tile_in_ptr=tile_in_ptr, in_tap_ptr=in_tap_ptr, tile_tap_ptr=in_tap_ptr[tile_in_ptr],
-                    in_entry=pad(e_idx, np.uint16), tile_hface=pad(hface, np.uint8),
+                    in_entry=pad(e_idx, np.uint16),
                     tap=pad((local_slot << 16) | widx, np.uint32), wtab=wtab.astype(np.float64),
                     max_slots=max_slots)
         return table, prog
@@ -376,7 +339,6 @@ class Engine:
         P.tile_in_ptr, P.in_tap_ptr, P.in_entry = (d["tile_in_ptr"].data_ptr(), d["in_tap_ptr"].data_ptr(),
                                                    d["in_entry"].data_ptr())
         P.tile_tap_ptr = d["tile_tap_ptr"].data_ptr()
-        P.tile_hface = d["tile_hface"].data_ptr()
         P.tap, P.wtab, P.n_wtab = d["tap"].data_ptr(), d["wtab"].data_ptr(), int(d["wtab"].numel())
         P.max_slots = self._max_slots
         P.U0, P.U1, P.K = self._U[0].data_ptr(), self._U[1].data_ptr(), self._K.data_ptr()
