@@ -144,8 +144,11 @@ typedef struct {
   const int64_t* tile_in_ptr;  /* [n_tiles+1] interpolation nodes of tile t */
   const int64_t* in_tap_ptr;   /* [n_in+1] taps of node j, CSR (ascending gid) order */
   const int64_t* tile_tap_ptr; /* [n_tiles+1] taps of tile t (= in_tap_ptr[tile_in_ptr[t]]) */
-  const uint16_t* in_entry;    /* [n_in] cross entry the node fills */
-  const uint32_t* tap;         /* [n_taps] (tile-local slot << 16) | weight id */
+  const uint16_t* in_cell;     /* [n_in] smem cell (padded ppo+4 box) the node fills */
+  const int32_t* tile_meta;    /* [n_tiles][4] {first gid, end gid, level | cadence<<8 | faces<<16, leaf} */
+  const uint16_t* cross_cells; /* [entries] padded-box cell of each stencil-cross entry */
+  const uint32_t* tap;         /* [n_taps] (tile-local slot << 16) | weight id; rows padded to a multiple of
+                                  4 taps with (zero slot = n_slots of the tile, weight 0) */
   const double* wtab;          /* distinct interpolation weights */
   int64_t n_wtab;
   int max_slots;               /* largest slot set of any tile (dynamic shared memory) */

@@ -83,7 +83,6 @@ __device__ __forceinline__ int cross_cell(int e) {
   return c;
 }
 
-__device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
 
 // Fields are SoA, the reference's (nvars, n_nodes) zip layout: var v of node g
 // at base[v*n + g]; stage j of K at K + j*2n.
@@ -334,8 +333,8 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   __shared__ double s_chi[T::NS];
   __shared__ double s_phi[T::NS];
   __shared__ short s_own[T::NI];
-  __shared__ double s_w[256];
-  extern __shared__ double2 slotv[];  // [max_slots] stage sources of the tile's tap nodes
+  extern __shared__ double2 slotv[];  // [max_slots] slot stage sources, [1] zero slot, then [n_wtab] weights
+  double* s_w = reinterpret_cast<double*>(slotv + P.max_slots + 1);
   const int64_t tile = blockIdx.x;
   const int32_t* __restrict__ tab = P.tile_table + tile * T::NE;
   const uint8_t* __restrict__ side = LTS ? P.tile_src_cad + tile * T::NE : nullptr;
@@ -360,14 +359,15 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
     sg[i] = k < nslot ? __ldg(P.slot_gid + sl0 + k) : -1;
     scs[i] = (LTS && k < nslot) ? __ldg(P.slot_cad + sl0 + k) : 0;
   }
-  const bool wsmall = P.n_wtab <= 256;
-  if (wsmall)
-    for (int i = threadIdx.x; i < P.n_wtab; i += T::THREADS) s_w[i] = P.wtab[i];
-  const int leaf = P.tile_ids[tile];
-  const int64_t g0 = P.leaf_start[leaf];
-  const int64_t g1 = P.leaf_start[leaf + 1];
-  const int lvl = P.leaf_level[leaf];
-  const int cad = P.leaf_cadence[leaf];
+  for (int i = threadIdx.x; i < P.n_wtab; i += T::THREADS) s_w[i] = P.wtab[i];
+  if (threadIdx.x == 0) slotv[nslot] = make_double2(0.0, 0.0);  // zero slot of padding taps
+  const int4 meta = __ldg(reinterpret_cast<const int4*>(P.tile_meta) + tile);  // {g0, g1, lvl|cad<<8|faces<<16, leaf}
+  const int leaf = meta.w;
+  const int64_t g0 = meta.x;
+  const int64_t g1 = meta.y;
+  const int lvl = meta.z & 0xFF;
+  const int cad = (meta.z >> 8) & 0xFF;
+  const int faces = (meta.z >> 16) & 0x3F;
   const int s = P.stage;
   const int64_t n = P.n_nodes;
   const int p = P.n_stages;
@@ -375,15 +375,6 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   const double* U1 = P.U1;
   const double* K = P.K;
   const AmrSliceCoef* C = P.coef;
-  int faces = 0;
-  const int64_t side_len = (int64_t)1 << (P.max_depth - lvl);
-  int32_t anc[3];
-#pragma unroll
-  for (int d = 0; d < DIM; ++d) {
-    anc[d] = P.leaf_anchor[leaf * 3 + d];
-    if (anc[d] == 0) faces |= 1 << (2 * d);
-    if (anc[d] + side_len == ((int64_t)1 << P.max_depth)) faces |= 2 << (2 * d);
-  }
   const bool phi_all = faces != 0;  // radiative rows need phi gradients: phi on the whole cross
   int js[NK];
   double cs[NK];
@@ -431,7 +422,7 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   for (int i = 0; i < EPT; ++i) {
     const int e = threadIdx.x + i * T::THREADS;
     if (e >= T::NE || ent[i] <= -2) continue;  // hanging rows are written in 1d
-    const int cell = cross_cell<DIM, PPO>(e);
+    const int cell = __ldg(P.cross_cells + e);
     const bool own = e < T::NI && ent[i] >= g0 && ent[i] < g1;
     if (own) s_own[ent[i] - g0] = (short)e;
     double yc = 0.0, yp = 0.0;
@@ -492,27 +483,43 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   }
   __syncthreads();
   // ---- 1d: hanging rows, 0 + sum_k w_k src(g_k) in ascending-gid order
-  //      (mesh.py:316-351; scipy csr_matvecs, mesh.py:418); tap words 8 at a time
-  for (int li = threadIdx.x; li < nin; li += T::THREADS) {
-    const int64_t k0 = __ldg(P.in_tap_ptr + j0 + li), k1 = __ldg(P.in_tap_ptr + j0 + li + 1);
-    double ax = 0.0, ay = 0.0;
-    for (int64_t k = k0; k < k1; k += 8) {
-      uint32_t tp[8];
+  //      (mesh.py:316-351; scipy csr_matvecs, mesh.py:418).  Rows hold a
+  //      multiple of 4 taps (padding taps: weight 0 on the zero slot, which
+  //      leaves the running sum unchanged), 16-byte aligned: one uint4 of tap
+  //      words per 4 taps.  in_cell is the row's smem cell.
+  if (phi_all) {
+    for (int li = threadIdx.x; li < nin; li += T::THREADS) {
+      const int64_t k0 = __ldg(P.in_tap_ptr + j0 + li), k1 = __ldg(P.in_tap_ptr + j0 + li + 1);
+      double ax = 0.0, ay = 0.0;
+      for (int64_t k = k0; k < k1; k += 4) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(P.tap + k));
+        const uint32_t tq[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-      for (int u = 0; u < 8; ++u) tp[u] = (k + u < k1) ? __ldg(P.tap + k + u) : 0u;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (k + u < k1) {
-          const double w = wsmall ? s_w[tp[u] & 0xFFFF] : __ldg(P.wtab + (tp[u] & 0xFFFF));
-          const double2 v = slotv[tp[u] >> 16];
+        for (int u = 0; u < 4; ++u) {
+          const double w = s_w[tq[u] & 0xFFFF];
+          const double2 v = slotv[tq[u] >> 16];
           ax = ax + w * v.x;
-          if (phi_all) ay = ay + w * v.y;
+          ay = ay + w * v.y;
         }
       }
+      const int cell = __ldg(P.in_cell + j0 + li);
+      s_chi[cell] = ax;
+      s_phi[cell] = ay;
     }
-    const int cell = cross_cell<DIM, PPO>(__ldg(P.in_entry + j0 + li));
-    s_chi[cell] = ax;
-    s_phi[cell] = ay;
+  } else {
+    for (int li = threadIdx.x; li < nin; li += T::THREADS) {
+      const int64_t k0 = __ldg(P.in_tap_ptr + j0 + li), k1 = __ldg(P.in_tap_ptr + j0 + li + 1);
+      double ax = 0.0;
+      for (int64_t k = k0; k < k1; k += 4) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(P.tap + k));
+        const uint32_t tq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ax = ax + s_w[tq[u] & 0xFFFF] * slotv[tq[u] >> 16].x;
+      }
+      const int cell = __ldg(P.in_cell + j0 + li);
+      s_chi[cell] = ax;
+      s_phi[cell] = 0.0;
+    }
   }
   __syncthreads();
 
@@ -531,6 +538,13 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   R.f0_phi = P.f0_phi;
   R.nonlinear = P.nonlinear;
   constexpr int scale = PPO - 1;
+  const bool need_x = faces != 0 || P.nonlinear == 1;  // radiative rows / sin(2chi)/r^2 need coordinates
+  const int64_t side_len = (int64_t)1 << (P.max_depth - lvl);
+  int32_t anc[3] = {0, 0, 0};
+  if (need_x) {
+#pragma unroll
+    for (int d = 0; d < DIM; ++d) anc[d] = P.leaf_anchor[leaf * 3 + d];
+  }
   const bool last = (s == p - 1);
   double* Unew = cur ? P.U0 : P.U1;
   double* Ks = P.K + (int64_t)s * 2 * n;
@@ -547,11 +561,13 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
     int cell = 0;
 #pragma unroll
     for (int d = 0; d < DIM; ++d) cell = cell * T::NP + (pos[d] + T::PAD);
-    double x[3];
+    double x[3] = {0.0, 0.0, 0.0};
+    if (need_x) {
 #pragma unroll
-    for (int d = 0; d < DIM; ++d) {
-      const int64_t lat = (int64_t)anc[d] * scale + side_len * pos[d];
-      x[d] = P.lo[d] + ((double)lat / (double)P.top_nodes) * P.extent[d];
+      for (int d = 0; d < DIM; ++d) {
+        const int64_t lat = (int64_t)anc[d] * scale + side_len * pos[d];
+        x[d] = P.lo[d] + ((double)lat / (double)P.top_nodes) * P.extent[d];
+      }
     }
     SmemAcc<DIM, PPO> acc{s_chi, s_phi, cell};
     const double2 ks = rhs_point<DIM>(acc, pos, PPO, faces, x, W, R);
@@ -655,7 +671,7 @@ __global__ void pack_kernel(int64_t n_ranges, const int64_t* __restrict__ start,
 template <int DIM, int PPO, bool LTS, int NT>
 int launch_stage_one(const AmrStageParams* p, cudaStream_t st) {
   using T = Tile<DIM, PPO>;
-  const size_t dyn = sizeof(double2) * (size_t)(p->max_slots > 0 ? p->max_slots : 1);
+  const size_t dyn = sizeof(double2) * (size_t)(p->max_slots + 1) + sizeof(double) * (size_t)p->n_wtab;
   static size_t configured = 0;
   if (dyn > configured) {
     cudaError_t e = cudaFuncSetAttribute(stage_kernel<DIM, PPO, LTS, NT>,

@@ -345,7 +345,8 @@ class Mesh:
             a3 = np.zeros((n, 3), dtype=np.int32)
             a3[:, : self.dim] = anchors
             self._tile = dict(table=table, entries=E, interp_ptr=iptr, interp_gid=igid, interp_w=iw,
-                              anchor3=a3, level=levels.astype(np.int32), starts=self.leaf_starts)
+                              anchor3=a3, level=levels.astype(np.int32), starts=self.leaf_starts,
+                              dim=self.dim, ppo=self.ppo, max_depth=self.L)
         return self._tile
 
     # -- sync maps -------------------------------------------------------------------

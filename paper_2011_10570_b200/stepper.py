@@ -142,6 +142,34 @@ class WorkCounters:
         return out
 
 
+def _cross_local(e: np.ndarray, dim: int, ppo: int, pad: int = 2) -> np.ndarray:
+    """Padded local coordinates of stencil-cross entries (the enumeration of
+    cross_entry_local in amr_mesh.cpp)."""
+    e = np.asarray(e, dtype=np.int64)
+    NI, NF = ppo ** dim, ppo ** (dim - 1)
+    loc = np.zeros((len(e), dim), dtype=np.int64)
+    inner = e < NI
+    r = e[inner].copy()
+    for d in range(dim - 1, -1, -1):
+        loc[inner, d] = pad + r % ppo
+        r //= ppo
+    h = ~inner
+    r = e[h] - NI
+    axis = r // (2 * pad * NF)
+    r = r % (2 * pad * NF)
+    layer = r // NF
+    within = r % NF
+    lp = np.where(layer < pad, layer, ppo + layer)
+    sub = np.zeros((len(r), dim), dtype=np.int64)
+    for d in range(dim - 1, -1, -1):
+        others = axis != d
+        sub[others, d] = pad + within[others] % ppo
+        within = np.where(others, within // ppo, within)
+    sub[np.arange(len(r)), axis] = lp
+    loc[h] = sub
+    return loc
+
+
 def _pow2_exact(x: float) -> bool:
     m, _ = np.frexp(x)
     return x > 0 and m == 0.5
@@ -230,7 +258,7 @@ class Engine:
         tiles = mine[order].astype(np.int32)
         tcad = leaf_cad[tiles]
         self._prefix = {c: int(np.sum(tcad >= c)) for c in range(self.l_max + 1)}
-        table, prog = self._tile_programs(td, tiles, node_cad)
+        table, prog = self._tile_programs(td, tiles, node_cad, leaf_cad)
         lts_kernel = mode == "lts" or any(c != self.l_max for c in cadence)
         if lts_kernel:
             side = np.zeros(table.shape, dtype=np.uint8)
@@ -272,17 +300,25 @@ class Engine:
         return cadence
 
     @staticmethod
-    def _tile_programs(td: dict, tiles: np.ndarray, node_cad: np.ndarray):
+    def _tile_programs(td: dict, tiles: np.ndarray, node_cad: np.ndarray, leaf_cad: np.ndarray):
         """Tile tables in launch order plus each tile's interpolation program.
 
         A tile's hanging points (table entries <= -2, one interpolation row
-        each) become its own interpolation nodes, numbered tile-locally in
-        the table.  Their taps refer to a per-tile set of unique source nodes
-        ("slots") that the kernel gathers once into shared memory; taps keep
-        the row's CSR (ascending gid) order and a 16-bit weight id."""
+        each) become its own rows, numbered tile-locally in the table.  Their
+        taps refer to a per-tile set of unique source nodes ("slots") that the
+        kernel gathers once into shared memory; taps keep the row's CSR
+        (ascending gid) order and a 16-bit weight id.  Rows are padded to a
+        multiple of 4 taps with weight 0 on the tile's zero slot (index
+        n_slots), which leaves the running sum unchanged."""
+        dim, ppo = td["dim"], td["ppo"]
         table = td["table"][tiles].copy()
         ptr, gid, w = td["interp_ptr"], td["interp_gid"], td["interp_w"]
         nt, E = table.shape
+        NP = ppo + 4
+        loc = _cross_local(np.arange(E), dim, ppo)
+        cross_cells = np.zeros(E, dtype=np.int64)
+        for d in range(dim):
+            cross_cells = cross_cells * NP + loc[:, d]
         t_idx, e_idx = np.nonzero(table <= -2)  # row-major: by tile, then entry
         rows = (-table[t_idx, e_idx] - 2).astype(np.int64)
         n_in = len(rows)
@@ -291,33 +327,55 @@ class Engine:
         local_in = np.arange(n_in) - tile_in_ptr[t_idx]
         table[t_idx, e_idx] = (-(local_in + 2)).astype(np.int32)
         counts = (ptr[rows + 1] - ptr[rows]).astype(np.int64)
+        padded = (counts + 3) // 4 * 4
         in_tap_ptr = np.zeros(n_in + 1, dtype=np.int64)
-        np.cumsum(counts, out=in_tap_ptr[1:])
-        n_taps = int(in_tap_ptr[-1])
-        within = np.arange(n_taps) - np.repeat(in_tap_ptr[:-1], counts)
+        np.cumsum(padded, out=in_tap_ptr[1:])
+        n_real = int(counts.sum())
+        within = np.arange(n_real) - np.repeat(np.cumsum(counts) - counts, counts)
         src_idx = np.repeat(ptr[rows], counts) + within
+        dst_idx = np.repeat(in_tap_ptr[:-1], counts) + within
         tap_gid = gid[src_idx].astype(np.int64)
         tap_tile = np.repeat(t_idx.astype(np.int64), counts)
-        key, inv = np.unique((tap_tile << 32) | tap_gid, return_inverse=True) if n_taps else \
+        key, inv = np.unique((tap_tile << 32) | tap_gid, return_inverse=True) if n_real else \
             (np.zeros(0, np.int64), np.zeros(0, np.int64))
         slot_tile = key >> 32
         tile_slot_ptr = np.zeros(nt + 1, dtype=np.int64)
         np.cumsum(np.bincount(slot_tile, minlength=nt), out=tile_slot_ptr[1:])
+        n_slots = np.diff(tile_slot_ptr)
         local_slot = inv - tile_slot_ptr[tap_tile]
-        max_slots = int(np.diff(tile_slot_ptr).max()) if nt else 0
-        if max_slots >= 1 << 16:
-            raise ValueError("more than 65535 interpolation sources in one tile")
-        wtab, widx = np.unique(w[src_idx], return_inverse=True) if n_taps else (np.zeros(1), np.zeros(0, np.int64))
+        max_slots = int(n_slots.max()) if nt else 0
+        if max_slots >= (1 << 16) - 1:
+            raise ValueError("more than 65534 interpolation sources in one tile")
+        wtab, widx = np.unique(np.concatenate([w[src_idx], [0.0]]), return_inverse=True)
         if len(wtab) > 1 << 16:
             raise ValueError("more than 65536 distinct interpolation weights")
+        zero_w = int(widx[-1])
+        tap = np.zeros(max(int(in_tap_ptr[-1]), 4), dtype=np.uint32)
+        # padding taps: (tile's zero slot, weight 0)
+        pad_in = np.repeat(np.arange(n_in), padded - counts)
+        pad_pos = np.repeat(in_tap_ptr[:-1] + counts, padded - counts) + (
+            np.arange(int((padded - counts).sum())) - np.repeat(np.cumsum(padded - counts) - (padded - counts),
+                                                                padded - counts))
+        tap[pad_pos] = ((n_slots[t_idx[pad_in]].astype(np.uint32) << 16) | np.uint32(zero_w)).astype(np.uint32)
+        tap[dst_idx] = ((local_slot.astype(np.uint32) << 16) | widx[:-1].astype(np.uint32)).astype(np.uint32)
         slot_gid = (key & 0xFFFFFFFF).astype(np.int32)
+        # per-tile metadata in launch order: {g0, g1, level | cadence<<8 | faces<<16, leaf}
+        starts, levels, a3 = td["starts"], td["level"], td["anchor3"]
+        L = td["max_depth"]
+        side = (1 << (L - levels[tiles].astype(np.int64)))
+        faces = np.zeros(nt, dtype=np.int64)
+        for d in range(dim):
+            faces |= (a3[tiles, d] == 0).astype(np.int64) << (2 * d)
+            faces |= ((a3[tiles, d] + side) == (1 << L)).astype(np.int64) << (2 * d + 1)
+        meta = np.stack([starts[tiles], starts[tiles + 1],
+                         levels[tiles] | (leaf_cad[tiles].astype(np.int64) << 8) | (faces << 16),
+                         tiles], axis=1).astype(np.int32)
         pad = lambda a, dt: a.astype(dt) if len(a) else np.zeros(1, dt)  # noqa: E731
         prog = dict(tile_slot_ptr=tile_slot_ptr, slot_gid=pad(slot_gid, np.int32),
                     slot_cad=pad(node_cad[slot_gid] if len(slot_gid) else slot_gid, np.uint8),
                     tile_in_ptr=tile_in_ptr, in_tap_ptr=in_tap_ptr, tile_tap_ptr=in_tap_ptr[tile_in_ptr],
-                    in_entry=pad(e_idx, np.uint16),
-                    tap=pad((local_slot << 16) | widx, np.uint32), wtab=wtab.astype(np.float64),
-                    max_slots=max_slots)
+                    in_cell=pad(cross_cells[e_idx], np.uint16), tap=tap, wtab=wtab.astype(np.float64),
+                    tile_meta=meta, cross_cells=cross_cells.astype(np.uint16), max_slots=max_slots)
         return table, prog
 
     def _make_params(self) -> _native.AmrStageParams:
@@ -336,9 +394,10 @@ class Engine:
         P.tile_src_cad = d["side"].data_ptr()
         P.tile_slot_ptr, P.slot_gid, P.slot_cad = (d["tile_slot_ptr"].data_ptr(), d["slot_gid"].data_ptr(),
                                                    d["slot_cad"].data_ptr())
-        P.tile_in_ptr, P.in_tap_ptr, P.in_entry = (d["tile_in_ptr"].data_ptr(), d["in_tap_ptr"].data_ptr(),
-                                                   d["in_entry"].data_ptr())
+        P.tile_in_ptr, P.in_tap_ptr = d["tile_in_ptr"].data_ptr(), d["in_tap_ptr"].data_ptr()
         P.tile_tap_ptr = d["tile_tap_ptr"].data_ptr()
+        P.in_cell, P.tile_meta, P.cross_cells = (d["in_cell"].data_ptr(), d["tile_meta"].data_ptr(),
+                                                 d["cross_cells"].data_ptr())
         P.tap, P.wtab, P.n_wtab = d["tap"].data_ptr(), d["wtab"].data_ptr(), int(d["wtab"].numel())
         P.max_slots = self._max_slots
         P.U0, P.U1, P.K = self._U[0].data_ptr(), self._U[1].data_ptr(), self._K.data_ptr()
