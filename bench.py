@@ -163,7 +163,7 @@ def units_per_round(eng, rank_only=True):
     for i in range(eng.schedule.slices_per_round):
         el = eng._eligible_cadences(i)
         total += eng.p * sum(by_cad.get(c, 0) for c in el)
-        launches += eng.p if el else 0
+        launches += eng.launches_per_slice(i)
     return total, launches
 
 
@@ -190,7 +190,7 @@ def time_rounds(eng, steps, torch, dist, per_launch=False):
             launches.append((e0, e1, int(P.n_tiles)))
             return rc
 
-        eng._lib = type("L", (), {"amr_stage": staticmethod(timed)})()
+        eng._lib = type("L", (), {"amr_stage": staticmethod(timed), "amr_iface": staticmethod(L.amr_iface)})()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     start.record(stream)

@@ -76,7 +76,8 @@ int amr_mesh_node_coords(const AmrMesh* m, int32_t* coords);
  * over the stencil cross (ppo^dim interior + 2*dim*pad*ppo^(dim-1) face halo).
  * entry >= 0: copy of zip node `entry`; -1: outside the domain (zero row);
  * <= -2: interpolation row (-entry-2) of the CSR below (the engine remaps
- * these to the tile's own interpolation nodes). */
+ * these to the tile's own interpolation rows, and LTS copies whose source
+ * steps differently to interface pairs: entry <= -(1<<20)). */
 int64_t amr_tile_entries(int dim, int ppo);
 int amr_mesh_tile_table(const AmrMesh* m, int32_t* table);
 int64_t amr_mesh_interp_rows(const AmrMesh* m);
@@ -135,12 +136,17 @@ typedef struct {
   const int32_t* leaf_cadence; /* [n_leaves] time level (== level for LTS; promoted for single-stage) */
   const int64_t* leaf_start;   /* [n_leaves+1] */
   const uint8_t* node_cadence; /* [n_nodes] cadence of the owning leaf (LTS) */
-  const uint8_t* tile_src_cad; /* [n_tiles][entries] cadence of each copy entry's source (LTS) */
+  /* LTS interface pairs (zip node, reader cadence) whose source steps differently
+   * from the reader: computed once per stage by amr_iface into ibuf */
+  int64_t n_iface;             /* pairs of this launch (prefix: finest readers first) */
+  int64_t n_iface_total;
+  const int32_t* if_gid;
+  const int32_t* if_cad;
+  double* ibuf;                /* [2][n_iface_total] */
   /* per-tile interpolation program: the hanging points of each tile (rows of
    * mesh.py:316-351), summed from a per-tile set of unique source nodes */
   const int64_t* tile_slot_ptr; /* [n_tiles+1] source slots of tile t: [ptr[t], ptr[t+1]) */
-  const int32_t* slot_gid;     /* zip node of each slot */
-  const uint8_t* slot_cad;     /* cadence of the slot's source leaf (LTS) */
+  const int32_t* slot_gid;     /* zip node of each slot; < 0: LTS interface pair (-slot-1) */
   const int64_t* tile_in_ptr;  /* [n_tiles+1] interpolation nodes of tile t */
   const int64_t* in_tap_ptr;   /* [n_in+1] taps of node j, CSR (ascending gid) order */
   const int64_t* tile_tap_ptr; /* [n_tiles+1] taps of tile t (= in_tap_ptr[tile_in_ptr[t]]) */
@@ -181,6 +187,11 @@ typedef struct {
  * gathers[b].dot + wave_rhs + the K/state scatter (stepper.py:274-314,
  * 395-453). */
 int amr_stage(const AmrStageParams* p, void* stream);
+
+/* LTS interface pass of a stage (before amr_stage): ibuf[i] = stage source of
+ * zip node if_gid[i] as seen by readers of cadence if_cad[i] — the delta=0
+ * stage transfer or the virtual substep + transfer (stepper.py:256-314). */
+int amr_iface(const AmrStageParams* p, void* stream);
 
 
 

@@ -44,8 +44,8 @@ class AmrStageParams(C.Structure):
         ("interp_ptr", _vp), ("interp_gid", _vp), ("interp_w", _vp),
         ("leaf_anchor", _vp), ("leaf_level", _vp), ("leaf_cadence", _vp), ("leaf_start", _vp),
         ("node_cadence", _vp),
-        ("tile_src_cad", _vp),
-        ("tile_slot_ptr", _vp), ("slot_gid", _vp), ("slot_cad", _vp), ("tile_in_ptr", _vp),
+        ("n_iface", C.c_int64), ("n_iface_total", C.c_int64), ("if_gid", _vp), ("if_cad", _vp), ("ibuf", _vp),
+        ("tile_slot_ptr", _vp), ("slot_gid", _vp), ("tile_in_ptr", _vp),
         ("in_tap_ptr", _vp), ("tile_tap_ptr", _vp), ("in_cell", _vp), ("tile_meta", _vp), ("cross_cells", _vp), ("tap", _vp), ("wtab", _vp), ("n_wtab", C.c_int64),
         ("max_slots", C.c_int),
         ("n_vt", C.c_int), ("vt_j", C.c_int * AMR_MAXP),
@@ -90,6 +90,7 @@ SIGNATURES = {
     "amr_mesh_block_gather": ([_vp, C.c_int64, _i64p, _i64p, _i64p, _i64p, _f64p], C.c_int),
     "amr_pack_chunks": ([C.c_int64, _i64p, _i32p, C.c_int64, _i64p, _i64p], C.c_int64),
     "amr_stage": ([C.POINTER(AmrStageParams), _vp], C.c_int),
+    "amr_iface": ([C.POINTER(AmrStageParams), _vp], C.c_int),
     "amr_gather_rows": ([C.c_int64, _vp, _vp, _vp, C.c_int, _vp, C.c_int64, _vp, C.c_int64, _vp], C.c_int),
     "amr_block_rhs": ([C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_double, C.c_double, _vp, C.c_double,
                        C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,

@@ -38,6 +38,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 }
 
 constexpr int cpow(int b, int e) { return e == 0 ? 1 : b * cpow(b, e - 1); }
+constexpr int AMR_IFACE_BASE = -(1 << 20);  // table entries <= this: interface pair AMR_IFACE_BASE - entry
 
 template <int DIM, int PPO>
 struct Tile {
@@ -301,12 +302,19 @@ struct SmemAcc {
 // (tile) order, so the table load does not wait for the tile's leaf id.
 // --------------------------------------------------------------------------
 
-// interface source (LTS, reader and source step sizes or times differ): out
-// of line so the verbatim hot path keeps its register budget.
-__device__ __noinline__ double2 iface_source(const double* __restrict__ U0, const double* __restrict__ U1,
-                                             const double* __restrict__ K, int64_t n, int p, int g, int s, int lr,
-                                             int ls, const AmrSliceCoef* __restrict__ C) {
-  return lts_source(U0, U1, K, n, p, g, s, lr, ls, C);
+// LTS interface pass: the stage source of every (zip node, reader cadence)
+// pair whose step size or time differs from the reader's (delta=0 transfer or
+// virtual substep + transfer, stepper.py:256-314), once per stage, so the
+// stage kernel reads it like a copy.  Pairs are sorted finest reader first:
+// the eligible readers of a slice are a prefix.
+__global__ void __launch_bounds__(256) iface_kernel(const AmrStageParams P) {
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (i >= P.n_iface) return;
+  const int g = __ldg(P.if_gid + i);
+  const int lr = __ldg(P.if_cad + i);
+  const double2 v = lts_source(P.U0, P.U1, P.K, P.n_nodes, P.n_stages, g, P.stage, lr, P.node_cadence[g], P.coef);
+  P.ibuf[i] = v.x;
+  P.ibuf[P.n_iface_total + i] = v.y;
 }
 
 #ifndef AMR_MIN_BLOCKS
@@ -337,27 +345,22 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   double* s_w = reinterpret_cast<double*>(slotv + P.max_slots + 1);
   const int64_t tile = blockIdx.x;
   const int32_t* __restrict__ tab = P.tile_table + tile * T::NE;
-  const uint8_t* __restrict__ side = LTS ? P.tile_src_cad + tile * T::NE : nullptr;
   // ---- 1a
   int ent[EPT];
-  uint8_t sc[EPT];
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
     const int e = threadIdx.x + i * T::THREADS;
     ent[i] = (e < T::NE) ? __ldg(tab + e) : -1;
-    sc[i] = (LTS && e < T::NE) ? __ldg(side + e) : 0;
   }
   const int64_t sl0 = __ldg(P.tile_slot_ptr + tile), sl1 = __ldg(P.tile_slot_ptr + tile + 1);
   const int64_t j0 = __ldg(P.tile_in_ptr + tile), j1 = __ldg(P.tile_in_ptr + tile + 1);
   const int nin = (int)(j1 - j0);
   const int nslot = (int)(sl1 - sl0);
   int sg[SPT];
-  uint8_t scs[SPT];
 #pragma unroll
   for (int i = 0; i < SPT; ++i) {
     const int k = threadIdx.x + i * T::THREADS;
-    sg[i] = k < nslot ? __ldg(P.slot_gid + sl0 + k) : -1;
-    scs[i] = (LTS && k < nslot) ? __ldg(P.slot_cad + sl0 + k) : 0;
+    sg[i] = k < nslot ? __ldg(P.slot_gid + sl0 + k) : INT32_MIN;
   }
   for (int i = threadIdx.x; i < P.n_wtab; i += T::THREADS) s_w[i] = P.wtab[i];
   if (threadIdx.x == 0) slotv[nslot] = make_double2(0.0, 0.0);  // zero slot of padding taps
@@ -374,6 +377,8 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   const double* U0 = P.U0;
   const double* U1 = P.U1;
   const double* K = P.K;
+  const double* IB = P.ibuf;  // interface sources of this stage: chi row, then phi row
+  const int64_t nib = P.n_iface_total;
   const AmrSliceCoef* C = P.coef;
   const bool phi_all = faces != 0;  // radiative rows need phi gradients: phi on the whole cross
   int js[NK];
@@ -386,47 +391,49 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   const int cur = LTS ? C->cur[cad] : P.gts_cur;
   const double* Ucur = cur ? U1 : U0;
 
-  // ---- 1b
-  uint32_t fast = 0, sfast = 0;
+  // ---- 1b: every gather of this thread in flight at once.  Copy entries are
+  //      verbatim (same cadence); LTS interface entries read the transfer the
+  //      interface pass computed for (node, this cadence).
   double cu[EPT], ck[EPT][NK], pu[EPI], pk[EPI][NK];
   double2 su[SPT], sk[SPT][NK];
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
-    bool f = ent[i] >= 0;
-    if (LTS && f) f = C->mode[cad][sc[i]] == 0;
-    fast |= (uint32_t)f << i;
-    if (f) {
-      cu[i] = __ldg(Ucur + ent[i]);
+    const int g = ent[i];
+    if (g >= 0) {
+      cu[i] = __ldg(Ucur + g);
 #pragma unroll
-      for (int t = 0; t < NT; ++t) ck[i][t] = __ldg(K + (int64_t)js[t] * 2 * n + ent[i]);
-      if (i < EPI && (phi_all || (ent[i] >= g0 && ent[i] < g1))) {
-        pu[i] = __ldg(Ucur + n + ent[i]);
+      for (int t = 0; t < NT; ++t) ck[i][t] = __ldg(K + (int64_t)js[t] * 2 * n + g);
+      if (i < EPI && (phi_all || (g >= g0 && g < g1))) {
+        pu[i] = __ldg(Ucur + n + g);
 #pragma unroll
-        for (int t = 0; t < NT; ++t) pk[i][t] = __ldg(K + (int64_t)js[t] * 2 * n + n + ent[i]);
+        for (int t = 0; t < NT; ++t) pk[i][t] = __ldg(K + (int64_t)js[t] * 2 * n + n + g);
       }
+    } else if (LTS && g <= AMR_IFACE_BASE) {
+      cu[i] = __ldg(IB + (AMR_IFACE_BASE - g));
     }
   }
 #pragma unroll
   for (int i = 0; i < SPT; ++i) {
-    bool f = sg[i] >= 0;
-    if (LTS && f) f = C->mode[cad][scs[i]] == 0;
-    sfast |= (uint32_t)f << i;
-    if (f) {
-      su[i] = ld_pair(Ucur, n, sg[i]);
+    const int g = sg[i];
+    if (g >= 0) {
+      su[i] = ld_pair(Ucur, n, g);
 #pragma unroll
-      for (int t = 0; t < NT; ++t) sk[i][t] = ld_pair(K + (int64_t)js[t] * 2 * n, n, sg[i]);
+      for (int t = 0; t < NT; ++t) sk[i][t] = ld_pair(K + (int64_t)js[t] * 2 * n, n, g);
+    } else if (LTS && g != INT32_MIN) {
+      su[i] = make_double2(__ldg(IB + (-g - 1)), __ldg(IB + nib + (-g - 1)));
     }
   }
   // ---- 1c
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
     const int e = threadIdx.x + i * T::THREADS;
-    if (e >= T::NE || ent[i] <= -2) continue;  // hanging rows are written in 1d
+    const int g = ent[i];
+    if (e >= T::NE || (g <= -2 && g > AMR_IFACE_BASE)) continue;  // hanging rows are written in 1d
     const int cell = __ldg(P.cross_cells + e);
-    const bool own = e < T::NI && ent[i] >= g0 && ent[i] < g1;
-    if (own) s_own[ent[i] - g0] = (short)e;
+    const bool own = e < T::NI && g >= g0 && g < g1;
+    if (own) s_own[g - g0] = (short)e;
     double yc = 0.0, yp = 0.0;
-    if (fast >> i & 1) {
+    if (g >= 0) {
       yc = 0.0 + cu[i];
 #pragma unroll
       for (int t = 0; t < NT; ++t) yc = yc + cs[t] * ck[i][t];
@@ -437,39 +444,37 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
 #pragma unroll
           for (int t = 0; t < NT; ++t) yp = yp + cs[t] * pk[i][t];
         } else {  // halo phi of a face tile (rare)
-          yp = 0.0 + __ldg(Ucur + n + ent[i]);
-          for (int t = 0; t < NT; ++t) yp = yp + cs[t] * __ldg(K + (int64_t)js[t] * 2 * n + n + ent[i]);
+          yp = 0.0 + __ldg(Ucur + n + g);
+          for (int t = 0; t < NT; ++t) yp = yp + cs[t] * __ldg(K + (int64_t)js[t] * 2 * n + n + g);
         }
         yp = 0.0 + yp;
       }
-    } else if (LTS && ent[i] >= 0) {
-      const double2 v = iface_source(U0, U1, K, n, p, ent[i], s, cad, sc[i], C);
-      yc = 0.0 + v.x;
-      yp = 0.0 + v.y;
+    } else if (LTS && g <= AMR_IFACE_BASE) {
+      yc = 0.0 + cu[i];
+      if (phi_all) yp = 0.0 + __ldg(IB + nib + (AMR_IFACE_BASE - g));
     }
     s_chi[cell] = yc;
     s_phi[cell] = yp;
   }
 #pragma unroll
   for (int i = 0; i < SPT; ++i) {
-    if (sg[i] < 0) continue;
-    double2 y;
-    if (sfast >> i & 1) {
+    const int g = sg[i];
+    if (g == INT32_MIN) continue;
+    double2 y = su[i];  // interface source, or the verbatim source below
+    if (g >= 0) {
       y = make_double2(0.0 + su[i].x, 0.0 + su[i].y);
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
         y.x = y.x + cs[t] * sk[i][t].x;
         y.y = y.y + cs[t] * sk[i][t].y;
       }
-    } else {
-      y = iface_source(U0, U1, K, n, p, sg[i], s, cad, scs[i], C);
     }
     slotv[threadIdx.x + i * T::THREADS] = y;
   }
   for (int k = threadIdx.x + SPT * T::THREADS; k < nslot; k += T::THREADS) {  // very large interface tiles
     const int g = __ldg(P.slot_gid + sl0 + k);
-    if (LTS) {
-      slotv[k] = iface_source(U0, U1, K, n, p, g, s, cad, __ldg(P.slot_cad + sl0 + k), C);
+    if (LTS && g < 0) {
+      slotv[k] = make_double2(__ldg(IB + (-g - 1)), __ldg(IB + nib + (-g - 1)));
     } else {
       double2 y = ld_pair(Ucur, n, g);
       y = make_double2(0.0 + y.x, 0.0 + y.y);
@@ -720,6 +725,13 @@ extern "C" int amr_stage(const AmrStageParams* p, void* stream) {
   }
   amr_set_error_internal("amr_stage: unsupported (dim, ppo)");
   return AMR_EINVAL;
+}
+
+extern "C" int amr_iface(const AmrStageParams* p, void* stream) {
+  if (p->n_iface <= 0) return AMR_OK;
+  iface_kernel<<<(unsigned)((p->n_iface + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*p);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? AMR_OK : cuda_fail(e, "amr_iface launch");
 }
 
 extern "C" int amr_gather_rows(int64_t n_rows, const int64_t* row_ptr, const int64_t* col, const double* val,

@@ -142,6 +142,9 @@ class WorkCounters:
         return out
 
 
+_IFACE_BASE = -(1 << 20)  # AMR_IFACE_BASE in amr_kernels.cu
+
+
 def _cross_local(e: np.ndarray, dim: int, ppo: int, pad: int = 2) -> np.ndarray:
     """Padded local coordinates of stencil-cross entries (the enumeration of
     cross_entry_local in amr_mesh.cpp)."""
@@ -258,20 +261,18 @@ class Engine:
         tiles = mine[order].astype(np.int32)
         tcad = leaf_cad[tiles]
         self._prefix = {c: int(np.sum(tcad >= c)) for c in range(self.l_max + 1)}
-        table, prog = self._tile_programs(td, tiles, node_cad, leaf_cad)
         lts_kernel = mode == "lts" or any(c != self.l_max for c in cadence)
-        if lts_kernel:
-            side = np.zeros(table.shape, dtype=np.uint8)
-            cp = table >= 0
-            side[cp] = node_cad[table[cp]]
-        else:
-            side = np.zeros(1, dtype=np.uint8)
+        table, prog = self._tile_programs(td, tiles, node_cad, leaf_cad, lts=lts_kernel)
+        n_iface = prog.pop("n_iface")
+        self._if_prefix = {c: int(np.sum(prog["if_cad"][:n_iface] >= c)) for c in range(self.l_max + 1)}
+        self._n_iface = n_iface
         dev = self.device
         T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
         self._d = dict(tiles=T(tiles), table=T(table), anchor=T(td["anchor3"]), level=T(td["level"]),
-                       cadence=T(leaf_cad), starts=T(td["starts"]), node_cad=T(node_cad), side=T(side),
+                       cadence=T(leaf_cad), starts=T(td["starts"]), node_cad=T(node_cad),
                        **{k: T(v) for k, v in prog.items() if k != "max_slots"})
         self._max_slots = prog["max_slots"]
+        self._ibuf = torch.zeros((2, max(n_iface, 1)), dtype=torch.float64, device=dev)
         n = mesh.n_nodes
         # the reference's (nvars, n_nodes) zip layout, SoA: chi row then phi row
         self._U = [torch.zeros((2, n), dtype=torch.float64, device=dev) for _ in range(2)]
@@ -300,7 +301,7 @@ class Engine:
         return cadence
 
     @staticmethod
-    def _tile_programs(td: dict, tiles: np.ndarray, node_cad: np.ndarray, leaf_cad: np.ndarray):
+    def _tile_programs(td: dict, tiles: np.ndarray, node_cad: np.ndarray, leaf_cad: np.ndarray, lts: bool = False):
         """Tile tables in launch order plus each tile's interpolation program.
 
         A tile's hanging points (table entries <= -2, one interpolation row
@@ -359,6 +360,28 @@ class Engine:
         tap[pad_pos] = ((n_slots[t_idx[pad_in]].astype(np.uint32) << 16) | np.uint32(zero_w)).astype(np.uint32)
         tap[dst_idx] = ((local_slot.astype(np.uint32) << 16) | widx[:-1].astype(np.uint32)).astype(np.uint32)
         slot_gid = (key & 0xFFFFFFFF).astype(np.int32)
+        # LTS interface pairs: copies and slots whose source leaf steps with another
+        # cadence than the reading tile get the stage source the interface pass
+        # computes once per (node, reader cadence)
+        if_gid = np.zeros(0, np.int32)
+        if_cad = np.zeros(0, np.int32)
+        if lts:
+            tcad = leaf_cad[tiles].astype(np.int64)
+            ct, ce = np.nonzero(table >= 0)
+            cg = table[ct, ce].astype(np.int64)
+            cm = node_cad[cg].astype(np.int64) != tcad[ct]
+            s_cad = tcad[slot_tile] if len(slot_tile) else np.zeros(0, np.int64)
+            sm = node_cad[slot_gid].astype(np.int64) != s_cad if len(slot_gid) else np.zeros(0, bool)
+            keys = np.concatenate([((31 - tcad[ct[cm]]) << 32) | cg[cm],
+                                   ((31 - s_cad[sm]) << 32) | slot_gid[sm].astype(np.int64)])
+            if len(keys):
+                ukeys, pinv = np.unique(keys, return_inverse=True)
+                ne = int(cm.sum())
+                table[ct[cm], ce[cm]] = (_IFACE_BASE - pinv[:ne]).astype(np.int32)
+                slot_gid = slot_gid.copy()
+                slot_gid[sm] = (-pinv[ne:] - 1).astype(np.int32)
+                if_gid = (ukeys & 0xFFFFFFFF).astype(np.int32)
+                if_cad = (31 - (ukeys >> 32)).astype(np.int32)
         # per-tile metadata in launch order: {g0, g1, level | cadence<<8 | faces<<16, leaf}
         starts, levels, a3 = td["starts"], td["level"], td["anchor3"]
         L = td["max_depth"]
@@ -372,7 +395,7 @@ class Engine:
                          tiles], axis=1).astype(np.int32)
         pad = lambda a, dt: a.astype(dt) if len(a) else np.zeros(1, dt)  # noqa: E731
         prog = dict(tile_slot_ptr=tile_slot_ptr, slot_gid=pad(slot_gid, np.int32),
-                    slot_cad=pad(node_cad[slot_gid] if len(slot_gid) else slot_gid, np.uint8),
+                    if_gid=pad(if_gid, np.int32), if_cad=pad(if_cad, np.int32), n_iface=len(if_gid),
                     tile_in_ptr=tile_in_ptr, in_tap_ptr=in_tap_ptr, tile_tap_ptr=in_tap_ptr[tile_in_ptr],
                     in_cell=pad(cross_cells[e_idx], np.uint16), tap=tap, wtab=wtab.astype(np.float64),
                     tile_meta=meta, cross_cells=cross_cells.astype(np.uint16), max_slots=max_slots)
@@ -391,9 +414,9 @@ class Engine:
         P.leaf_anchor, P.leaf_level = d["anchor"].data_ptr(), d["level"].data_ptr()
         P.leaf_cadence, P.leaf_start = d["cadence"].data_ptr(), d["starts"].data_ptr()
         P.node_cadence = d["node_cad"].data_ptr()
-        P.tile_src_cad = d["side"].data_ptr()
-        P.tile_slot_ptr, P.slot_gid, P.slot_cad = (d["tile_slot_ptr"].data_ptr(), d["slot_gid"].data_ptr(),
-                                                   d["slot_cad"].data_ptr())
+        P.tile_slot_ptr, P.slot_gid = d["tile_slot_ptr"].data_ptr(), d["slot_gid"].data_ptr()
+        P.if_gid, P.if_cad, P.ibuf = d["if_gid"].data_ptr(), d["if_cad"].data_ptr(), self._ibuf.data_ptr()
+        P.n_iface_total = self._n_iface
         P.tile_in_ptr, P.in_tap_ptr = d["tile_in_ptr"].data_ptr(), d["in_tap_ptr"].data_ptr()
         P.tile_tap_ptr = d["tile_tap_ptr"].data_ptr()
         P.in_cell, P.tile_meta, P.cross_cells = (d["in_cell"].data_ptr(), d["tile_meta"].data_ptr(),
@@ -571,6 +594,7 @@ class Engine:
         n_tiles = self._prefix[min(elig)] if elig else 0
         P = self._prm
         P.n_tiles = n_tiles
+        P.n_iface = self._if_prefix[min(elig)] if elig else 0
 
         if P.lts:
             P.coef = self._slice_coef(i).data_ptr()
@@ -585,6 +609,10 @@ class Engine:
             for t, j in enumerate(vt):
                 P.vt_j[t] = j
             if n_tiles:
+                if P.n_iface:
+                    rc = self._lib.amr_iface(C.byref(P), stream)
+                    if rc:
+                        _native.check(rc, "amr_iface")
                 rc = self._lib.amr_stage(C.byref(P), stream)
                 if rc:
                     _native.check(rc, "amr_stage")
@@ -615,7 +643,11 @@ class Engine:
             self.advance_slice()
 
     def launches_per_slice(self, i: int) -> int:
-        return self.p if self._eligible_cadences(i) else 0
+        """Kernel launches advance_slice(i) issues (stage + LTS interface passes)."""
+        el = self._eligible_cadences(i)
+        if not el:
+            return 0
+        return self.p * (2 if self._if_prefix[min(el)] else 1)
 
     def close(self):
         self._exchange = None
