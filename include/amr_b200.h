@@ -153,6 +153,7 @@ typedef struct {
   const uint16_t* in_cell;     /* [n_in] smem cell (padded ppo+4 box) the node fills */
   const int32_t* tile_meta;    /* [n_tiles][4] {first gid, end gid, level | cadence<<8 | faces<<16, leaf} */
   const uint16_t* cross_cells; /* [entries] padded-box cell of each stencil-cross entry */
+  const uint16_t* cross_pos;   /* [entries] interior position a0 | a1<<4 | a2<<8 (interior entries) */
   const uint32_t* tap;         /* [n_taps] (tile-local slot << 16) | weight id; rows padded to a multiple of
                                   4 taps with (zero slot = n_slots of the tile, weight 0) */
   const double* wtab;          /* distinct interpolation weights */

@@ -285,6 +285,25 @@ __device__ __forceinline__ double2 rhs_point(const Acc& acc, const int* pos, int
   return make_double2(dchi, dphi);
 }
 
+// interior fast path: no physical face on the tile and no coordinate-dependent
+// source: centred 4th-order Laplacian (+ cubic), dchi = phi (wave.py:147-170)
+template <int DIM, class Acc>
+__device__ __forceinline__ double2 rhs_interior(const Acc& acc, const Weights& W, const RhsConst& R) {
+  double lap = 0.0;
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) {
+    double t = W.d2c[0] * acc.at(0, d, -2);
+#pragma unroll
+    for (int k = 1; k < 5; ++k) t = t + W.d2c[k] * acc.at(0, d, k - 2);
+    t = R.pow2 ? t * R.inv_h2 : t / R.h2;
+    lap = (d == 0) ? t : lap + t;
+  }
+  const double chi = acc.at(0, 0, 0);
+  double dphi = lap;
+  if (R.nonlinear == 2) dphi = dphi - (chi * chi) * chi;
+  return make_double2(acc.at(1, 0, 0), dphi);
+}
+
 template <int DIM, int PPO>
 struct SmemAcc {
   const double* chi;
@@ -340,7 +359,7 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   constexpr int NK = NT > 0 ? NT : 1;
   __shared__ double s_chi[T::NS];
   __shared__ double s_phi[T::NS];
-  __shared__ short s_own[T::NI];
+  __shared__ int s_own[T::NI];  // owned node k: its smem cell | packed interior position << 12
   extern __shared__ double2 slotv[];  // [max_slots] slot stage sources, [1] zero slot, then [n_wtab] weights
   double* s_w = reinterpret_cast<double*>(slotv + P.max_slots + 1);
   const int64_t tile = blockIdx.x;
@@ -431,7 +450,7 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
     if (e >= T::NE || (g <= -2 && g > AMR_IFACE_BASE)) continue;  // hanging rows are written in 1d
     const int cell = __ldg(P.cross_cells + e);
     const bool own = e < T::NI && g >= g0 && g < g1;
-    if (own) s_own[g - g0] = (short)e;
+    if (own) s_own[g - g0] = cell | ((int)__ldg(P.cross_pos + e) << 12);
     double yc = 0.0, yp = 0.0;
     if (g >= 0) {
       yc = 0.0 + cu[i];
@@ -544,6 +563,7 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   R.nonlinear = P.nonlinear;
   constexpr int scale = PPO - 1;
   const bool need_x = faces != 0 || P.nonlinear == 1;  // radiative rows / sin(2chi)/r^2 need coordinates
+  const bool fast_rhs = !need_x;
   const int64_t side_len = (int64_t)1 << (P.max_depth - lvl);
   int32_t anc[3] = {0, 0, 0};
   if (need_x) {
@@ -556,16 +576,10 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   const int n_own = (int)(g1 - g0);
   for (int k = threadIdx.x; k < n_own; k += T::THREADS) {
     const int q = s_own[k];
+    const int cell = q & 0xFFF;
     int pos[3];
-    int r = q;
 #pragma unroll
-    for (int d = DIM - 1; d >= 0; --d) {
-      pos[d] = r % PPO;
-      r /= PPO;
-    }
-    int cell = 0;
-#pragma unroll
-    for (int d = 0; d < DIM; ++d) cell = cell * T::NP + (pos[d] + T::PAD);
+    for (int d = 0; d < DIM; ++d) pos[d] = (q >> (12 + 4 * d)) & 15;
     double x[3] = {0.0, 0.0, 0.0};
     if (need_x) {
 #pragma unroll
@@ -575,7 +589,7 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
       }
     }
     SmemAcc<DIM, PPO> acc{s_chi, s_phi, cell};
-    const double2 ks = rhs_point<DIM>(acc, pos, PPO, faces, x, W, R);
+    const double2 ks = fast_rhs ? rhs_interior<DIM>(acc, W, R) : rhs_point<DIM>(acc, pos, PPO, faces, x, W, R);
     const int64_t g = g0 + k;
     if (!last || LTS) {
       Ks[g] = ks.x;

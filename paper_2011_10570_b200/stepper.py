@@ -318,8 +318,10 @@ class Engine:
         NP = ppo + 4
         loc = _cross_local(np.arange(E), dim, ppo)
         cross_cells = np.zeros(E, dtype=np.int64)
+        cross_pos = np.zeros(E, dtype=np.int64)
         for d in range(dim):
             cross_cells = cross_cells * NP + loc[:, d]
+            cross_pos |= np.clip(loc[:, d] - 2, 0, 15) << (4 * d)
         t_idx, e_idx = np.nonzero(table <= -2)  # row-major: by tile, then entry
         rows = (-table[t_idx, e_idx] - 2).astype(np.int64)
         n_in = len(rows)
@@ -398,7 +400,8 @@ class Engine:
                     if_gid=pad(if_gid, np.int32), if_cad=pad(if_cad, np.int32), n_iface=len(if_gid),
                     tile_in_ptr=tile_in_ptr, in_tap_ptr=in_tap_ptr, tile_tap_ptr=in_tap_ptr[tile_in_ptr],
                     in_cell=pad(cross_cells[e_idx], np.uint16), tap=tap, wtab=wtab.astype(np.float64),
-                    tile_meta=meta, cross_cells=cross_cells.astype(np.uint16), max_slots=max_slots)
+                    tile_meta=meta, cross_cells=cross_cells.astype(np.uint16),
+                    cross_pos=cross_pos.astype(np.uint16), max_slots=max_slots)
         return table, prog
 
     def _make_params(self) -> _native.AmrStageParams:
@@ -421,6 +424,7 @@ class Engine:
         P.tile_tap_ptr = d["tile_tap_ptr"].data_ptr()
         P.in_cell, P.tile_meta, P.cross_cells = (d["in_cell"].data_ptr(), d["tile_meta"].data_ptr(),
                                                  d["cross_cells"].data_ptr())
+        P.cross_pos = d["cross_pos"].data_ptr()
         P.tap, P.wtab, P.n_wtab = d["tap"].data_ptr(), d["wtab"].data_ptr(), int(d["wtab"].numel())
         P.max_slots = self._max_slots
         P.U0, P.U1, P.K = self._U[0].data_ptr(), self._U[1].data_ptr(), self._K.data_ptr()
