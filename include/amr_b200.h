@@ -159,6 +159,7 @@ typedef struct {
   const double* wtab;          /* distinct interpolation weights */
   int64_t n_wtab;
   int max_slots;               /* largest slot set of any tile (dynamic shared memory) */
+  int64_t prefetch_dist;       /* tiles ahead to prefetch into L2 (resident CTAs of the launch; 0 = off) */
   int n_vt;                    /* verbatim stage-source terms at this stage (a[s][j] != 0) */
   int vt_j[AMR_MAXP];          /* their j */
   double* U0;                  /* [2][n_nodes]: the reference's zip layout (chi row, phi row) */

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/amr_b200.h"
@@ -87,6 +88,10 @@ __device__ __forceinline__ int cross_cell(int e) {
 
 // Fields are SoA, the reference's (nvars, n_nodes) zip layout: var v of node g
 // at base[v*n + g]; stage j of K at K + j*2n.
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 __device__ __forceinline__ double2 ld_pair(const double* __restrict__ base, int64_t n, int64_t g) {
   return make_double2(__ldg(base + g), __ldg(base + n + g));
 }
@@ -383,6 +388,31 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   }
   for (int i = threadIdx.x; i < P.n_wtab; i += T::THREADS) s_w[i] = P.wtab[i];
   if (threadIdx.x == 0) slotv[nslot] = make_double2(0.0, 0.0);  // zero slot of padding taps
+  // L2 prefetch for the tile that will take this CTA slot one wave later:
+  // its table, tap program and owned field ranges (compulsory DRAM misses
+  // then meet that tile in L2)
+  if (P.prefetch_dist > 0) {
+    const int64_t nt = tile + P.prefetch_dist;
+    if (nt < P.n_tiles) {
+      const char* tb = reinterpret_cast<const char*>(P.tile_table + nt * T::NE);
+      for (int off = threadIdx.x * 128; off < T::NE * 4; off += T::THREADS * 128) prefetch_l2(tb + off);
+      const int4 nm = __ldg(reinterpret_cast<const int4*>(P.tile_meta) + nt);
+      const int64_t a0 = __ldg(P.tile_tap_ptr + nt), a1 = __ldg(P.tile_tap_ptr + nt + 1);
+      const char* tp = reinterpret_cast<const char*>(P.tap + a0);
+      for (int64_t off = threadIdx.x * 128; off < (a1 - a0) * 4; off += T::THREADS * 128) prefetch_l2(tp + off);
+      const int ncur = LTS ? P.coef->cur[(nm.z >> 8) & 0xFF] : P.gts_cur;
+      const double* Un = ncur ? P.U1 : P.U0;
+      const int64_t nb = (int64_t)(nm.y - nm.x) * 8;
+      const int nstreams = 2 + 2 * NT;  // u chi/phi, and the verbatim K_j chi/phi
+      for (int64_t w = threadIdx.x; w < nstreams * ((nb + 127) / 128); w += T::THREADS) {
+        const int st = (int)(w / ((nb + 127) / 128));
+        const int64_t off = (w % ((nb + 127) / 128)) * 128;
+        const double* base = st < 2 ? Un + (int64_t)st * P.n_nodes
+                                    : P.K + (int64_t)P.vt_j[(st - 2) >> 1] * 2 * P.n_nodes + ((st - 2) & 1) * P.n_nodes;
+        prefetch_l2(reinterpret_cast<const char*>(base + nm.x) + off);
+      }
+    }
+  }
   const int4 meta = __ldg(reinterpret_cast<const int4*>(P.tile_meta) + tile);  // {g0, g1, lvl|cad<<8|faces<<16, leaf}
   const int leaf = meta.w;
   const int64_t g0 = meta.x;
@@ -698,7 +728,19 @@ int launch_stage_one(const AmrStageParams* p, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(stage_kernel)");
     configured = dyn;
   }
-  stage_kernel<DIM, PPO, LTS, NT><<<(unsigned)p->n_tiles, T::THREADS, dyn, st>>>(*p);
+  // L2 prefetch distance: one wave of resident CTAs (AMR_PREFETCH=0 disables)
+  static int wave = -1;
+  if (wave < 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage_kernel<DIM, PPO, LTS, NT>, T::THREADS, dyn);
+    const char* env = std::getenv("AMR_PREFETCH");
+    wave = (env && std::atoi(env) == 0) ? 0 : sms * (per_sm > 0 ? per_sm : 1);
+  }
+  AmrStageParams q = *p;
+  q.prefetch_dist = p->prefetch_dist < 0 ? wave : p->prefetch_dist;
+  stage_kernel<DIM, PPO, LTS, NT><<<(unsigned)p->n_tiles, T::THREADS, dyn, st>>>(q);
   return AMR_OK;
 }
 

@@ -411,6 +411,7 @@ class Engine:
         P.lts = 1 if self.mode == "lts" or any(c != self.l_max for c in self.cadence) else 0
         P.n_stages = self.p
         P.nonlinear = self._nl
+        P.prefetch_dist = -1  # auto: one wave of resident CTAs
         P.n_nodes = m.n_nodes
         d = self._d
         P.tile_ids, P.tile_table = d["tiles"].data_ptr(), d["table"].data_ptr()
