@@ -411,7 +411,7 @@ class Engine:
         P.lts = 1 if self.mode == "lts" or any(c != self.l_max for c in self.cadence) else 0
         P.n_stages = self.p
         P.nonlinear = self._nl
-        P.prefetch_dist = -1  # auto: one wave of resident CTAs
+        P.prefetch_dist = 0  # L2 prefetch of the next wave: measured neutral on cfg2 (-1 = auto)
         P.n_nodes = m.n_nodes
         d = self._d
         P.tile_ids, P.tile_table = d["tiles"].data_ptr(), d["table"].data_ptr()
@@ -640,8 +640,64 @@ class Engine:
     def lts_coarse_step(self) -> None:
         if self.i_fine % self.schedule.slices_per_round != 0:
             raise RuntimeError("blocks are not synchronized at a coarse time")
-        for _ in range(self.schedule.slices_per_round):
+        R = self.schedule.slices_per_round
+        if self.use_graphs and self._dist is None:
+            self._replay_round(R)
+            return
+        for _ in range(R):
             self.advance_slice()
+
+    # -- CUDA graphs ----------------------------------------------------------------------
+    use_graphs = True
+
+    def _replay_round(self, R: int) -> None:
+        """One coarse round as a captured CUDA graph.  The launch sequence of a
+        round depends only on the round parity (coefficient blocks, buffer
+        parities), so two graphs cover every round.  The first round of each
+        parity runs eagerly (warm-up: kernel attributes, coefficient blocks),
+        the second is captured, later ones replay."""
+        import torch
+
+        key = (self.i_fine // R) & 1
+        g = self._graphs.get(key) if hasattr(self, "_graphs") else None
+        if g is None:
+            if not hasattr(self, "_graphs"):
+                self._graphs, self._graph_seen = {}, set()
+            if key not in self._graph_seen:
+                self._graph_seen.add(key)
+                for _ in range(R):
+                    self.advance_slice()
+                return
+            i0 = self.i_fine
+            for j in range(R):  # coefficient blocks must exist before capture
+                self._slice_coef(i0 + j) if self._prm.lts else None
+            torch.cuda.synchronize(self.device)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                for _ in range(R):
+                    self.advance_slice()
+            # capture recorded the launches without running them: run once now
+            self._graphs[key] = graph
+            self.i_fine = i0
+            self._untally_round(i0, R)
+            graph.replay()
+            self._tally_round(i0, R)
+            self.i_fine = i0 + R
+            return
+        i0 = self.i_fine
+        g.replay()
+        self._tally_round(i0, R)
+        self.i_fine = i0 + R
+
+    def _tally_round(self, i0: int, R: int) -> None:
+        for i in range(i0, i0 + R):
+            self.counters._tally(self._eligible_cadences(i))
+
+    def _untally_round(self, i0: int, R: int) -> None:
+        for i in range(i0, i0 + R):
+            for c in self._eligible_cadences(i):
+                self.counters._steps_total[c] -= 1
+                self.counters._steps_work[c] -= 1
 
     def run_to(self, i_fine_target: int) -> None:
         while self.i_fine < i_fine_target:

@@ -88,3 +88,24 @@ def test_ball_dom2_fields_match_reference(cuda, tag):
     _run_case(mesh, gaussian_pulse((0.0, 0.0), 0.8, 1.0), gd, "ball_", tag, results, runs)
     print(results)
     _assert_results(results)
+
+
+def test_graph_replayed_rounds_equal_eager(cuda):
+    """lts_coarse_step replays captured CUDA graphs (two round parities); the
+    result must be bit-identical to eager slices and to the reference."""
+    gd = golden("cfg1")
+    mesh = config_mesh("cfg1")
+    outs, counts = [], []
+    for graphs in (True, False):
+        eng = Engine(mesh, tableau="rk4", cfl=0.25, mode="lts")
+        eng.use_graphs = graphs
+        eng.initialize(CONFIGS["cfg1"].chi0())
+        for _ in range(8):  # eager warm-up rounds, capture, replays of both parities
+            eng.lts_coarse_step()
+        assert eng.i_fine == 64
+        outs.append(eng.current_zip())
+        counts.append((eng.counters.point_steps, dict(eng.counters.steps_by_level)))
+    assert np.array_equal(outs[0], outs[1])
+    assert counts[0] == counts[1]
+    exact, rel = compare_field(outs[0], gd, "lts_rk4_i64")
+    assert exact, rel
