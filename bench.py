@@ -196,8 +196,11 @@ def time_rounds(eng, steps, torch, dist, per_launch=False):
     start.record(stream)
     n_slices = eng.schedule.slices_per_round
     for _ in range(steps):
-        for _ in range(n_slices):
-            eng.advance_slice()
+        if per_launch:  # eager slices so every launch can be bracketed by events
+            for _ in range(n_slices):
+                eng.advance_slice()
+        else:  # the public API: one coarse round (CUDA-graph replay after warm-up)
+            eng.lts_coarse_step()
     end.record(stream)
     torch.cuda.synchronize(dev)
     if dist is not None:
