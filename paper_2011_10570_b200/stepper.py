@@ -653,39 +653,33 @@ class Engine:
     def _replay_round(self, R: int) -> None:
         """One coarse round as a captured CUDA graph.  The launch sequence of a
         round depends only on the round parity (coefficient blocks, buffer
-        parities), so two graphs cover every round.  The first round of each
-        parity runs eagerly (warm-up: kernel attributes, coefficient blocks),
-        the second is captured, later ones replay."""
+        parities), so two graphs cover every round.  The first round runs
+        eagerly (kernel attributes, coefficient blocks); both graphs are then
+        recorded (capture does not execute) and every later round replays."""
         import torch
 
-        key = (self.i_fine // R) & 1
-        g = self._graphs.get(key) if hasattr(self, "_graphs") else None
-        if g is None:
-            if not hasattr(self, "_graphs"):
-                self._graphs, self._graph_seen = {}, set()
-            if key not in self._graph_seen:
-                self._graph_seen.add(key)
-                for _ in range(R):
-                    self.advance_slice()
-                return
-            i0 = self.i_fine
-            for j in range(R):  # coefficient blocks must exist before capture
-                self._slice_coef(i0 + j) if self._prm.lts else None
+        if not hasattr(self, "_graphs"):
+            self._graphs = {}
+        if not self._graphs:
+            for _ in range(R):
+                self.advance_slice()
+            i_next = self.i_fine
+            for i in range(i_next, i_next + 2 * R):  # coefficient blocks of both parities
+                if self._prm.lts:
+                    self._slice_coef(i)
             torch.cuda.synchronize(self.device)
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
-                for _ in range(R):
-                    self.advance_slice()
-            # capture recorded the launches without running them: run once now
-            self._graphs[key] = graph
-            self.i_fine = i0
-            self._untally_round(i0, R)
-            graph.replay()
-            self._tally_round(i0, R)
-            self.i_fine = i0 + R
+            for start in (i_next, i_next + R):
+                graph = torch.cuda.CUDAGraph()
+                self.i_fine = start
+                with torch.cuda.graph(graph):
+                    for _ in range(R):
+                        self.advance_slice()
+                self._untally_round(start, R)
+                self._graphs[(start // R) & 1] = graph
+            self.i_fine = i_next
             return
         i0 = self.i_fine
-        g.replay()
+        self._graphs[(i0 // R) & 1].replay()
         self._tally_round(i0, R)
         self.i_fine = i0 + R
 
