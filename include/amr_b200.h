@@ -160,8 +160,9 @@ typedef struct {
   int64_t n_wtab;
   int max_slots;               /* largest slot set of any tile (dynamic shared memory) */
   int64_t prefetch_dist;       /* tiles ahead to prefetch into L2 (resident CTAs of the launch; 0 = off) */
-  int n_vt;                    /* verbatim stage-source terms at this stage (a[s][j] != 0) */
+  int n_vt;                    /* verbatim stage-source terms of stage s+1 (a[s+1][j] != 0) */
   int vt_j[AMR_MAXP];          /* their j */
+  double* Y;                   /* [2][n_nodes]: verbatim source of stage s+1, written by the owners at stage s */
   double* U0;                  /* [2][n_nodes]: the reference's zip layout (chi row, phi row) */
   double* U1;
   double* K;                   /* [n_stages][2][n_nodes] */

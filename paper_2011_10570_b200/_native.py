@@ -49,7 +49,7 @@ class AmrStageParams(C.Structure):
         ("in_tap_ptr", _vp), ("tile_tap_ptr", _vp), ("in_cell", _vp), ("tile_meta", _vp), ("cross_cells", _vp), ("cross_pos", _vp), ("tap", _vp), ("wtab", _vp), ("n_wtab", C.c_int64),
         ("max_slots", C.c_int),
         ("prefetch_dist", C.c_int64),
-        ("n_vt", C.c_int), ("vt_j", C.c_int * AMR_MAXP),
+        ("n_vt", C.c_int), ("vt_j", C.c_int * AMR_MAXP), ("Y", _vp),
         ("U0", _vp), ("U1", _vp), ("K", _vp),
         ("coef", _vp),
         ("g_cstage", (C.c_double * AMR_MAXP) * AMR_MAXP),

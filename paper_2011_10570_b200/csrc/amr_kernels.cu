@@ -361,7 +361,6 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   constexpr int EPT = (T::NE + T::THREADS - 1) / T::THREADS;
   constexpr int EPI = (T::NI + T::THREADS - 1) / T::THREADS;  // entries per thread inside the leaf (e < NI)
   constexpr int SPT = 2;                                      // slots per thread issued with the gathers
-  constexpr int NK = NT > 0 ? NT : 1;
   __shared__ double s_chi[T::NS];
   __shared__ double s_phi[T::NS];
   __shared__ int s_own[T::NI];  // owned node k: its smem cell | packed interior position << 12
@@ -430,33 +429,23 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   const int64_t nib = P.n_iface_total;
   const AmrSliceCoef* C = P.coef;
   const bool phi_all = faces != 0;  // radiative rows need phi gradients: phi on the whole cross
-  int js[NK];
-  double cs[NK];
-#pragma unroll
-  for (int t = 0; t < NK; ++t) {
-    js[t] = t < NT ? P.vt_j[t] : 0;
-    cs[t] = t < NT ? (LTS ? C->cstage[cad][s][js[t]] : P.g_cstage[s][js[t]]) : 0.0;
-  }
   const int cur = LTS ? C->cur[cad] : P.gts_cur;
   const double* Ucur = cur ? U1 : U0;
+  // verbatim stage sources: u at stage 0; at stage s > 0 the Y the owners wrote
+  // in stage s-1 (Y = (0 + u) + sum_j dt a_sj K_j, stepper.py:290-296)
+  const double* V = (s == 0) ? Ucur : P.Y;
 
-  // ---- 1b: every gather of this thread in flight at once.  Copy entries are
-  //      verbatim (same cadence); LTS interface entries read the transfer the
-  //      interface pass computed for (node, this cadence).
-  double cu[EPT], ck[EPT][NK], pu[EPI], pk[EPI][NK];
-  double2 su[SPT], sk[SPT][NK];
+  // ---- 1b: every gather of this thread in flight at once: one verbatim value
+  //      per copy entry and slot (chi; phi only where the stencil reads it);
+  //      LTS interface entries read the transfer of the interface pass.
+  double cu[EPT], pu[EPI];
+  double2 su[SPT];
 #pragma unroll
   for (int i = 0; i < EPT; ++i) {
     const int g = ent[i];
     if (g >= 0) {
-      cu[i] = __ldg(Ucur + g);
-#pragma unroll
-      for (int t = 0; t < NT; ++t) ck[i][t] = __ldg(K + (int64_t)js[t] * 2 * n + g);
-      if (i < EPI && (phi_all || (g >= g0 && g < g1))) {
-        pu[i] = __ldg(Ucur + n + g);
-#pragma unroll
-        for (int t = 0; t < NT; ++t) pk[i][t] = __ldg(K + (int64_t)js[t] * 2 * n + n + g);
-      }
+      cu[i] = __ldg(V + g);
+      if (i < EPI && (phi_all || (g >= g0 && g < g1))) pu[i] = __ldg(V + n + g);
     } else if (LTS && g <= AMR_IFACE_BASE) {
       cu[i] = __ldg(IB + (AMR_IFACE_BASE - g));
     }
@@ -465,9 +454,7 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   for (int i = 0; i < SPT; ++i) {
     const int g = sg[i];
     if (g >= 0) {
-      su[i] = ld_pair(Ucur, n, g);
-#pragma unroll
-      for (int t = 0; t < NT; ++t) sk[i][t] = ld_pair(K + (int64_t)js[t] * 2 * n, n, g);
+      su[i] = ld_pair(V, n, g);
     } else if (LTS && g != INT32_MIN) {
       su[i] = make_double2(__ldg(IB + (-g - 1)), __ldg(IB + nib + (-g - 1)));
     }
@@ -483,20 +470,11 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
     if (own) s_own[g - g0] = cell | ((int)__ldg(P.cross_pos + e) << 12);
     double yc = 0.0, yp = 0.0;
     if (g >= 0) {
-      yc = 0.0 + cu[i];
-#pragma unroll
-      for (int t = 0; t < NT; ++t) yc = yc + cs[t] * ck[i][t];
-      yc = 0.0 + yc;  // copy row: 0 + 1.0*src
+      // copy row 0 + 1.0*src; at stage 0 the source itself is 0 + u
+      yc = (s == 0) ? 0.0 + (0.0 + cu[i]) : 0.0 + cu[i];
       if (phi_all || own) {
-        if (i < EPI) {
-          yp = 0.0 + pu[i];
-#pragma unroll
-          for (int t = 0; t < NT; ++t) yp = yp + cs[t] * pk[i][t];
-        } else {  // halo phi of a face tile (rare)
-          yp = 0.0 + __ldg(Ucur + n + g);
-          for (int t = 0; t < NT; ++t) yp = yp + cs[t] * __ldg(K + (int64_t)js[t] * 2 * n + n + g);
-        }
-        yp = 0.0 + yp;
+        const double vp = (i < EPI) ? pu[i] : __ldg(V + n + g);  // halo phi of a face tile (rare)
+        yp = (s == 0) ? 0.0 + (0.0 + vp) : 0.0 + vp;
       }
     } else if (LTS && g <= AMR_IFACE_BASE) {
       yc = 0.0 + cu[i];
@@ -509,15 +487,8 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   for (int i = 0; i < SPT; ++i) {
     const int g = sg[i];
     if (g == INT32_MIN) continue;
-    double2 y = su[i];  // interface source, or the verbatim source below
-    if (g >= 0) {
-      y = make_double2(0.0 + su[i].x, 0.0 + su[i].y);
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        y.x = y.x + cs[t] * sk[i][t].x;
-        y.y = y.y + cs[t] * sk[i][t].y;
-      }
-    }
+    double2 y = su[i];  // interface source, or the verbatim source
+    if (g >= 0 && s == 0) y = make_double2(0.0 + su[i].x, 0.0 + su[i].y);
     slotv[threadIdx.x + i * T::THREADS] = y;
   }
   for (int k = threadIdx.x + SPT * T::THREADS; k < nslot; k += T::THREADS) {  // very large interface tiles
@@ -525,13 +496,8 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
     if (LTS && g < 0) {
       slotv[k] = make_double2(__ldg(IB + (-g - 1)), __ldg(IB + nib + (-g - 1)));
     } else {
-      double2 y = ld_pair(Ucur, n, g);
-      y = make_double2(0.0 + y.x, 0.0 + y.y);
-      for (int t = 0; t < NT; ++t) {
-        const double2 kk = ld_pair(K + (int64_t)js[t] * 2 * n, n, g);
-        y.x = y.x + cs[t] * kk.x;
-        y.y = y.y + cs[t] * kk.y;
-      }
+      double2 y = ld_pair(V, n, g);
+      if (s == 0) y = make_double2(0.0 + y.x, 0.0 + y.y);
       slotv[k] = y;
     }
   }
@@ -624,6 +590,20 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
     if (!last || LTS) {
       Ks[g] = ks.x;
       Ks[n + g] = ks.y;
+    }
+    if (!last) {  // next stage's verbatim source of this owned node
+      double yx = 0.0 + __ldg(Ucur + g), yy = 0.0 + __ldg(Ucur + n + g);
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const int j = P.vt_j[t];
+        const double c = LTS ? C->cstage[cad][s + 1][j] : P.g_cstage[s + 1][j];
+        const double kx = (j == s) ? ks.x : __ldg(K + (int64_t)j * 2 * n + g);
+        const double ky = (j == s) ? ks.y : __ldg(K + (int64_t)j * 2 * n + n + g);
+        yx = yx + c * kx;
+        yy = yy + c * ky;
+      }
+      P.Y[g] = yx;
+      P.Y[n + g] = yy;
     }
     if (last) {
       double ux = 0.0 + __ldg(Ucur + g), uy = 0.0 + __ldg(Ucur + n + g);

@@ -277,6 +277,7 @@ class Engine:
         # the reference's (nvars, n_nodes) zip layout, SoA: chi row then phi row
         self._U = [torch.zeros((2, n), dtype=torch.float64, device=dev) for _ in range(2)]
         self._K = torch.zeros((self.p, 2, n), dtype=torch.float64, device=dev)
+        self._Y = torch.zeros((2, n), dtype=torch.float64, device=dev)  # next stage's verbatim sources
         self._node_cad_t = self._d["node_cad"].long()
         self._vt = [[j for j in range(s_) if self.tab.a[s_][j] != 0.0] for s_ in range(self.p)]
         self._prm = self._make_params()
@@ -429,6 +430,7 @@ class Engine:
         P.tap, P.wtab, P.n_wtab = d["tap"].data_ptr(), d["wtab"].data_ptr(), int(d["wtab"].numel())
         P.max_slots = self._max_slots
         P.U0, P.U1, P.K = self._U[0].data_ptr(), self._U[1].data_ptr(), self._K.data_ptr()
+        P.Y = self._Y.data_ptr()
         for s in range(self.p):
             for j in range(self.p):
                 a = self.tab.a[s][j]
@@ -609,7 +611,7 @@ class Engine:
         t0 = time.perf_counter()
         for s in range(self.p):
             P.stage = s
-            vt = self._vt[s]
+            vt = self._vt[s + 1] if s + 1 < self.p else []  # the writer forms stage s+1's sources
             P.n_vt = len(vt)
             for t, j in enumerate(vt):
                 P.vt_j[t] = j
@@ -818,6 +820,8 @@ class _EngineExchange:
         if elig:
             t0 = time.perf_counter()
             self.gx.swap_from_cadence(self.eng._K[s], min(elig))
+            if s + 1 < self.eng.p:  # the verbatim sources the owners formed for stage s+1
+                self.gx.swap_from_cadence(self.eng._Y, min(elig))
             self.eng.counters.phases["comm"] += time.perf_counter() - t0
 
     def after_step(self, i: int, elig: list[int]) -> None:
