@@ -162,7 +162,8 @@ typedef struct {
   int64_t prefetch_dist;       /* tiles ahead to prefetch into L2 (resident CTAs of the launch; 0 = off) */
   int n_vt;                    /* verbatim stage-source terms of stage s+1 (a[s+1][j] != 0) */
   int vt_j[AMR_MAXP];          /* their j */
-  double* Y;                   /* [2][n_nodes]: verbatim source of stage s+1, written by the owners at stage s */
+  double* Y;                   /* [2 buffers][2][n_nodes]: verbatim sources; stage s reads buffer s&1 and its
+                                  owners write stage s+1's into buffer (s+1)&1 */
   double* U0;                  /* [2][n_nodes]: the reference's zip layout (chi row, phi row) */
   double* U1;
   double* K;                   /* [n_stages][2][n_nodes] */

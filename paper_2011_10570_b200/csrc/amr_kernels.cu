@@ -433,7 +433,8 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   const double* Ucur = cur ? U1 : U0;
   // verbatim stage sources: u at stage 0; at stage s > 0 the Y the owners wrote
   // in stage s-1 (Y = (0 + u) + sum_j dt a_sj K_j, stepper.py:290-296)
-  const double* V = (s == 0) ? Ucur : P.Y;
+  // Y is double-buffered by stage parity: stage s reads Y[s&1], writes Y[(s+1)&1]
+  const double* V = (s == 0) ? Ucur : P.Y + (int64_t)(s & 1) * 2 * n;
 
   // ---- 1b: every gather of this thread in flight at once: one verbatim value
   //      per copy entry and slot (chi; phi only where the stencil reads it);
@@ -602,8 +603,9 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
         yx = yx + c * kx;
         yy = yy + c * ky;
       }
-      P.Y[g] = yx;
-      P.Y[n + g] = yy;
+      double* Yout = P.Y + (int64_t)((s + 1) & 1) * 2 * n;
+      Yout[g] = yx;
+      Yout[n + g] = yy;
     }
     if (last) {
       double ux = 0.0 + __ldg(Ucur + g), uy = 0.0 + __ldg(Ucur + n + g);

@@ -277,7 +277,8 @@ class Engine:
         # the reference's (nvars, n_nodes) zip layout, SoA: chi row then phi row
         self._U = [torch.zeros((2, n), dtype=torch.float64, device=dev) for _ in range(2)]
         self._K = torch.zeros((self.p, 2, n), dtype=torch.float64, device=dev)
-        self._Y = torch.zeros((2, n), dtype=torch.float64, device=dev)  # next stage's verbatim sources
+        # verbatim stage sources, double-buffered by stage parity
+        self._Y = torch.zeros((2, 2, n), dtype=torch.float64, device=dev)
         self._node_cad_t = self._d["node_cad"].long()
         self._vt = [[j for j in range(s_) if self.tab.a[s_][j] != 0.0] for s_ in range(self.p)]
         self._prm = self._make_params()
@@ -821,7 +822,7 @@ class _EngineExchange:
             t0 = time.perf_counter()
             self.gx.swap_from_cadence(self.eng._K[s], min(elig))
             if s + 1 < self.eng.p:  # the verbatim sources the owners formed for stage s+1
-                self.gx.swap_from_cadence(self.eng._Y, min(elig))
+                self.gx.swap_from_cadence(self.eng._Y[(s + 1) & 1], min(elig))
             self.eng.counters.phases["comm"] += time.perf_counter() - t0
 
     def after_step(self, i: int, elig: list[int]) -> None:
