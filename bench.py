@@ -122,6 +122,16 @@ class ClockSampler:
                 "samples": len(sm), "samples_total": n_all}
 
 
+def _workload(name: str) -> str:
+    from paper_2011_10570_b200.configs import CONFIGS
+
+    c = CONFIGS[name]
+    src = {False: "linear", "cubic": "cubic", "sin": "sin"}[c.nonlinear]
+    levels = {"cfg1": "3-6", "cfg2": "3-7", "cfg3": "4-9", "cfg4": "2-13", "cfg5": "4-12"}.get(name, "?")
+    return (f"{name}: {c.dim}D {src} wave on [-1,1]^{c.dim}, levels {levels}, ppo {c.ppo}, pad {c.pad}, "
+            f"{c.tableau.upper()}, CFL {c.cfl}; step = one LTS coarse round")
+
+
 def _ncu_traffic():
     """DRAM bytes per stage launch from the committed ncu capture
     (profiles/traffic.json, written by tools/ncu_traffic.py from one
@@ -330,8 +340,7 @@ def run_ours(args):
         "dtype": "f64",
         "data": "synthetic (BASELINE configs[1] mesh; Gaussian pulse initial data)",
         "config": {
-            "workload": f"{args.config}: 3D linear wave, levels 3-7 (nested spheres 0.4/0.2/0.1), ppo 9, pad 2, "
-                        "RK4, CFL 0.25; step = one LTS coarse round (16 fine slices)",
+            "workload": _workload(args.config),
             "leaves": len(mesh.tree.leaves), "zip_nodes": mesh.n_nodes,
             "l2_policy": "inputs larger than L2 (state u0,u1,K0..K3 = "
                          f"{6 * 16 * mesh.n_nodes / 1e6:.0f} MB > 126 MB)",
@@ -424,8 +433,7 @@ def run_reference(args):
         "unit": "updates/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (BASELINE configs[1])",
-        "config": {"workload": f"{args.config}: step = one LTS coarse round ({R} fine slices)",
-                   "zip_nodes": m.n_nodes},
+        "config": {"workload": _workload(args.config), "zip_nodes": m.n_nodes},
         "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": "port",
                          "sample": f"{args.steps} LTS rounds of {args.config} on the oracle port "
                                    "(the reference amrlts is pure Python and not present on the GPU box)"},

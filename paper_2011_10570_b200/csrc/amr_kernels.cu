@@ -361,11 +361,14 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   constexpr int EPT = (T::NE + T::THREADS - 1) / T::THREADS;
   constexpr int EPI = (T::NI + T::THREADS - 1) / T::THREADS;  // entries per thread inside the leaf (e < NI)
   constexpr int SPT = 2;                                      // slots per thread issued with the gathers
-  __shared__ double s_chi[T::NS];
-  __shared__ double s_phi[T::NS];
   __shared__ int s_own[T::NI];  // owned node k: its smem cell | packed interior position << 12
-  extern __shared__ double2 slotv[];  // [max_slots] slot stage sources, [1] zero slot, then [n_wtab] weights
-  double* s_w = reinterpret_cast<double*>(slotv + P.max_slots + 1);
+  // dynamic: the tile's slot sources (+ zero slot), the stencil input (chi,
+  // phi) on the padded box, the interpolation weights
+  extern __shared__ double2 dyn_smem[];
+  double2* slotv = dyn_smem;                                    // [max_slots + 1]
+  double* s_chi = reinterpret_cast<double*>(slotv + P.max_slots + 1);  // [NS]
+  double* s_phi = s_chi + T::NS;                                // [NS]
+  double* s_w = s_phi + T::NS;                                  // [n_wtab]
   const int64_t tile = blockIdx.x;
   const int32_t* __restrict__ tab = P.tile_table + tile * T::NE;
   // ---- 1a
@@ -503,6 +506,15 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
     }
   }
   __syncthreads();
+  // u at this thread's owned nodes, for the epilogue: loaded now, in flight
+  // during the hanging-row sums (owned node k is handled by thread k % THREADS)
+  constexpr int OPT = (T::NI + T::THREADS - 1) / T::THREADS;
+  double2 uo[OPT];
+#pragma unroll
+  for (int r = 0; r < OPT; ++r) {
+    const int64_t g = g0 + threadIdx.x + r * T::THREADS;
+    uo[r] = g < g1 ? ld_pair(Ucur, n, g) : make_double2(0.0, 0.0);
+  }
   // ---- 1d: hanging rows, 0 + sum_k w_k src(g_k) in ascending-gid order
   //      (mesh.py:316-351; scipy csr_matvecs, mesh.py:418).  Rows hold a
   //      multiple of 4 taps (padding taps: weight 0 on the zero slot, which
@@ -571,7 +583,10 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   double* Unew = cur ? P.U0 : P.U1;
   double* Ks = P.K + (int64_t)s * 2 * n;
   const int n_own = (int)(g1 - g0);
-  for (int k = threadIdx.x; k < n_own; k += T::THREADS) {
+#pragma unroll
+  for (int r = 0; r < OPT; ++r) {
+    const int k = threadIdx.x + r * T::THREADS;
+    if (k >= n_own) break;
     const int q = s_own[k];
     const int cell = q & 0xFFF;
     int pos[3];
@@ -593,7 +608,7 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
       Ks[n + g] = ks.y;
     }
     if (!last) {  // next stage's verbatim source of this owned node
-      double yx = 0.0 + __ldg(Ucur + g), yy = 0.0 + __ldg(Ucur + n + g);
+      double yx = 0.0 + uo[r].x, yy = 0.0 + uo[r].y;
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
         const int j = P.vt_j[t];
@@ -608,7 +623,7 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
       Yout[n + g] = yy;
     }
     if (last) {
-      double ux = 0.0 + __ldg(Ucur + g), uy = 0.0 + __ldg(Ucur + n + g);
+      double ux = 0.0 + uo[r].x, uy = 0.0 + uo[r].y;
       for (int j = 0; j < p; ++j) {
         const double c = LTS ? C->comb[cad][j] : P.g_comb[j];
         if (c == 0.0) continue;
@@ -702,7 +717,7 @@ __global__ void pack_kernel(int64_t n_ranges, const int64_t* __restrict__ start,
 template <int DIM, int PPO, bool LTS, int NT>
 int launch_stage_one(const AmrStageParams* p, cudaStream_t st) {
   using T = Tile<DIM, PPO>;
-  const size_t dyn = sizeof(double2) * (size_t)(p->max_slots + 1) + sizeof(double) * (size_t)p->n_wtab;
+  const size_t dyn = sizeof(double2) * (size_t)(p->max_slots + 1) + sizeof(double) * (size_t)(2 * T::NS + p->n_wtab);
   static size_t configured = 0;
   if (dyn > configured) {
     cudaError_t e = cudaFuncSetAttribute(stage_kernel<DIM, PPO, LTS, NT>,

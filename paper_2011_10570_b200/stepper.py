@@ -326,6 +326,11 @@ class Engine:
             cross_pos |= np.clip(loc[:, d] - 2, 0, 15) << (4 * d)
         t_idx, e_idx = np.nonzero(table <= -2)  # row-major: by tile, then entry
         rows = (-table[t_idx, e_idx] - 2).astype(np.int64)
+        # within a tile, longest rows first: thread t sums rows t, t+256, ... so
+        # this balances the sequential sums across threads (any order is exact)
+        cnt0 = ptr[rows + 1] - ptr[rows]
+        order = np.lexsort((e_idx, -cnt0, t_idx))
+        t_idx, e_idx, rows = t_idx[order], e_idx[order], rows[order]
         n_in = len(rows)
         tile_in_ptr = np.zeros(nt + 1, dtype=np.int64)
         np.cumsum(np.bincount(t_idx, minlength=nt), out=tile_in_ptr[1:])
