@@ -211,6 +211,11 @@ CONFIGS: dict[str, WaveConfig] = {
         nonlinear="cubic", pulse_centers=_CFG5_C, pulse_amps=_CFG5_A, pulse_width=0.02,
         t_end=0.390625,
     ),
+    # uniform level-5 3D mesh (32 768 leaves, no level interfaces): the tile
+    # kernel's best case, for performance diagnosis only
+    "uni5": WaveConfig(
+        "uni5", 3, 5, BandRefine(5, (), ((0.0, 0.0, 0.0),)), pulse_width=0.2, t_end=1.0,
+    ),
     # small 3D mesh for goldens and fast parity (levels 2-4)
     "mini3d": WaveConfig(
         "mini3d", 3, 4, BandRefine(2, ((0.6, 3), (0.25, 4)), ((0.1, 0.0, 0.0),)),
