@@ -115,6 +115,45 @@ class SphereSeeds:
 
 
 @dataclass(frozen=True)
+class GradedSpheres:
+    """Per-sphere graded refinement: sphere (c, r) with target level
+    lmax - round(log2(r / 0.005)) (small spheres refine deepest) refines boxes
+    within rscale*r*2^k of its centre to target - k (BASELINE cfg4)."""
+
+    base: int
+    lmax: int
+    spheres: tuple
+    rscale: float = 1.0
+    lo: float = -1.0
+    hi: float = 1.0
+
+    def _targets(self):
+        return [(c, r * self.rscale, min(self.lmax, self.lmax - int(round(math.log2(r / 0.005)))))
+                for c, r, _ in self.spheres]
+
+    def __call__(self, key) -> bool:
+        if key.level < self.base:
+            return True
+        for c, r, lt in self._targets():
+            d2 = box_dist2(key, c, self.lo, self.hi)
+            for k in range(8):
+                if key.level < lt - k and d2 < (r * 2 ** k) ** 2:
+                    return True
+        return False
+
+    def batch(self, anchors: np.ndarray, level: int, max_depth: int) -> np.ndarray:
+        if level < self.base:
+            return np.ones(len(anchors), dtype=bool)
+        out = np.zeros(len(anchors), dtype=bool)
+        for c, r, lt in self._targets():
+            d2 = box_dist2_batch(anchors, level, max_depth, c, self.lo, self.hi)
+            for k in range(8):
+                if level < lt - k:
+                    out |= d2 < (r * 2 ** k) ** 2
+        return out
+
+
+@dataclass(frozen=True)
 class WaveConfig:
     name: str
     dim: int
@@ -197,9 +236,11 @@ CONFIGS: dict[str, WaveConfig] = {
         nonlinear="cubic", pulse_centers=((-0.3, 0.0, 0.0), (0.3, 0.0, 0.0)),
         pulse_amps=(1.0, 1.0), pulse_width=0.05, t_end=1.0,
     ),
-    # configs[3]: deep adaptivity, levels 2-13 around 16 seeded spheres
+    # configs[3]: deep adaptivity, levels 2-13 around 16 seeded spheres; graded
+    # refinement calibrated (rscale 0.25) to BASELINE's ~50 M points: 108 298
+    # leaves after balance
     "cfg4": WaveConfig(
-        "cfg4", 3, 13, SphereSeeds(2, _cfg4_spheres()),
+        "cfg4", 3, 13, GradedSpheres(2, 13, _cfg4_spheres(), rscale=0.25),
         pulse_centers=tuple(s[0] for s in _cfg4_spheres()), pulse_amps=(0.5,) * 16,
         pulse_width=0.05, t_end=1.0,
         note="random-phase superposition defined as 16 Gaussians at the sphere centres",
@@ -207,7 +248,8 @@ CONFIGS: dict[str, WaveConfig] = {
     # configs[4]: 64 Gaussian sources, levels 4-12, cubic
     "cfg5": WaveConfig(
         "cfg5", 3, 12,
-        BandRefine(4, ((0.3, 6), (0.1, 8), (0.04, 10), (0.01, 12)), _CFG5_C),
+        # bands calibrated (x0.5) to BASELINE's ~500 M points: 1 216 972 leaves after balance
+        BandRefine(4, ((0.15, 6), (0.05, 8), (0.02, 10), (0.005, 12)), _CFG5_C),
         nonlinear="cubic", pulse_centers=_CFG5_C, pulse_amps=_CFG5_A, pulse_width=0.02,
         t_end=0.390625,
     ),
