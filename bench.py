@@ -338,7 +338,7 @@ def run_ours(args):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (BASELINE configs[1] mesh; Gaussian pulse initial data)",
+        "data": f"synthetic ({args.config} mesh and Gaussian initial data, seeded; no dataset exists for this path)",
         "config": {
             "workload": _workload(args.config),
             "leaves": len(mesh.tree.leaves), "zip_nodes": mesh.n_nodes,
