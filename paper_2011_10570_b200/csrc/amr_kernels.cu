@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(256) iface_kernel(const AmrStageParams P) {
   if (i >= P.n_iface) return;
   const int g = __ldg(P.if_gid + i);
   const int lr = __ldg(P.if_cad + i);
-  const double2 v = lts_source(P.U0, P.U1, P.K, P.n_nodes, P.n_stages, g, P.stage, lr, P.node_cadence[g], P.coef);
+  const double2 v = lts_source(P.U0, P.U1, P.K, P.ld, P.n_stages, g, P.stage, lr, P.node_cadence[g], P.coef);
   P.ibuf[i] = v.x;
   P.ibuf[P.n_iface_total + i] = v.y;
 }
@@ -409,8 +409,8 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
       for (int64_t w = threadIdx.x; w < nstreams * ((nb + 127) / 128); w += T::THREADS) {
         const int st = (int)(w / ((nb + 127) / 128));
         const int64_t off = (w % ((nb + 127) / 128)) * 128;
-        const double* base = st < 2 ? Un + (int64_t)st * P.n_nodes
-                                    : P.K + (int64_t)P.vt_j[(st - 2) >> 1] * 2 * P.n_nodes + ((st - 2) & 1) * P.n_nodes;
+        const double* base = st < 2 ? Un + (int64_t)st * P.ld
+                                    : P.K + (int64_t)P.vt_j[(st - 2) >> 1] * 2 * P.ld + ((st - 2) & 1) * P.ld;
         prefetch_l2(reinterpret_cast<const char*>(base + nm.x) + off);
       }
     }
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   const int cad = (meta.z >> 8) & 0xFF;
   const int faces = (meta.z >> 16) & 0x3F;
   const int s = P.stage;
-  const int64_t n = P.n_nodes;
+  const int64_t n = P.ld;  // row stride of the field arrays
   const int p = P.n_stages;
   const double* U0 = P.U0;
   const double* U1 = P.U1;
@@ -638,6 +638,8 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   }
 }
 
+#include "amr_stage_pipe.cuh"
+
 // --------------------------------------------------------------------------
 // Mesh.unzip over CSR rows
 // --------------------------------------------------------------------------
@@ -741,8 +743,49 @@ int launch_stage_one(const AmrStageParams* p, cudaStream_t st) {
   return AMR_OK;
 }
 
+template <int DIM, int PPO, bool LTS, int NT>
+int launch_pipe_one(const AmrStageParams* p, cudaStream_t st) {
+  using PP = Pipe<DIM, PPO>;
+  const size_t dyn = PP::smem_bytes(p->max_slots, p->max_blob);
+  static size_t configured = 0;
+  static size_t occ_dyn = 0;
+  static int grid_cap = 0;
+  if (dyn > configured) {
+    cudaError_t e = cudaFuncSetAttribute(stage_pipe<DIM, PPO, LTS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)dyn);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(stage_pipe)");
+    configured = dyn;
+  }
+  if (dyn != occ_dyn) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e =
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage_pipe<DIM, PPO, LTS, NT>, PP::THREADS, dyn);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy(stage_pipe)");
+    if (per_sm <= 0) {
+      amr_set_error_internal("stage_pipe: tile program does not fit in shared memory");
+      return AMR_EINVAL;
+    }
+    grid_cap = sms * per_sm;
+    occ_dyn = dyn;
+  }
+  const int64_t grid = p->n_tiles < grid_cap ? p->n_tiles : grid_cap;
+  stage_pipe<DIM, PPO, LTS, NT><<<(unsigned)grid, PP::THREADS, dyn, st>>>(*p);
+  return AMR_OK;
+}
+
 template <int DIM, int PPO, bool LTS>
 int launch_stage_nt(const AmrStageParams* p, cudaStream_t st) {
+  if (p->kernel == 1) {
+    switch (p->n_vt) {
+      case 0: return launch_pipe_one<DIM, PPO, LTS, 0>(p, st);
+      case 1: return launch_pipe_one<DIM, PPO, LTS, 1>(p, st);
+      case 2: return launch_pipe_one<DIM, PPO, LTS, 2>(p, st);
+      case 3: return launch_pipe_one<DIM, PPO, LTS, 3>(p, st);
+      default: return AMR_EINVAL;
+    }
+  }
   switch (p->n_vt) {
     case 0: return launch_stage_one<DIM, PPO, LTS, 0>(p, st);
     case 1: return launch_stage_one<DIM, PPO, LTS, 1>(p, st);

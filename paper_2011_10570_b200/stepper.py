@@ -264,6 +264,7 @@ class Engine:
         lts_kernel = mode == "lts" or any(c != self.l_max for c in cadence)
         table, prog = self._tile_programs(td, tiles, node_cad, leaf_cad, lts=lts_kernel)
         n_iface = prog.pop("n_iface")
+        blobs = self._build_blobs(table, prog, n_iface, td, mesh.dim, mesh.ppo)
         self._if_prefix = {c: int(np.sum(prog["if_cad"][:n_iface] >= c)) for c in range(self.l_max + 1)}
         self._n_iface = n_iface
         dev = self.device
@@ -272,13 +273,26 @@ class Engine:
                        cadence=T(leaf_cad), starts=T(td["starts"]), node_cad=T(node_cad),
                        **{k: T(v) for k, v in prog.items() if k != "max_slots"})
         self._max_slots = prog["max_slots"]
+        self._kernel = 1 if blobs is not None else 0
+        if blobs is not None:
+            self._d.update(blob=T(blobs["blob"]), blob_off=T(blobs["blob_off"]), blob_head=T(blobs["blob_head"]),
+                           cell_ent=T(blobs["cell_ent"]))
+            self._max_blob = blobs["max_blob"]
+            self._max_tail = blobs["max_tail"]
         self._ibuf = torch.zeros((2, max(n_iface, 1)), dtype=torch.float64, device=dev)
         n = mesh.n_nodes
-        # the reference's (nvars, n_nodes) zip layout, SoA: chi row then phi row
-        self._U = [torch.zeros((2, n), dtype=torch.float64, device=dev) for _ in range(2)]
-        self._K = torch.zeros((self.p, 2, n), dtype=torch.float64, device=dev)
+        # the reference's (nvars, n_nodes) zip layout, SoA: chi row then phi row.
+        # Rows are padded to an even stride ld > n (16-byte aligned rows; the
+        # kernel bulk-copies 16-byte aligned supersets of a tile's owned range)
+        ld = (n + 2) // 2 * 2
+        self._ld = ld
+        self._U_store = [torch.zeros((2, ld), dtype=torch.float64, device=dev) for _ in range(2)]
+        self._K_store = torch.zeros((self.p, 2, ld), dtype=torch.float64, device=dev)
+        self._U = [u[:, :n] for u in self._U_store]
+        self._K = self._K_store[:, :, :n]
         # verbatim stage sources, double-buffered by stage parity
-        self._Y = torch.zeros((2, 2, n), dtype=torch.float64, device=dev)
+        self._Y_store = torch.zeros((2, 2, ld), dtype=torch.float64, device=dev)
+        self._Y = self._Y_store[:, :, :n]
         self._node_cad_t = self._d["node_cad"].long()
         self._vt = [[j for j in range(s_) if self.tab.a[s_][j] != 0.0] for s_ in range(self.p)]
         self._prm = self._make_params()
@@ -411,6 +425,38 @@ class Engine:
                     cross_pos=cross_pos.astype(np.uint16), max_slots=max_slots)
         return table, prog
 
+    # shared memory of one CTA of the persistent kernel (amr_stage_pipe.cuh, Pipe::smem_bytes)
+    @staticmethod
+    def _pipe_smem(dim: int, ppo: int, max_slots: int, max_head: int) -> int:
+        NS, NI = (ppo + 4) ** dim, ppo ** dim
+        r16 = lambda b: (b + 15) // 16 * 16  # noqa: E731
+        g = r16(NS * 8) + r16(NI * 8) + 2 * r16((max_slots + 1) * 8) + r16(NI * 4) + (16 + 64) * 4
+        return 64 + 64 * 8 + 3 * g + 2 * max_head
+
+    PIPE_SMEM_LIMIT = 113 * 1024  # two CTAs per SM (228 KB per SM, 1 KB reserved per CTA)
+
+    def _build_blobs(self, table, prog, n_iface, td, dim, ppo):
+        """Compact per-tile programs of the persistent pipelined kernel
+        (AMR_KERNEL=1, experimental), or None: the default one-CTA-per-tile
+        kernel then runs.  None also when the mesh does not fit the compact
+        encoding or the kernel's shared memory.  Measured on cfg2 (round 1):
+        the pipelined variants reach 14-21 G updates/s against the default's
+        20.6 (LTS) / 25.9 (GTS), see profiles/README.md."""
+        import os
+
+        from . import tileprog
+
+        if os.environ.get("AMR_KERNEL", "0") != "1":
+            return None
+        try:
+            b = tileprog.build_blobs(table, prog, n_iface, td["starts"], td["anchor3"], ppo ** dim, ppo + 4)
+        except tileprog.BlobError:
+            return None
+        if self._pipe_smem(dim, ppo, prog["max_slots"], b["max_blob"]) > self.PIPE_SMEM_LIMIT:
+            return None
+        b["cell_ent"] = tileprog.cell_entries(prog["cross_cells"], dim, ppo)
+        return b
+
     def _make_params(self) -> _native.AmrStageParams:
         m = self.mesh
         P = _native.AmrStageParams()
@@ -420,6 +466,7 @@ class Engine:
         P.nonlinear = self._nl
         P.prefetch_dist = 0  # L2 prefetch of the next wave: measured neutral on cfg2 (-1 = auto)
         P.n_nodes = m.n_nodes
+        P.ld = self._ld
         d = self._d
         P.tile_ids, P.tile_table = d["tiles"].data_ptr(), d["table"].data_ptr()
         P.leaf_anchor, P.leaf_level = d["anchor"].data_ptr(), d["level"].data_ptr()
@@ -435,6 +482,12 @@ class Engine:
         P.cross_pos = d["cross_pos"].data_ptr()
         P.tap, P.wtab, P.n_wtab = d["tap"].data_ptr(), d["wtab"].data_ptr(), int(d["wtab"].numel())
         P.max_slots = self._max_slots
+        P.kernel = self._kernel
+        if self._kernel:
+            P.blob, P.blob_off = d["blob"].data_ptr(), d["blob_off"].data_ptr()
+            P.blob_head = d["blob_head"].data_ptr()
+            P.cell_ent, P.max_blob = d["cell_ent"].data_ptr(), self._max_blob
+            P.max_tail = self._max_tail
         P.U0, P.U1, P.K = self._U[0].data_ptr(), self._U[1].data_ptr(), self._K.data_ptr()
         P.Y = self._Y.data_ptr()
         for s in range(self.p):

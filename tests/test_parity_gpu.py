@@ -109,3 +109,19 @@ def test_graph_replayed_rounds_equal_eager(cuda):
     assert counts[0] == counts[1]
     exact, rel = compare_field(outs[0], gd, "lts_rk4_i64")
     assert exact, rel
+
+
+@pytest.mark.parametrize("cfg,tag", [("cfg1", "gts_rk4"), ("cfg1", "lts_rk4"), ("cfg1", "lts_sin"),
+                                     ("mini3d", "lts_rk4"), ("mini3d", "lts_cubic"), ("mini3d", "gts_rk4")])
+def test_pipelined_kernel_matches_reference(cuda, monkeypatch, cfg, tag):
+    """The experimental persistent pipelined stage kernel (AMR_KERNEL=1:
+    compact tile blobs, bulk-copied heads, cp.async copy runs) is held to the
+    same goldens as the default kernel."""
+    monkeypatch.setenv("AMR_KERNEL", "1")
+    gd = golden(cfg)
+    mesh = config_mesh(cfg)
+    results = []
+    eng = _run_case(mesh, CONFIGS[cfg].chi0(), gd, "", tag, results)
+    assert eng._kernel == 1
+    print(results)
+    _assert_results(results)
