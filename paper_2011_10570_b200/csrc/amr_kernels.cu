@@ -309,6 +309,27 @@ __device__ __forceinline__ double2 rhs_interior(const Acc& acc, const Weights& W
   return make_double2(acc.at(1, 0, 0), dphi);
 }
 
+// centred 4th-order Laplacian at box pointer b when h**2 is a power of two
+// (the division by h**2 is then an exact multiplication): the operation order
+// of rhs_interior / derivative_axis (wave.py:57-109)
+template <int DIM, int PPO>
+__device__ __forceinline__ double lap_pow2(const double* b, const AmrStageParams& W, double inv_h2) {
+  constexpr int NP = Tile<DIM, PPO>::NP;
+  double lap = 0.0;
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) {
+    const int S = (DIM == 3) ? (d == 0 ? NP * NP : (d == 1 ? NP : 1)) : (d == 0 ? NP : 1);
+    double t = W.d2c[0] * b[-2 * S];
+    t = t + W.d2c[1] * b[-S];
+    t = t + W.d2c[2] * b[0];
+    t = t + W.d2c[3] * b[S];
+    t = t + W.d2c[4] * b[2 * S];
+    t = t * inv_h2;
+    lap = (d == 0) ? t : lap + t;
+  }
+  return lap;
+}
+
 template <int DIM, int PPO>
 struct SmemAcc {
   const double* chi;
@@ -448,6 +469,13 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   for (int i = 0; i < EPT; ++i) {
     const int g = ent[i];
     if (g >= 0) {
+#ifdef AMR_ABLATE
+      if (P.dbg_skip & 1) {  // ablation (tools/ablate.py): no field gathers
+        cu[i] = 1.0;
+        pu[i] = 1.0;
+        continue;
+      }
+#endif
       cu[i] = __ldg(V + g);
       if (i < EPI && (phi_all || (g >= g0 && g < g1))) pu[i] = __ldg(V + n + g);
     } else if (LTS && g <= AMR_IFACE_BASE) {
@@ -520,6 +548,10 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   //      multiple of 4 taps (padding taps: weight 0 on the zero slot, which
   //      leaves the running sum unchanged), 16-byte aligned: one uint4 of tap
   //      words per 4 taps.  in_cell is the row's smem cell.
+#ifdef AMR_ABLATE
+  if (P.dbg_skip & 2) {  // ablation: no hanging-row sums
+  } else
+#endif
   if (phi_all) {
     for (int li = threadIdx.x; li < nin; li += T::THREADS) {
       const int64_t k0 = __ldg(P.in_tap_ptr + j0 + li), k1 = __ldg(P.in_tap_ptr + j0 + li + 1);
@@ -582,7 +614,11 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
   const bool last = (s == p - 1);
   double* Unew = cur ? P.U0 : P.U1;
   double* Ks = P.K + (int64_t)s * 2 * n;
+#ifdef AMR_ABLATE
+  const int n_own = (P.dbg_skip & 4) ? 0 : (int)(g1 - g0);  // ablation: no RHS / epilogue
+#else
   const int n_own = (int)(g1 - g0);
+#endif
 #pragma unroll
   for (int r = 0; r < OPT; ++r) {
     const int k = threadIdx.x + r * T::THREADS;

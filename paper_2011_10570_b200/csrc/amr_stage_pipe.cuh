@@ -66,8 +66,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 template <int DIM, int PPO>
 struct Pipe {
   using T = Tile<DIM, PPO>;
-  static constexpr int THREADS = DIM == 3 ? 512 : 128;
-  static constexpr int MIN_CTAS = 2;  // two CTAs per SM: 32 resident warps
+  static constexpr int THREADS = DIM == 3 ? 256 : 128;
+  static constexpr int MIN_CTAS = 2;  // two independent CTAs per SM: their phases interleave
   static constexpr int NG = 3;  // gather buffers: tile landing, tile in its row phase, tile in its RHS phase
   static constexpr int NB = 2;  // blob-head ring slots (a head is consumed when its tile's gathers issue)
   static constexpr int HEAD = 64 + 64 * 8;  // mbarriers, interpolation weights
@@ -84,27 +84,6 @@ struct Pipe {
     return HEAD + (size_t)NG * gbuf_bytes(max_slots) + (size_t)NB * max_head;
   }
 };
-
-// centred 4th-order Laplacian at box pointer b when h**2 is a power of two
-// (the division by h**2 is then an exact multiplication): the operation order
-// of rhs_interior / derivative_axis (wave.py:57-109)
-template <int DIM, int PPO>
-__device__ __forceinline__ double lap_pow2(const double* b, const AmrStageParams& W, double inv_h2) {
-  constexpr int NP = Tile<DIM, PPO>::NP;
-  double lap = 0.0;
-#pragma unroll
-  for (int d = 0; d < DIM; ++d) {
-    const int S = (DIM == 3) ? (d == 0 ? NP * NP : (d == 1 ? NP : 1)) : (d == 0 ? NP : 1);
-    double t = W.d2c[0] * b[-2 * S];
-    t = t + W.d2c[1] * b[-S];
-    t = t + W.d2c[2] * b[0];
-    t = t + W.d2c[3] * b[S];
-    t = t + W.d2c[4] * b[2 * S];
-    t = t * inv_h2;
-    lap = (d == 0) ? t : lap + t;
-  }
-  return lap;
-}
 
 template <int DIM, int PPO>
 struct AccI {  // interior fast path: chi from the box, phi of the node
@@ -394,7 +373,7 @@ __global__ void __launch_bounds__(Pipe<DIM, PPO>::THREADS, Pipe<DIM, PPO>::MIN_C
       if (k >= n_own) break;
       const int64_t g = g0 + k;
       const int cell = own[k];
-      // node values from global memory, issued before the stencil
+      // node values from global memory (L2-warm), issued before the stencil
       const double uc = __ldg(Ucur + g), up = __ldg(Ucur + n + g);
       const double ph = __ldg(V + n + g);
       double2 ks;
