@@ -675,6 +675,7 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
 }
 
 #include "amr_stage_pipe.cuh"
+#include "amr_stage_blob.cuh"
 
 // --------------------------------------------------------------------------
 // Mesh.unzip over CSR rows
@@ -811,8 +812,32 @@ int launch_pipe_one(const AmrStageParams* p, cudaStream_t st) {
   return AMR_OK;
 }
 
+template <int DIM, int PPO, bool LTS, int NT>
+int launch_blob_one(const AmrStageParams* p, cudaStream_t st) {
+  using BK = BlobK<DIM, PPO>;
+  const size_t dyn = BK::smem_bytes(p->max_slots, p->max_blob);
+  static size_t configured = 0;
+  if (dyn > configured) {
+    cudaError_t e = cudaFuncSetAttribute(stage_blob<DIM, PPO, LTS, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)dyn);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(stage_blob)");
+    configured = dyn;
+  }
+  stage_blob<DIM, PPO, LTS, NT><<<(unsigned)p->n_tiles, BK::THREADS, dyn, st>>>(*p);
+  return AMR_OK;
+}
+
 template <int DIM, int PPO, bool LTS>
 int launch_stage_nt(const AmrStageParams* p, cudaStream_t st) {
+  if (p->kernel == 2) {
+    switch (p->n_vt) {
+      case 0: return launch_blob_one<DIM, PPO, LTS, 0>(p, st);
+      case 1: return launch_blob_one<DIM, PPO, LTS, 1>(p, st);
+      case 2: return launch_blob_one<DIM, PPO, LTS, 2>(p, st);
+      case 3: return launch_blob_one<DIM, PPO, LTS, 3>(p, st);
+      default: return AMR_EINVAL;
+    }
+  }
   if (p->kernel == 1) {
     switch (p->n_vt) {
       case 0: return launch_pipe_one<DIM, PPO, LTS, 0>(p, st);

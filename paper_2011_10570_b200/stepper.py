@@ -273,7 +273,7 @@ class Engine:
                        cadence=T(leaf_cad), starts=T(td["starts"]), node_cad=T(node_cad),
                        **{k: T(v) for k, v in prog.items() if k != "max_slots"})
         self._max_slots = prog["max_slots"]
-        self._kernel = 1 if blobs is not None else 0
+        self._kernel = blobs["kernel"] if blobs is not None else 0
         if blobs is not None:
             self._d.update(blob=T(blobs["blob"]), blob_off=T(blobs["blob_off"]), blob_head=T(blobs["blob_head"]),
                            cell_ent=T(blobs["cell_ent"]))
@@ -436,24 +436,30 @@ class Engine:
     PIPE_SMEM_LIMIT = 113 * 1024  # two CTAs per SM (228 KB per SM, 1 KB reserved per CTA)
 
     def _build_blobs(self, table, prog, n_iface, td, dim, ppo):
-        """Compact per-tile programs of the persistent pipelined kernel
-        (AMR_KERNEL=1, experimental), or None: the default one-CTA-per-tile
-        kernel then runs.  None also when the mesh does not fit the compact
-        encoding or the kernel's shared memory.  Measured on cfg2 (round 1):
-        the pipelined variants reach 14-21 G updates/s against the default's
-        20.6 (LTS) / 25.9 (GTS), see profiles/README.md."""
+        """Compact per-tile programs (tileprog.py) for the blob kernels, or None
+        (the int32-table kernel then runs).
+
+        AMR_KERNEL selects the stage kernel: 2 (default) one CTA per tile with
+        the blob front-end (bulk-copied head, cp.async copy runs); 1 the
+        persistent pipelined kernel (experimental); 0 the int32-table kernel.
+        A mesh that does not fit the compact encoding (or kernel 1's shared
+        memory) falls back to kernel 0.  Measured on cfg2 (round 1, LTS / GTS
+        G updates/s): kernel 2 23.9 / 25.9, kernel 0 20.4 / 25.5, kernel 1
+        15-21 / 14-20 (profiles/README.md)."""
         import os
 
         from . import tileprog
 
-        if os.environ.get("AMR_KERNEL", "0") != "1":
+        kernel = os.environ.get("AMR_KERNEL", "2")
+        if kernel not in ("1", "2"):
             return None
         try:
             b = tileprog.build_blobs(table, prog, n_iface, td["starts"], td["anchor3"], ppo ** dim, ppo + 4)
         except tileprog.BlobError:
             return None
-        if self._pipe_smem(dim, ppo, prog["max_slots"], b["max_blob"]) > self.PIPE_SMEM_LIMIT:
+        if kernel == "1" and self._pipe_smem(dim, ppo, prog["max_slots"], b["max_blob"]) > self.PIPE_SMEM_LIMIT:
             return None
+        b["kernel"] = int(kernel)
         b["cell_ent"] = tileprog.cell_entries(prog["cross_cells"], dim, ppo)
         return b
 

@@ -111,17 +111,18 @@ def test_graph_replayed_rounds_equal_eager(cuda):
     assert exact, rel
 
 
+@pytest.mark.parametrize("kernel", [1, 2])
 @pytest.mark.parametrize("cfg,tag", [("cfg1", "gts_rk4"), ("cfg1", "lts_rk4"), ("cfg1", "lts_sin"),
                                      ("mini3d", "lts_rk4"), ("mini3d", "lts_cubic"), ("mini3d", "gts_rk4")])
-def test_pipelined_kernel_matches_reference(cuda, monkeypatch, cfg, tag):
-    """The experimental persistent pipelined stage kernel (AMR_KERNEL=1:
-    compact tile blobs, bulk-copied heads, cp.async copy runs) is held to the
-    same goldens as the default kernel."""
-    monkeypatch.setenv("AMR_KERNEL", "1")
+def test_blob_kernels_match_reference(cuda, monkeypatch, cfg, tag, kernel):
+    """The stage kernels on the compact tile blobs (AMR_KERNEL=1: persistent
+    pipeline; 2: one CTA per tile, bulk-copied head, cp.async copy runs) are
+    held to the same goldens as the table kernel."""
+    monkeypatch.setenv("AMR_KERNEL", str(kernel))
     gd = golden(cfg)
     mesh = config_mesh(cfg)
     results = []
     eng = _run_case(mesh, CONFIGS[cfg].chi0(), gd, "", tag, results)
-    assert eng._kernel == 1
+    assert eng._kernel == kernel
     print(results)
     _assert_results(results)
