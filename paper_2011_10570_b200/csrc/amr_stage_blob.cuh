@@ -21,7 +21,10 @@
 template <int DIM, int PPO>
 struct BlobK {
   using T = Tile<DIM, PPO>;
-  static constexpr int THREADS = DIM == 3 ? 256 : 128;
+#ifndef AMR_BLOB_THREADS
+#define AMR_BLOB_THREADS 256
+#endif
+  static constexpr int THREADS = DIM == 3 ? AMR_BLOB_THREADS : 128;
   static constexpr int HEAD = 16 + 64 * 8;                  // mbarrier, interpolation weights
   static constexpr int BOXB = (T::NS * 8 + 15) / 16 * 16;   // one stencil box
   static constexpr int OWNC = (T::NI * 4 + 15) / 16 * 16;   // owned node -> box cell
@@ -90,6 +93,23 @@ __global__ void __launch_bounds__(BlobK<DIM, PPO>::THREADS, AMR_BLOB_MIN_BLOCKS)
   if (tid == 0) {
     const uint32_t tail = 2u * (uint32_t)(h[7] - h[11]);
     if (tail) bulk_prefetch_l2(gblob + h[11], tail);
+    if (last) {  // the combine's K_j over the owned range
+      const int64_t a16 = g0 & ~1, e16 = (g0 + n_own + 1) & ~1;
+      const uint32_t bytes = (uint32_t)(e16 - a16) * 8;
+      for (int jj = 0; jj < s; ++jj) {
+        bulk_prefetch_l2(P.K + (int64_t)jj * 2 * n + a16, bytes);
+        bulk_prefetch_l2(P.K + (int64_t)jj * 2 * n + n + a16, bytes);
+      }
+    }
+  }
+  // u at this thread's owned nodes, for the epilogue (in flight during the
+  // gathers and the rows)
+  double2 uo[OPT];
+#pragma unroll
+  for (int r = 0; r < OPT; ++r) {
+    const int k = tid + r * NTH;
+    const int64_t g = g0 + (k < n_own ? k : 0);
+    uo[r] = make_double2(__ldg(Ucur + g), __ldg(Ucur + n + g));
   }
 
   // ---- 2: gathers
@@ -136,14 +156,6 @@ __global__ void __launch_bounds__(BlobK<DIM, PPO>::THREADS, AMR_BLOB_MIN_BLOCKS)
     slp[nslot] = 0.0;
   }
   cp_async_commit();
-  // u at this thread's owned nodes, for the epilogue (in flight during the rows)
-  double2 uo[OPT];
-#pragma unroll
-  for (int r = 0; r < OPT; ++r) {
-    const int k = tid + r * NTH;
-    const int64_t g = g0 + (k < n_own ? k : 0);
-    uo[r] = make_double2(__ldg(Ucur + g), __ldg(Ucur + n + g));
-  }
   cp_async_wait<0>();
   __syncthreads();
 
