@@ -823,7 +823,19 @@ int launch_blob_one(const AmrStageParams* p, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(stage_blob)");
     configured = dyn;
   }
-  stage_blob<DIM, PPO, LTS, NT><<<(unsigned)p->n_tiles, BK::THREADS, dyn, st>>>(*p);
+  // L2 prefetch distance: one wave of resident CTAs (AMR_PREFETCH=0 disables)
+  static int wave = -1;
+  if (wave < 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage_blob<DIM, PPO, LTS, NT>, BK::THREADS, dyn);
+    const char* env = std::getenv("AMR_PREFETCH");
+    wave = (env && std::atoi(env) == 0) ? 0 : sms * (per_sm > 0 ? per_sm : 1);
+  }
+  AmrStageParams q = *p;
+  q.prefetch_dist = p->prefetch_dist < 0 ? wave : p->prefetch_dist;
+  stage_blob<DIM, PPO, LTS, NT><<<(unsigned)p->n_tiles, BK::THREADS, dyn, st>>>(q);
   return AMR_OK;
 }
 

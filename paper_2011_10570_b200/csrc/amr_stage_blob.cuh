@@ -73,6 +73,11 @@ __global__ void __launch_bounds__(BlobK<DIM, PPO>::THREADS, AMR_BLOB_MIN_BLOCKS)
     const int hb = __ldg(P.blob_head + tile);
     mbar_expect_tx(bar, (uint32_t)hb);
     bulk_g2s(head, reinterpret_cast<const unsigned char*>(blob) + o0, (uint32_t)hb, bar);
+    // the tile that takes this CTA slot one wave later: its head into L2
+    const int64_t nt = tile + P.prefetch_dist;
+    if (P.prefetch_dist > 0 && nt < P.n_tiles)
+      bulk_prefetch_l2(reinterpret_cast<const unsigned char*>(blob) + __ldg(P.blob_off + nt),
+                       (uint32_t)__ldg(P.blob_head + nt));
   }
   for (int i = tid; i < P.n_wtab; i += NTH) s_w[i] = __ldg(P.wtab + i);
   __syncthreads();  // mbarrier initialised before anyone waits on it
@@ -113,7 +118,12 @@ __global__ void __launch_bounds__(BlobK<DIM, PPO>::THREADS, AMR_BLOB_MIN_BLOCKS)
   }
 
   // ---- 2: gathers
-  for (int r = tid; r < nrun; r += NTH) {
+#ifdef AMR_ABLATE
+  const int nrun_ = (P.dbg_skip & 1) ? 0 : nrun;  // ablation (tools/ablate.py): no copy gathers
+#else
+  const int nrun_ = nrun;
+#endif
+  for (int r = tid; r < nrun_; r += NTH) {
     const uint32_t w = runs[r];
     const int cell = w & 0xFFF, len = ((w >> 12) & 15) + 1;
     const int bi = w >> 26, off = (w >> 16) & 1023;
@@ -164,13 +174,20 @@ __global__ void __launch_bounds__(BlobK<DIM, PPO>::THREADS, AMR_BLOB_MIN_BLOCKS)
   {
     const uint32_t* rows = reinterpret_cast<const uint32_t*>(gblob + h[13]);
     const uint2* taps = reinterpret_cast<const uint2*>(gblob + h[14]);
-    for (int r = tid; r < nrow; r += NTH) {
+#ifdef AMR_ABLATE
+    const int nrow_ = (P.dbg_skip & 2) ? 0 : nrow;  // ablation: no hanging-row sums
+#else
+    const int nrow_ = nrow;
+#endif
+    for (int r = tid; r < nrow_; r += NTH) {
       const uint32_t w = __ldg(rows + r);
       const int nq = (w >> 12) & 31;
       const uint2* tq = taps + (w >> 17);
       double ax = 0.0, ay = 0.0;
+      uint2 vn = nq > 0 ? __ldg(tq) : make_uint2(0u, 0u);
       for (int q = 0; q < nq; ++q) {
-        const uint2 v = __ldg(tq + q);
+        const uint2 v = vn;
+        if (q + 1 < nq) vn = __ldg(tq + q + 1);  // next tap word in flight during this quad
         const uint32_t t4[4] = {v.x & 0xFFFF, v.x >> 16, v.y & 0xFFFF, v.y >> 16};
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -202,10 +219,15 @@ __global__ void __launch_bounds__(BlobK<DIM, PPO>::THREADS, AMR_BLOB_MIN_BLOCKS)
   const bool need_x = face || P.nonlinear == 1;
   double* Unew = cur ? P.U0 : P.U1;
   double* Ks = P.K + (int64_t)s * 2 * n;
+#ifdef AMR_ABLATE
+  const int n_own_ = (P.dbg_skip & 4) ? 0 : n_own;  // ablation: no RHS / epilogue
+#else
+  const int n_own_ = n_own;
+#endif
 #pragma unroll
   for (int r = 0; r < OPT; ++r) {
     const int k = tid + r * NTH;
-    if (k >= n_own) break;
+    if (k >= n_own_) break;
     const int cell = own[k];
     SmemAcc<DIM, PPO> acc{s_chi, s_phi, cell};
     double2 ks;

@@ -24,6 +24,7 @@ B200 design:
 """
 from __future__ import annotations
 
+import os
 import time
 from collections import defaultdict
 from dataclasses import dataclass, field
@@ -470,7 +471,8 @@ class Engine:
         P.lts = 1 if self.mode == "lts" or any(c != self.l_max for c in self.cadence) else 0
         P.n_stages = self.p
         P.nonlinear = self._nl
-        P.prefetch_dist = 0  # L2 prefetch of the next wave: measured neutral on cfg2 (-1 = auto)
+        # L2 prefetch of the tile one wave of CTAs ahead (-1: one wave, 0: off)
+        P.prefetch_dist = int(os.environ.get("AMR_PREFETCH_DIST", "0"))
         P.n_nodes = m.n_nodes
         P.ld = self._ld
         d = self._d
