@@ -189,6 +189,7 @@ typedef struct {
   const uint16_t* blob;        /* all blobs, 16-byte aligned */
   const int64_t* blob_off;     /* [n_tiles+1] byte offset of each tile's blob */
   const int32_t* blob_head;    /* [n_tiles] bytes of each blob's head */
+  const uint8_t* heads;        /* [n_tiles][max_blob]: the heads again at a fixed stride (kernel 2) */
   int max_blob;                /* largest blob head in bytes (ring slot size) */
   int max_tail;                /* largest blob tail (rows + taps) in bytes */
   int kernel;                  /* 0: per-tile kernel (v17 tables), 1: persistent pipeline (blobs) */

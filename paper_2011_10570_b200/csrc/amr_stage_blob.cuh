@@ -69,15 +69,14 @@ __global__ void __launch_bounds__(BlobK<DIM, PPO>::THREADS, AMR_BLOB_MIN_BLOCKS)
   if (tid == 0) {
     mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    const int64_t o0 = __ldg(P.blob_off + tile);
-    const int hb = __ldg(P.blob_head + tile);
-    mbar_expect_tx(bar, (uint32_t)hb);
-    bulk_g2s(head, reinterpret_cast<const unsigned char*>(blob) + o0, (uint32_t)hb, bar);
+    // heads live at a fixed stride (no dependent offset load before the copy)
+    const uint32_t hb = (uint32_t)P.max_blob;
+    mbar_expect_tx(bar, hb);
+    bulk_g2s(head, reinterpret_cast<const unsigned char*>(P.heads) + tile * (int64_t)hb, hb, bar);
     // the tile that takes this CTA slot one wave later: its head into L2
     const int64_t nt = tile + P.prefetch_dist;
     if (P.prefetch_dist > 0 && nt < P.n_tiles)
-      bulk_prefetch_l2(reinterpret_cast<const unsigned char*>(blob) + __ldg(P.blob_off + nt),
-                       (uint32_t)__ldg(P.blob_head + nt));
+      bulk_prefetch_l2(P.heads + nt * (int64_t)hb, hb);
   }
   for (int i = tid; i < P.n_wtab; i += NTH) s_w[i] = __ldg(P.wtab + i);
   __syncthreads();  // mbarrier initialised before anyone waits on it

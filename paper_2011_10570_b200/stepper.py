@@ -277,6 +277,7 @@ class Engine:
         self._kernel = blobs["kernel"] if blobs is not None else 0
         if blobs is not None:
             self._d.update(blob=T(blobs["blob"]), blob_off=T(blobs["blob_off"]), blob_head=T(blobs["blob_head"]),
+                           heads=T(blobs["heads"]),
                            cell_ent=T(blobs["cell_ent"]))
             self._max_blob = blobs["max_blob"]
             self._max_tail = blobs["max_tail"]
@@ -493,7 +494,7 @@ class Engine:
         P.kernel = self._kernel
         if self._kernel:
             P.blob, P.blob_off = d["blob"].data_ptr(), d["blob_off"].data_ptr()
-            P.blob_head = d["blob_head"].data_ptr()
+            P.blob_head, P.heads = d["blob_head"].data_ptr(), d["heads"].data_ptr()
             P.cell_ent, P.max_blob = d["cell_ent"].data_ptr(), self._max_blob
             P.max_tail = self._max_tail
         P.U0, P.U1, P.K = self._U[0].data_ptr(), self._U[1].data_ptr(), self._K.data_ptr()

@@ -250,7 +250,16 @@ def build_blobs(table: np.ndarray, prog: dict, n_iface: int, starts: np.ndarray,
         raise BlobError("tile blobs exceed 32 GB")
     head = (off_ent * 2).astype(np.int32)  # header, bases, runs, slots: staged in shared memory
     tail = (length - off_ent) * 2          # face entry codes, rows, taps: read through L2
-    return dict(blob=blob, blob_off=(tstart * 2).astype(np.int64), blob_head=head,
+    # the heads again at a fixed stride (the per-tile kernel copies without an offset lookup)
+    mh = int(head.max()) if nt else 16
+    hstart = tstart[:nt] * 2
+    heads = np.zeros((max(nt, 1), mh), dtype=np.uint8)
+    bb = blob.view(np.uint8)
+    if nt:
+        within = np.arange(mh)[None, :]
+        src = np.minimum(hstart[:, None] + within, len(bb) - 1)
+        heads[:nt] = np.where(within < head[:, None], bb[src], 0)
+    return dict(blob=blob, blob_off=(tstart * 2).astype(np.int64), blob_head=head, heads=heads,
                 max_blob=int(head.max()) if nt else 16, max_tail=int(tail.max()) if nt else 0,
                 max_rows=int(nrow.max()) if nt else 0)
 

@@ -37,6 +37,12 @@ def test_blobs_decode_to_the_tile_programs(name):
     cells = prog["cross_cells"].astype(np.int64)
     cell_to_e = {int(c): e for e, c in enumerate(cells)}
     assert B["max_blob"] == int(B["blob_head"].max())
+    heads = B["heads"]
+    assert heads.shape == (nt, B["max_blob"])
+    for t in range(nt):  # the fixed-stride copy of every head
+        hb = int(B["blob_head"][t])
+        assert np.array_equal(heads[t, :hb], blob.view(np.uint8)[off[t]:off[t] + hb])
+        assert not heads[t, hb:].any()
     for t in range(nt):
         b = blob[off[t] // 2: off[t + 1] // 2]
         h = b[:32].view(np.int32)
