@@ -178,6 +178,39 @@ __global__ void __launch_bounds__(BlobK<DIM, PPO>::THREADS, AMR_BLOB_MIN_BLOCKS)
 #else
     const int nrow_ = nrow;
 #endif
+    if (!face) {
+      // two quads per step: their 8 products are formed before the 8 ordered
+      // adds, and the next two tap words are in flight meanwhile
+      for (int r = tid; r < nrow_; r += NTH) {
+        const uint32_t w = __ldg(rows + r);
+        const int nq = (w >> 12) & 31;
+        const uint2* tq = taps + (w >> 17);
+        double ax = 0.0;
+        uint2 a = nq > 0 ? __ldg(tq) : make_uint2(0u, 0u);
+        uint2 b = nq > 1 ? __ldg(tq + 1) : make_uint2(0u, 0u);
+        int q = 0;
+        for (; q + 2 <= nq; q += 2) {
+          const uint32_t t8[8] = {a.x & 0xFFFF, a.x >> 16, a.y & 0xFFFF, a.y >> 16,
+                                  b.x & 0xFFFF, b.x >> 16, b.y & 0xFFFF, b.y >> 16};
+          if (q + 2 < nq) a = __ldg(tq + q + 2);
+          if (q + 3 < nq) b = __ldg(tq + q + 3);
+          double pr[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pr[u] = s_w[t8[u] & 63] * slc[t8[u] >> 6];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) ax = ax + pr[u];
+        }
+        if (q < nq) {  // odd quad count: the last quad is in a
+          const uint32_t t4[4] = {a.x & 0xFFFF, a.x >> 16, a.y & 0xFFFF, a.y >> 16};
+          double pr[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) pr[u] = s_w[t4[u] & 63] * slc[t4[u] >> 6];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) ax = ax + pr[u];
+        }
+        s_chi[w & 0xFFF] = ax;
+      }
+    } else
     for (int r = tid; r < nrow_; r += NTH) {
       const uint32_t w = __ldg(rows + r);
       const int nq = (w >> 12) & 31;
