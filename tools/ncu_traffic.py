@@ -9,8 +9,8 @@ import sys
 
 
 def _is_lts(name: str) -> bool:
-    """stage_kernel<DIM, PPO, LTS, NT> as ncu prints it (demangled forms vary)."""
-    m = re.search(r"stage_kernel<\(?\w*\)?(\d+), \(?\w*\)?(\d+), \(?\w*\)?(\w+)", name)
+    """stage_{kernel,blob,pipe}<DIM, PPO, LTS, NT> as ncu prints it (demangled forms vary)."""
+    m = re.search(r"stage_(?:kernel|blob|pipe)<\(?\w*\)?(\d+), \(?\w*\)?(\d+), \(?\w*\)?(\w+)", name)
     return bool(m) and m.group(3) in ("1", "true")
 
 import numpy as np
@@ -48,4 +48,4 @@ def main(rep, out="profiles/traffic.json"):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], *sys.argv[2:3])
