@@ -118,11 +118,11 @@ __global__ void __launch_bounds__(BlobK<DIM, PPO>::THREADS, AMR_BLOB_MIN_BLOCKS)
 
   // ---- 2: gathers
 #ifdef AMR_ABLATE
-  const int nrun_ = (P.dbg_skip & 1) ? 0 : nrun;  // ablation (tools/ablate.py): no copy gathers
+  const bool gather = !(P.dbg_skip & 1);  // ablation (tools/ablate.py): no copy gathers
 #else
-  const int nrun_ = nrun;
+  constexpr bool gather = true;
 #endif
-  for (int r = tid; r < nrun_; r += NTH) {
+  for (int r = tid; r < nrun; r += NTH) {
     const uint32_t w = runs[r];
     const int cell = w & 0xFFF, len = ((w >> 12) & 15) + 1;
     const int bi = w >> 26, off = (w >> 16) & 1023;
@@ -136,9 +136,10 @@ __global__ void __launch_bounds__(BlobK<DIM, PPO>::THREADS, AMR_BLOB_MIN_BLOCKS)
     const int base = bases[bi];
     if (!LTS || base >= 0) {
       const double* src = V + base + off;
-      for (int i = 0; i < len; ++i) cp_async8(s_chi + cell + i, src + i);
+      if (gather)
+        for (int i = 0; i < len; ++i) cp_async8(s_chi + cell + i, src + i);
       const bool mine = base == g0;
-      if (face || mine)
+      if (gather && (face || mine))
         for (int i = 0; i < len; ++i) cp_async8(s_phi + cell + i, src + n + i);
       if (mine)
         for (int i = 0; i < len; ++i) own[off + i] = cell + i;
