@@ -182,21 +182,21 @@ typedef struct {
   double k_chi, k_phi, f0_chi, f0_phi;
   /* stencil weights: the reference's Fornberg arrays, bit for bit (wave.py:49-54) */
   double d2c[5], d2e0[6], d2e1[6], d1c[5], d1e0[5], d1e1[5];
-  /* persistent pipelined stage kernel: one compact program blob per tile in
-   * launch order (paper_2011_10570_b200/tileprog.py); its head (header, bases,
-   * entry/slot codes) is bulk-copied into a shared-memory ring and its tail
-   * (rows, taps) into the tile's gather buffer, two tiles ahead */
+  /* blob stage kernels (kernel 1, 2): one compact program blob per tile in
+   * launch order (paper_2011_10570_b200/tileprog.py).  Its head (header,
+   * source bases, copy runs, slot codes) is bulk-copied into shared memory;
+   * its tail (face entry codes, rows, taps) is read through L2 */
   const uint16_t* blob;        /* all blobs, 16-byte aligned */
   const int64_t* blob_off;     /* [n_tiles+1] byte offset of each tile's blob */
   const int32_t* blob_head;    /* [n_tiles] bytes of each blob's head */
   const uint8_t* heads;        /* [n_tiles][max_blob]: the heads again at a fixed stride (kernel 2) */
-  int max_blob;                /* largest blob head in bytes (ring slot size) */
-  int max_tail;                /* largest blob tail (rows + taps) in bytes */
-  int kernel;                  /* 0: per-tile kernel (v17 tables), 1: persistent pipeline (blobs) */
+  int max_blob;                /* largest blob head in bytes (the head stride / smem slot size) */
+  int kernel;                  /* 0: int32-table kernel, 1: persistent pipeline, 2: one CTA per tile on blobs */
   const uint16_t* cell_ent;    /* [(ppo+4)^dim] cross entry of each padded-box cell (0xFFFF: none) */
   int64_t ld;                  /* row stride (elements) of U0/U1/K/Y: even, >= n_nodes + 1 */
-  long long* dbg;              /* NULL, or per-warp phase cycle counters of the persistent kernel (tools/phase_probe.py) */
-  int dbg_skip;                /* ablation bits for tools/phase_probe.py (results invalid): 1 gathers, 2 rows, 4 RHS */
+  long long* dbg;              /* NULL, or per-warp phase cycle counters of kernel 1 (tools/phase_probe.py) */
+  int dbg_skip;                /* ablation bits (results invalid; kernels 0/2 only with -DAMR_ABLATE,
+                                  tools/ablate.py): 1 gathers, 2 rows, 4 RHS */
 } AmrStageParams;
 
 /* One RK stage over a prefix of the tile list: fused unzip (spatial + LTS time

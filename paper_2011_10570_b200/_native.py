@@ -64,7 +64,7 @@ class AmrStageParams(C.Structure):
         ("k_chi", C.c_double), ("k_phi", C.c_double), ("f0_chi", C.c_double), ("f0_phi", C.c_double),
         ("d2c", C.c_double * 5), ("d2e0", C.c_double * 6), ("d2e1", C.c_double * 6),
         ("d1c", C.c_double * 5), ("d1e0", C.c_double * 5), ("d1e1", C.c_double * 5),
-        ("blob", _vp), ("blob_off", _vp), ("blob_head", _vp), ("heads", _vp), ("max_blob", C.c_int), ("max_tail", C.c_int),
+        ("blob", _vp), ("blob_off", _vp), ("blob_head", _vp), ("heads", _vp), ("max_blob", C.c_int),
         ("kernel", C.c_int),
         ("cell_ent", _vp), ("ld", C.c_int64), ("dbg", _vp), ("dbg_skip", C.c_int),
     ]

@@ -280,7 +280,6 @@ class Engine:
                            heads=T(blobs["heads"]),
                            cell_ent=T(blobs["cell_ent"]))
             self._max_blob = blobs["max_blob"]
-            self._max_tail = blobs["max_tail"]
         self._ibuf = torch.zeros((2, max(n_iface, 1)), dtype=torch.float64, device=dev)
         n = mesh.n_nodes
         # the reference's (nvars, n_nodes) zip layout, SoA: chi row then phi row.
@@ -496,7 +495,6 @@ class Engine:
             P.blob, P.blob_off = d["blob"].data_ptr(), d["blob_off"].data_ptr()
             P.blob_head, P.heads = d["blob_head"].data_ptr(), d["heads"].data_ptr()
             P.cell_ent, P.max_blob = d["cell_ent"].data_ptr(), self._max_blob
-            P.max_tail = self._max_tail
         P.U0, P.U1, P.K = self._U[0].data_ptr(), self._U[1].data_ptr(), self._K.data_ptr()
         P.Y = self._Y.data_ptr()
         for s in range(self.p):

@@ -1,4 +1,4 @@
-"""Per-tile program blobs of the persistent stage kernel (amr_stage, v18).
+"""Per-tile program blobs of the blob stage kernels (amr_stage, AMR_KERNEL 1 and 2).
 
 One blob per leaf tile, in launch order, 16-byte aligned.  The kernel fetches
 its head (header, bases, runs, slot codes) with a single bulk copy
@@ -260,7 +260,7 @@ def build_blobs(table: np.ndarray, prog: dict, n_iface: int, starts: np.ndarray,
         src = np.minimum(hstart[:, None] + within, len(bb) - 1)
         heads[:nt] = np.where(within < head[:, None], bb[src], 0)
     return dict(blob=blob, blob_off=(tstart * 2).astype(np.int64), blob_head=head, heads=heads,
-                max_blob=int(head.max()) if nt else 16, max_tail=int(tail.max()) if nt else 0,
+                max_blob=int(head.max()) if nt else 16, max_tail=int(tail.max()) if nt else 0,  # tail: info
                 max_rows=int(nrow.max()) if nt else 0)
 
 
