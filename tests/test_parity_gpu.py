@@ -126,3 +126,17 @@ def test_blob_kernels_match_reference(cuda, monkeypatch, cfg, tag, kernel):
     assert eng._kernel == kernel
     print(results)
     _assert_results(results)
+
+
+def test_unencodable_mesh_falls_back_to_table_kernel(cuda, monkeypatch):
+    """A mesh that does not fit the compact blob encoding (here: a forced
+    1-source-group limit) runs on the int32-table kernel, with the same bits."""
+    from paper_2011_10570_b200 import tileprog
+
+    monkeypatch.setattr(tileprog, "MAX_BASES", 1)
+    gd = golden("cfg1")
+    mesh = config_mesh("cfg1")
+    results = []
+    eng = _run_case(mesh, CONFIGS["cfg1"].chi0(), gd, "", "lts_rk4", results)
+    assert eng._kernel == 0
+    _assert_results(results)
