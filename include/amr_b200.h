@@ -141,7 +141,7 @@ typedef struct {
   int64_t n_iface;             /* pairs of this launch (prefix: finest readers first) */
   int64_t n_iface_total;
   const int32_t* if_gid;
-  const int32_t* if_cad;
+  const int32_t* if_cad;       /* reader cadence | source cadence << 8 */
   double* ibuf;                /* [2][n_iface_total] */
   /* per-tile interpolation program: the hanging points of each tile (rows of
    * mesh.py:316-351), summed from a per-tile set of unique source nodes */

@@ -356,8 +356,8 @@ __global__ void __launch_bounds__(256) iface_kernel(const AmrStageParams P) {
   const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
   if (i >= P.n_iface) return;
   const int g = __ldg(P.if_gid + i);
-  const int lr = __ldg(P.if_cad + i);
-  const double2 v = lts_source(P.U0, P.U1, P.K, P.ld, P.n_stages, g, P.stage, lr, P.node_cadence[g], P.coef);
+  const int cc = __ldg(P.if_cad + i);  // reader cadence | source cadence << 8 (no dependent lookup)
+  const double2 v = lts_source(P.U0, P.U1, P.K, P.ld, P.n_stages, g, P.stage, cc & 0xFF, cc >> 8, P.coef);
   P.ibuf[i] = v.x;
   P.ibuf[P.n_iface_total + i] = v.y;
 }

@@ -266,7 +266,7 @@ class Engine:
         table, prog = self._tile_programs(td, tiles, node_cad, leaf_cad, lts=lts_kernel)
         n_iface = prog.pop("n_iface")
         blobs = self._build_blobs(table, prog, n_iface, td, mesh.dim, mesh.ppo)
-        self._if_prefix = {c: int(np.sum(prog["if_cad"][:n_iface] >= c)) for c in range(self.l_max + 1)}
+        self._if_prefix = {c: int(np.sum((prog["if_cad"][:n_iface] & 0xFF) >= c)) for c in range(self.l_max + 1)}
         self._n_iface = n_iface
         dev = self.device
         T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
@@ -405,7 +405,9 @@ class Engine:
                 slot_gid = slot_gid.copy()
                 slot_gid[sm] = (-pinv[ne:] - 1).astype(np.int32)
                 if_gid = (ukeys & 0xFFFFFFFF).astype(np.int32)
-                if_cad = (31 - (ukeys >> 32)).astype(np.int32)
+                # reader cadence | source cadence << 8: the interface pass needs
+                # no dependent node-cadence lookup
+                if_cad = ((31 - (ukeys >> 32)) | (node_cad[if_gid].astype(np.int64) << 8)).astype(np.int32)
         # per-tile metadata in launch order: {g0, g1, level | cadence<<8 | faces<<16, leaf}
         starts, levels, a3 = td["starts"], td["level"], td["anchor3"]
         L = td["max_depth"]

@@ -78,7 +78,7 @@ def build_blobs(table: np.ndarray, prog: dict, n_iface: int, starts: np.ndarray,
     #    the pairs of one (cadence, source leaf) are contiguous
     if n_iface:
         if_gid = prog["if_gid"][:n_iface].astype(np.int64)
-        if_cad = prog["if_cad"][:n_iface].astype(np.int64)
+        if_cad = prog["if_cad"][:n_iface].astype(np.int64) & 0xFF  # reader cadence
         if_leaf = np.searchsorted(starts, if_gid, side="right") - 1
         gkey = (if_cad << 40) | if_leaf
         new = np.ones(n_iface, dtype=bool)
