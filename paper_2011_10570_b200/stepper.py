@@ -555,14 +555,14 @@ class Engine:
         """Load a (2, n_nodes) zip field (host numpy or device tensor): u_pre = u_curr = z, K = 0."""
         import torch
 
-        if isinstance(z, torch.Tensor):
-            zt = z.to(self.device, dtype=torch.float64)
-        else:
-            zt = torch.from_numpy(np.ascontiguousarray(z, dtype=np.float64)).to(self.device, non_blocking=True)
-        if tuple(zt.shape) != (self.NVARS, self.mesh.n_nodes):
-            raise ValueError(f"zip field must be (2, {self.mesh.n_nodes}), got {tuple(zt.shape)}")
-        self._U[0].copy_(zt)
-        self._U[1].copy_(zt)
+        if not isinstance(z, torch.Tensor):
+            z = torch.from_numpy(np.ascontiguousarray(z, dtype=np.float64))
+        if tuple(z.shape) != (self.NVARS, self.mesh.n_nodes):
+            raise ValueError(f"zip field must be (2, {self.mesh.n_nodes}), got {tuple(z.shape)}")
+        # straight into the live buffer (one host->device copy; pinned host
+        # memory makes it a DMA), then device-side into the other parity
+        self._U[0].copy_(z.to(dtype=torch.float64), non_blocking=True)
+        self._U[1].copy_(self._U[0])
         self._K.zero_()
         self.i_fine = 0
 
@@ -579,8 +579,12 @@ class Engine:
         import torch
 
         i = self.i_fine
-        par = torch.tensor([self._cur_parity(i, c) for c in range(self.l_max + 1)], device=self.device)
-        sel = par[self._node_cad_t].bool().unsqueeze(0)
+        key = tuple(self._cur_parity(i, c) for c in range(self.l_max + 1))
+        cache = self.__dict__.setdefault("_sel_cache", {})
+        sel = cache.get(key)
+        if sel is None:  # which u buffer is live, per node: a function of the cadence parities only
+            par = torch.tensor(key, device=self.device)
+            sel = cache[key] = par[self._node_cad_t].bool().unsqueeze(0)
         return torch.where(sel, self._U[1], self._U[0])
 
     def current_zip(self) -> np.ndarray:
