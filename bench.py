@@ -132,6 +132,14 @@ def _workload(name: str) -> str:
             f"{c.tableau.upper()}, CFL {c.cfl}; step = one LTS coarse round")
 
 
+def _speedup_model(mesh, work_ratio):
+    from paper_2011_10570_b200.perfmodel import estimate, histogram_from_mesh
+
+    est = estimate(histogram_from_mesh(mesh.blocks))
+    return {"perfmodel_speedup": est.speedup, "perfmodel_bound": est.bound,
+            "zip_node_work_ratio": work_ratio}
+
+
 def _ncu_traffic():
     """DRAM bytes per stage launch from the committed ncu capture
     (profiles/traffic.json, written by tools/ncu_traffic.py from one
@@ -350,6 +358,8 @@ def run_ours(args):
         "gts": {"value": gts_value, "ms_per_step": gts["ms"] / args.steps,
                 "units_per_step": gts["units_per_step"]},
         "lts_vs_gts_wall_speedup": gts["ms"] / lts["ms"],
+        # the reference's work model (perfmodel.py:52-71) and the zip-node work ratio, beside the measured speedup
+        "lts_vs_gts_model": _speedup_model(mesh, gts["units_per_step"] / lts["units_per_step"]),
         "lts_gts_equivalent_rate": gts["units_per_step"] * args.steps / (lts["ms"] * 1e-3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note,
