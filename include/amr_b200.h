@@ -238,6 +238,22 @@ int amr_unpack_ranges(int64_t n_ranges, const int64_t* range_start, const int64_
                       const int64_t* range_off, int width, const double* buf, double* dst,
                       int64_t total, void* stream);
 
+/* -------------------------------------------------------------- wavelet -- */
+
+/* Interpolation-residual refinement coefficient of n octants
+ * (wavelet_coefficient, wavelet.py:70-105) and, when `flags` is non-NULL, the
+ * per-octant decision in the same launch: mode 0 = refine_flags
+ * (wavelet.py:108-124; 1 refine, 0 keep, -1 coarsen, coarsen_thr =
+ * coarsen_factor*tolerance), mode 1 = refinement_predicate (wavelet.py:127-144;
+ * 1 split, 0 leaf).  values: device [n][npd^dim] samples on each octant's
+ * closed tensor grid (octant_samples, wavelet.py:57-67; last axis fastest);
+ * W: device [npd][(npd+1)/2], the reference's _lagrange_matrix(xs[::2], xs)
+ * (wavelet.py:41-54); levels: device [n] (NULL when flags is NULL); coeff:
+ * device [n] or NULL.  npd odd, 3..15; dim 2 or 3. */
+int amr_wavelet_coeff(int dim, int npd, int64_t n, const double* values, const double* W,
+                      const int32_t* levels, int mode, double tol, double coarsen_thr,
+                      int min_level, int max_level, double* coeff, int8_t* flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1373,3 +1373,73 @@ int ora_engine_advance(OraEngine* e, int64_t n_keys, const int64_t* keys, const 
   e->i_fine++;
   return 0;
 }
+
+/* ------------------------------------------------------------ wavelet -- */
+/* Interpolation residual of n octants (wavelet.py:94-103), TEST ORACLE.
+ * values [n][npd^dim] (last axis fastest), W [npd][nc].  Restates the
+ * reference literally: recon = coarse; for each axis in order, recon =
+ * tensordot(W, recon, axis) (an ascending FMA chain from 0 over the full
+ * coarse axis, the OpenBLAS dgemm bits on the generating host); then the max
+ * of |values - recon| over nodes with any odd index, NaN-propagating like
+ * np.max.  Full tensors at every step, as the reference builds them. */
+int ora_wavelet_coeff(int dim, int npd, int64_t n, const double* values, const double* W, double* coeff) {
+  if (dim < 1 || dim > 3 || npd < 3 || (npd % 2) == 0) return ora_fail("ora_wavelet_coeff: bad dim/npd");
+  const int nc = (npd + 1) / 2;
+  int64_t nv = 1;
+  for (int d = 0; d < dim; ++d) nv *= npd;
+#pragma omp parallel for schedule(static)
+  for (int64_t o = 0; o < n; ++o) {
+    const double* v = values + o * nv;
+    double a[15 * 15 * 15], b[15 * 15 * 15];
+    int shp[3];
+    for (int d = 0; d < dim; ++d) shp[d] = nc;
+    /* coarse = values[::2, ::2, ...] */
+    int64_t nco = 1;
+    for (int d = 0; d < dim; ++d) nco *= nc;
+    for (int64_t t = 0; t < nco; ++t) {
+      int64_t r = t, src = 0, mul = 1;
+      for (int d = dim - 1; d >= 0; --d) {
+        int idx = (int)(r % nc);
+        r /= nc;
+        src += (int64_t)(2 * idx) * mul;
+        mul *= npd;
+      }
+      a[t] = v[src];
+    }
+    for (int ax = 0; ax < dim; ++ax) {
+      int nshp[3];
+      for (int d = 0; d < dim; ++d) nshp[d] = shp[d];
+      nshp[ax] = npd;
+      int64_t tot = 1;
+      for (int d = 0; d < dim; ++d) tot *= nshp[d];
+      for (int64_t t = 0; t < tot; ++t) {
+        int idx[3];
+        int64_t r = t;
+        for (int d = dim - 1; d >= 0; --d) { idx[d] = (int)(r % nshp[d]); r /= nshp[d]; }
+        double acc = 0.0;
+        for (int k = 0; k < nc; ++k) {
+          int64_t s = 0;
+          for (int d = 0; d < dim; ++d) s = s * shp[d] + (d == ax ? k : idx[d]);
+          acc = fma(W[idx[ax] * nc + k], a[s], acc);
+        }
+        b[t] = acc;
+      }
+      memcpy(a, b, sizeof(double) * tot);
+      for (int d = 0; d < dim; ++d) shp[d] = nshp[d];
+    }
+    double m = 0.0;
+    int any = 0;
+    for (int64_t t = 0; t < nv; ++t) {
+      int64_t r = t;
+      int odd = 0;
+      for (int d = dim - 1; d >= 0; --d) { odd |= (int)(r % npd) & 1; r /= npd; }
+      if (!odd) continue;
+      double dlt = fabs(v[t] - a[t]);
+      if (!any) m = dlt;
+      else if (!isnan(m) && (isnan(dlt) || dlt > m)) m = dlt;
+      any = 1;
+    }
+    coeff[o] = m;
+  }
+  return 0;
+}

@@ -42,6 +42,7 @@ def lib():
                 pass
         L = C.CDLL(LIB_PATH)
         sig = {
+            "ora_wavelet_coeff": ([C.c_int, C.c_int, C.c_int64, _f64p, _f64p, _f64p], C.c_int),
             "ora_morton_sort": ([C.c_int, C.c_int, C.c_int64, _i32p, _i32p, _i64p], C.c_int),
             "ora_balance": ([C.c_int, C.c_int, C.c_int64, _i32p, _i32p, _i64p], _vp),
             "ora_tree_fetch": ([_vp, _i32p, _i32p], C.c_int),
@@ -328,3 +329,57 @@ def _stencils():
 
     return [fw(2, range(-2, 3)), fw(2, range(0, 6)), fw(2, range(-1, 5)),
             fw(1, range(-2, 3)), fw(1, range(0, 5)), fw(1, range(-1, 4))]
+
+
+# ---------------------------------------------------------------------------
+# wavelet refinement criterion (wavelet.py:41-144), restated
+
+def lagrange_matrix(src, dst, max_points=4):
+    """Sliding-window Lagrange weights, wavelet.py:41-54 (same window rule and product order)."""
+    npts = min(max_points, len(src))
+    out = np.zeros((len(dst), len(src)))
+    for i, x in enumerate(dst):
+        j0 = max(0, min(int(np.searchsorted(src, x) - npts // 2), len(src) - npts))
+        for a in range(npts):
+            w = 1.0
+            for b in range(npts):
+                if a != b:
+                    w *= (x - src[j0 + b]) / (src[j0 + a] - src[j0 + b])
+            out[i, j0 + a] = w
+    return out
+
+
+def wavelet_samples(f, anchor, level, max_depth, npd, domain_lo=None, domain_hi=None):
+    """f on one octant's closed npd^dim grid, wavelet.py:57-67,86-92."""
+    dim = len(anchor)
+    lo_d = (0.0,) * dim if domain_lo is None else domain_lo
+    hi_d = (float(1 << max_depth),) * dim if domain_hi is None else domain_hi
+    top = float(1 << max_depth)
+    side = 1 << (max_depth - level)
+    axes = [np.linspace(lo_d[d] + (anchor[d] / top) * (hi_d[d] - lo_d[d]),
+                        lo_d[d] + ((anchor[d] + side) / top) * (hi_d[d] - lo_d[d]), npd) for d in range(dim)]
+    return np.asarray(f(*np.meshgrid(*axes, indexing="ij")), dtype=float)
+
+
+def wavelet_coeffs(values, npd, dim):
+    """Coefficients of (n, npd^dim) samples through the C restatement."""
+    v = np.ascontiguousarray(values, dtype=np.float64).reshape(-1, npd ** dim)
+    xs = np.linspace(0.0, 1.0, npd)
+    W = np.ascontiguousarray(lagrange_matrix(xs[::2], xs))
+    out = np.zeros(v.shape[0])
+    rc = lib().ora_wavelet_coeff(dim, npd, v.shape[0], v.ctypes.data_as(_f64p), W.ctypes.data_as(_f64p),
+                                 out.ctypes.data_as(_f64p))
+    if rc:
+        raise ValueError(lib().ora_last_error().decode())
+    return out
+
+
+def wavelet_flag_codes(coeff, levels, tolerance, coarsen_factor, min_level, max_level):
+    """refine_flags' rule, wavelet.py:118-123: 1 refine, 0 keep, -1 coarsen."""
+    out = np.zeros(len(coeff), dtype=np.int8)
+    for i, (c, lv) in enumerate(zip(coeff, levels)):
+        if c > tolerance and lv < max_level:
+            out[i] = 1
+        elif c < coarsen_factor * tolerance and lv > min_level:
+            out[i] = -1
+    return out

@@ -101,6 +101,8 @@ SIGNATURES = {
                        C.POINTER(AmrStageParams), _vp], C.c_int),
     "amr_pack_ranges": ([C.c_int64, _vp, _vp, _vp, C.c_int, _vp, _vp, C.c_int64, _vp], C.c_int),
     "amr_unpack_ranges": ([C.c_int64, _vp, _vp, _vp, C.c_int, _vp, _vp, C.c_int64, _vp], C.c_int),
+    "amr_wavelet_coeff": ([C.c_int, C.c_int, C.c_int64, _vp, _vp, _vp, C.c_int, C.c_double, C.c_double,
+                           C.c_int, C.c_int, _vp, _vp, _vp], C.c_int),
 }
 
 _LIB = None

@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libamr_b200.so")
 INCLUDE = os.path.abspath(os.path.join(HERE, "..", "include"))
-SOURCES = ["amr_kernels.cu", "amr_mesh.cpp"]
+SOURCES = ["amr_kernels.cu", "amr_wavelet.cu", "amr_mesh.cpp"]
 HEADERS = ["amr_stage_pipe.cuh", "amr_stage_blob.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

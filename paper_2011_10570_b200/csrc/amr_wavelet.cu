@@ -1,0 +1,264 @@
+// amr_wavelet.cu — sm_100a kernel for the interpolation-residual ("wavelet")
+// refinement coefficient of many octants at once (wavelet.py:70-144).
+//
+// Per octant the reference samples a field on an odd npd^D closed tensor
+// grid, rebuilds it from the even-index nodes with sliding 4-point Lagrange
+// windows one axis after the other (np.tensordot per axis, wavelet.py:94-97),
+// and takes the max |value - reconstruction| over nodes with at least one odd
+// index (wavelet.py:98-103).  The refine/keep/coarsen decision
+// (wavelet.py:108-124) or the construction predicate (wavelet.py:127-144) is
+// applied in the same launch.
+//
+// Layout: values [n][npd^D] fp64, last axis fastest (meshgrid "ij"), so one
+// octant is one contiguous run that one warp streams in with coalesced loads.
+// Work per octant is ~4*npd^D flops against 8*npd^D bytes: HBM-bound, so a
+// warp per octant, as many warps resident per SM as shared memory allows,
+// and no tensor cores.
+//
+// Bit parity: each reconstructed value is an np.tensordot output.  On the
+// generating host that is OpenBLAS dgemm, whose outputs equal an ascending
+// FMA chain from 0 over the full coarse axis (zeros included) — verified
+// against the reference in tests/test_wavelet.py.  The file is compiled with
+// -fmad=false; fma() appears only there.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <string>
+
+#include "../../include/amr_b200.h"
+
+extern "C" void amr_set_error_internal(const char* msg);
+
+namespace {
+
+constexpr int WV_MAX_NPD = 15;
+
+__device__ __forceinline__ double nan_max(double m, double d) {
+  // np.max propagates NaN; otherwise the plain maximum
+  if (m != m) return m;
+  return (d != d || d > m) ? d : m;
+}
+
+template <int DIM, int NPD>
+struct WvShape {
+  static constexpr int NC = (NPD + 1) / 2;
+  static constexpr int NV = DIM == 2 ? NPD * NPD : NPD * NPD * NPD;
+  static constexpr int N1 = DIM == 2 ? NPD * NC : NPD * NC * NC;  // after axis 0
+  static constexpr int N2 = DIM == 2 ? 0 : NPD * NPD * NC;        // after axis 1 (3D)
+  static constexpr int PER_WARP = NV + N1 + N2;
+  static constexpr int NW = NPD * NC;
+  static constexpr int PRE = (NV + 31) / 32;  // samples per lane
+  static constexpr bool PREFETCH = PRE <= 24;  // next octant held in registers
+};
+
+// One warp per octant; the next octant's samples are loaded into registers
+// while the current one is reduced from shared memory, so each warp keeps one
+// octant's HBM read in flight.  NPD is a template parameter: every index
+// division is by a constant and every chain is unrolled.
+template <int DIM, int NPD>
+__global__ void __launch_bounds__(256) wavelet_kernel(int64_t n, const double* __restrict__ V,
+                                                      const double* __restrict__ Wg, const int32_t* __restrict__ levels,
+                                                      int mode, double tol, double coarsen_thr, int min_level,
+                                                      int max_level, double* __restrict__ coeff,
+                                                      int8_t* __restrict__ flags) {
+  using S = WvShape<DIM, NPD>;
+  constexpr int nc = S::NC, npd = NPD, nv = S::NV;
+  extern __shared__ double sm[];
+  const int warps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* W = sm;  // [npd][nc]
+  for (int i = threadIdx.x; i < S::NW; i += blockDim.x) W[i] = Wg[i];
+  double* v = sm + S::NW + warp * S::PER_WARP;
+  double* r1 = v + nv;
+  double* r2 = r1 + S::N1;
+  __syncthreads();
+
+  const int64_t stride = (int64_t)gridDim.x * warps;
+  int64_t oct = (int64_t)blockIdx.x * warps + warp;
+  double pre[S::PREFETCH ? S::PRE : 1];
+  if (S::PREFETCH && oct < n) {
+#pragma unroll
+    for (int q = 0; q < S::PRE; ++q) {
+      const int i = lane + 32 * q;
+      if (i < nv) pre[q] = __ldcs(V + oct * nv + i);
+    }
+  }
+  for (; oct < n; oct += stride) {
+    if (S::PREFETCH) {
+#pragma unroll
+      for (int q = 0; q < S::PRE; ++q) {
+        const int i = lane + 32 * q;
+        if (i < nv) v[i] = pre[q];
+      }
+      const int64_t nxt = oct + stride;
+      if (nxt < n) {
+#pragma unroll
+        for (int q = 0; q < S::PRE; ++q) {
+          const int i = lane + 32 * q;
+          if (i < nv) pre[q] = __ldcs(V + nxt * nv + i);
+        }
+      }
+    } else {
+      for (int i = lane; i < nv; i += 32) v[i] = __ldcs(V + oct * nv + i);
+    }
+    __syncwarp();
+    double m = 0.0;
+    bool any = false;
+    if (DIM == 2) {
+      // r1[i][b] = sum_a W[i][a] * v[2a][2b]   (axis 0)
+#pragma unroll
+      for (int t0 = 0; t0 < S::N1; t0 += 32) {
+        const int t = t0 + lane;
+        if (t < S::N1) {
+          const int i = t / nc, b = t - i * nc;
+          double acc = 0.0;
+#pragma unroll
+          for (int a = 0; a < nc; ++a) acc = fma(W[i * nc + a], v[(2 * a) * npd + 2 * b], acc);
+          r1[t] = acc;
+        }
+      }
+      __syncwarp();
+      // rec[i][j] = sum_b W[j][b] * r1[i][b]   (axis 1), odd nodes only
+#pragma unroll
+      for (int t0 = 0; t0 < nv; t0 += 32) {
+        const int t = t0 + lane;
+        const int i = t / npd, j = t - i * npd;
+        if (t < nv && ((i | j) & 1)) {
+          double acc = 0.0;
+#pragma unroll
+          for (int b = 0; b < nc; ++b) acc = fma(W[j * nc + b], r1[i * nc + b], acc);
+          const double d = fabs(v[t] - acc);
+          m = any ? nan_max(m, d) : d;
+          any = true;
+        }
+      }
+    } else {
+      // r1[i][b][c] = sum_a W[i][a] * v[2a][2b][2c]
+#pragma unroll
+      for (int t0 = 0; t0 < S::N1; t0 += 32) {
+        const int t = t0 + lane;
+        if (t < S::N1) {
+          const int i = t / (nc * nc), bc = t - i * nc * nc, b = bc / nc, c = bc - b * nc;
+          double acc = 0.0;
+#pragma unroll
+          for (int a = 0; a < nc; ++a) acc = fma(W[i * nc + a], v[((2 * a) * npd + 2 * b) * npd + 2 * c], acc);
+          r1[t] = acc;
+        }
+      }
+      __syncwarp();
+      // r2[i][j][c] = sum_b W[j][b] * r1[i][b][c]
+#pragma unroll
+      for (int t0 = 0; t0 < S::N2; t0 += 32) {
+        const int t = t0 + lane;
+        if (t < S::N2) {
+          const int i = t / (npd * nc), jc = t - i * npd * nc, j = jc / nc, c = jc - j * nc;
+          double acc = 0.0;
+#pragma unroll
+          for (int b = 0; b < nc; ++b) acc = fma(W[j * nc + b], r1[(i * nc + b) * nc + c], acc);
+          r2[t] = acc;
+        }
+      }
+      __syncwarp();
+      // rec[i][j][k] = sum_c W[k][c] * r2[i][j][c], odd nodes only
+#pragma unroll 4
+      for (int t0 = 0; t0 < nv; t0 += 32) {
+        const int t = t0 + lane;
+        const int i = t / (npd * npd), jk = t - i * npd * npd, j = jk / npd, k = jk - j * npd;
+        if (t < nv && ((i | j | k) & 1)) {
+          double acc = 0.0;
+#pragma unroll
+          for (int c = 0; c < nc; ++c) acc = fma(W[k * nc + c], r2[(i * npd + j) * nc + c], acc);
+          const double d = fabs(v[t] - acc);
+          m = any ? nan_max(m, d) : d;
+          any = true;
+        }
+      }
+    }
+    // warp max; lanes without an odd node contribute nothing
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, m, off);
+      const int oa = __shfl_xor_sync(0xffffffffu, (int)any, off);
+      if (oa) m = any ? nan_max(m, o) : o;
+      any = any || oa;
+    }
+    if (lane == 0) {
+      if (coeff) coeff[oct] = m;
+      if (flags) {
+        const int lvl = levels[oct];
+        int8_t f;
+        if (mode == 0) {  // refine_flags (wavelet.py:118-123)
+          if (m > tol && lvl < max_level) f = 1;
+          else if (m < coarsen_thr && lvl > min_level) f = -1;
+          else f = 0;
+        } else {  // refinement_predicate (wavelet.py:137-142)
+          f = lvl < min_level ? 1 : (lvl >= max_level ? 0 : (m > tol ? 1 : 0));
+        }
+        flags[oct] = f;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+using WvKernel = void (*)(int64_t, const double*, const double*, const int32_t*, int, double, double, int, int,
+                          double*, int8_t*);
+
+template <int DIM>
+WvKernel pick(int npd, int* per_warp) {
+#define WV_CASE(N)                         \
+  case N:                                  \
+    *per_warp = WvShape<DIM, N>::PER_WARP; \
+    return wavelet_kernel<DIM, N>;
+  switch (npd) {
+    WV_CASE(3) WV_CASE(5) WV_CASE(7) WV_CASE(9) WV_CASE(11) WV_CASE(13) WV_CASE(15)
+  }
+#undef WV_CASE
+  return nullptr;
+}
+
+int fail(const char* msg) {
+  amr_set_error_internal(msg);
+  return AMR_EINVAL;
+}
+
+}  // namespace
+
+extern "C" int amr_wavelet_coeff(int dim, int npd, int64_t n, const double* values, const double* W,
+                                 const int32_t* levels, int mode, double tol, double coarsen_thr, int min_level,
+                                 int max_level, double* coeff, int8_t* flags, void* stream) {
+  if (dim != 2 && dim != 3) return fail("amr_wavelet_coeff: dim must be 2 or 3");
+  if (npd < 3 || npd % 2 == 0 || npd > WV_MAX_NPD) return fail("amr_wavelet_coeff: nodes_per_dim must be odd, 3..15");
+  if (n < 0 || mode < 0 || mode > 1) return fail("amr_wavelet_coeff: bad n or mode");
+  if (flags && !levels) return fail("amr_wavelet_coeff: flags need levels");
+  if (n == 0) return AMR_OK;
+  const int nc = (npd + 1) / 2;
+  int per_warp = 0;
+  WvKernel kern = dim == 2 ? pick<2>(npd, &per_warp) : pick<3>(npd, &per_warp);
+  const size_t budget = 48 * 1024;  // per CTA: several CTAs resident per SM
+  int warps = (int)((budget / sizeof(double) - npd * nc) / per_warp);
+  warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
+  const size_t smem = sizeof(double) * (npd * nc + (size_t)warps * per_warp);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = 1;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
+  if (e != cudaSuccess) {
+    amr_set_error_internal((std::string("amr_wavelet_coeff: ") + cudaGetErrorString(e)).c_str());
+    return AMR_ECUDA;
+  }
+  const int64_t need = (n + warps - 1) / warps;
+  const int64_t cap = (int64_t)sms * (per_sm < 1 ? 1 : per_sm);
+  const int grid = (int)(need < cap ? need : cap);
+  kern<<<grid, warps * 32, smem, (cudaStream_t)stream>>>(n, values, W, levels, mode, tol, coarsen_thr,
+                                                          min_level, max_level, coeff, flags);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    amr_set_error_internal((std::string("amr_wavelet_coeff launch: ") + cudaGetErrorString(e)).c_str());
+    return AMR_ECUDA;
+  }
+  return AMR_OK;
+}

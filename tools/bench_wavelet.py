@@ -1,0 +1,88 @@
+"""Benchmark of the wavelet refinement criterion.
+
+Workload: every leaf of a uniform level-6 3D tree (262 144 octants) on
+[-1,1]^3, nodes_per_dim 7 (the reference default), field tests' gauss3.
+  * device: amr_wavelet_coeff on device-resident samples (720 MB > L2),
+    CUDA events around K launches; roofline = 8 B x npd^3 read + 8 B coeff +
+    4 B level + 1 B flag per octant against measured HBM GB/s;
+  * e2e: W.refine_flags(f, tree, policy) — host sampling + f, H2D, kernel,
+    D2H of the flags — wall time;
+  * cpu: oracle/amr_oracle.c ora_wavelet_coeff on the same samples (C +
+    OpenMP, all host cores): the reference's arithmetic restated.
+One JSON line on stdout.
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+from paper_2011_10570_b200 import wavelet as W  # noqa: E402
+from paper_2011_10570_b200.octree import uniform_tree  # noqa: E402
+from wavelet_fields import FIELDS  # noqa: E402
+
+
+def main(steps=20, warmup=3, level=6, npd=7):
+    dim, L = 3, level
+    tree = uniform_tree(dim, L, level)
+    an, lv = tree.arrays()
+    lo, hi = (-1.0,) * 3, (1.0,) * 3
+    f = FIELDS["gauss3"]
+    pol = W.RefinePolicy(tolerance=1e-4, min_level=1, max_level=L + 1)
+    n = len(an)
+    vals = W._sample_values(f, W._sample_axes(an.astype(np.int64), lv, L, lo, hi, npd), npd)
+    dv = torch.from_numpy(vals).cuda()
+    dl = torch.from_numpy(lv).cuda()
+    for _ in range(warmup):
+        W.coefficients_from_values(dv, npd, dim, dl, pol)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        W.coefficients_from_values(dv, npd, dim, dl, pol)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / steps
+    bytes_per = 8 * npd ** dim + 8 + 4 + 1
+    gbs = bytes_per * n / (ms * 1e-3) / 1e9
+    peak = 6456.8
+    try:
+        peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        pass
+    # e2e through the drop-in API (host f, pinned H2D, kernel, D2H)
+    W.refine_codes(f, tree, pol, npd, lo, hi)
+    t0 = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        codes = W.refine_codes(f, tree, pol, npd, lo, hi)
+    e2e_s = (time.perf_counter() - t0) / reps
+    out = {
+        "metric": "wavelet coefficients + flags (octants/s)", "value": n / (ms * 1e-3), "unit": "octants/s",
+        "ms_per_launch": ms, "octants": n, "nodes_per_dim": npd, "dim": dim,
+        "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                     "bytes_per_octant": bytes_per},
+        "e2e": {"value": n / e2e_s, "unit": "octants/s", "s_per_call": e2e_s,
+                "h2d_bytes": int(vals.nbytes + 4 * n), "d2h_bytes": int(9 * n)},
+        "flags_hist": {str(k): int(v) for k, v in zip(*np.unique(codes, return_counts=True))},
+    }
+    if "--no-cpu" not in sys.argv:
+        from oracle import oracle as O
+
+        sub = vals[: n // 4]
+        t0 = time.perf_counter()
+        O.wavelet_coeffs(sub, npd, dim)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": len(sub) / dt, "unit": "octants/s", "cores": len(os.sched_getaffinity(0)),
+                               "kind": "port", "sample": f"{len(sub)} octants, oracle ora_wavelet_coeff (C+OpenMP)"}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
