@@ -40,6 +40,19 @@ __device__ __forceinline__ double nan_max(double m, double d) {
   return (d != d || d > m) ? d : m;
 }
 
+// W per npd, back to back in constant memory (npd = 3, 5, ..., 15): the 3D
+// path reads it with warp-uniform indices.  Filled before each launch.
+constexpr int WV_CONST_TOTAL = 3 * 2 + 5 * 3 + 7 * 4 + 9 * 5 + 11 * 6 + 13 * 7 + 15 * 8;
+__constant__ double cW[WV_CONST_TOTAL];
+template <int NPD>
+struct WvOff {
+  static constexpr int value = NPD <= 3 ? 0 : WvOff<NPD - 2>::value + (NPD - 2) * ((NPD - 1) / 2);
+};
+template <>
+struct WvOff<3> {
+  static constexpr int value = 0;
+};
+
 template <int DIM, int NPD>
 struct WvShape {
   static constexpr int NC = (NPD + 1) / 2;
@@ -49,7 +62,8 @@ struct WvShape {
   static constexpr int PER_WARP = NV + N1 + N2;
   static constexpr int NW = NPD * NC;
   static constexpr int PRE = (NV + 31) / 32;  // samples per lane
-  static constexpr bool PREFETCH = PRE <= 24;  // next octant held in registers
+  static constexpr bool PREFETCH = PRE <= 12;  // next octant held in registers
+  static constexpr int MINB = PREFETCH && DIM == 3 ? 4 : 1;  // 3D: 32 warps per SM
 };
 
 // One warp per octant; the next octant's samples are loaded into registers
@@ -57,7 +71,7 @@ struct WvShape {
 // octant's HBM read in flight.  NPD is a template parameter: every index
 // division is by a constant and every chain is unrolled.
 template <int DIM, int NPD>
-__global__ void __launch_bounds__(256) wavelet_kernel(int64_t n, const double* __restrict__ V,
+__global__ void __launch_bounds__(256, WvShape<DIM, NPD>::MINB) wavelet_kernel(int64_t n, const double* __restrict__ V,
                                                       const double* __restrict__ Wg, const int32_t* __restrict__ levels,
                                                       int mode, double tol, double coarsen_thr, int min_level,
                                                       int max_level, double* __restrict__ coeff,
@@ -134,44 +148,70 @@ __global__ void __launch_bounds__(256) wavelet_kernel(int64_t n, const double* _
         }
       }
     } else {
-      // r1[i][b][c] = sum_a W[i][a] * v[2a][2b][2c]
+      // 3D as 1-D lines: a lane owns one line along the axis being rebuilt,
+      // holds its nc coarse inputs in registers and emits the npd outputs
+      // with compile-time output index, so W[i][a] is a warp-uniform
+      // constant-bank operand (cW) and no index is divided at run time.
+      const double* Wc = cW + WvOff<NPD>::value;
+      // axis 0: r1[i][b][c] = sum_a W[i][a] * v[2a][2b][2c]; lines (b, c)
 #pragma unroll
-      for (int t0 = 0; t0 < S::N1; t0 += 32) {
-        const int t = t0 + lane;
-        if (t < S::N1) {
-          const int i = t / (nc * nc), bc = t - i * nc * nc, b = bc / nc, c = bc - b * nc;
-          double acc = 0.0;
+      for (int l0 = 0; l0 < nc * nc; l0 += 32) {
+        const int l = l0 + lane;
+        if (l < nc * nc) {
+          const int b = l / nc, c = l - b * nc;
+          double x[nc];
 #pragma unroll
-          for (int a = 0; a < nc; ++a) acc = fma(W[i * nc + a], v[((2 * a) * npd + 2 * b) * npd + 2 * c], acc);
-          r1[t] = acc;
+          for (int q = 0; q < nc; ++q) x[q] = v[((2 * q) * npd + 2 * b) * npd + 2 * c];
+#pragma unroll
+          for (int i = 0; i < npd; ++i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < nc; ++q) acc = fma(Wc[i * nc + q], x[q], acc);
+            r1[i * nc * nc + l] = acc;
+          }
         }
       }
       __syncwarp();
-      // r2[i][j][c] = sum_b W[j][b] * r1[i][b][c]
+      // axis 1: r2[i][j][c] = sum_b W[j][b] * r1[i][b][c]; lines (i, c)
 #pragma unroll
-      for (int t0 = 0; t0 < S::N2; t0 += 32) {
-        const int t = t0 + lane;
-        if (t < S::N2) {
-          const int i = t / (npd * nc), jc = t - i * npd * nc, j = jc / nc, c = jc - j * nc;
-          double acc = 0.0;
+      for (int l0 = 0; l0 < npd * nc; l0 += 32) {
+        const int l = l0 + lane;
+        if (l < npd * nc) {
+          const int i = l / nc, c = l - i * nc;
+          double x[nc];
 #pragma unroll
-          for (int b = 0; b < nc; ++b) acc = fma(W[j * nc + b], r1[(i * nc + b) * nc + c], acc);
-          r2[t] = acc;
+          for (int q = 0; q < nc; ++q) x[q] = r1[(i * nc + q) * nc + c];
+#pragma unroll
+          for (int j = 0; j < npd; ++j) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < nc; ++q) acc = fma(Wc[j * nc + q], x[q], acc);
+            r2[(i * npd + j) * nc + c] = acc;
+          }
         }
       }
       __syncwarp();
-      // rec[i][j][k] = sum_c W[k][c] * r2[i][j][c], odd nodes only
-#pragma unroll 4
-      for (int t0 = 0; t0 < nv; t0 += 32) {
-        const int t = t0 + lane;
-        const int i = t / (npd * npd), jk = t - i * npd * npd, j = jk / npd, k = jk - j * npd;
-        if (t < nv && ((i | j | k) & 1)) {
-          double acc = 0.0;
+      // axis 2: rec[i][j][k] = sum_c W[k][c] * r2[i][j][c]; lines (i, j);
+      // residual at nodes with any odd index
 #pragma unroll
-          for (int c = 0; c < nc; ++c) acc = fma(W[k * nc + c], r2[(i * npd + j) * nc + c], acc);
-          const double d = fabs(v[t] - acc);
-          m = any ? nan_max(m, d) : d;
-          any = true;
+      for (int l0 = 0; l0 < npd * npd; l0 += 32) {
+        const int l = l0 + lane;
+        if (l < npd * npd) {
+          const int i = l / npd, j = l - i * npd;
+          const bool even_ij = !((i | j) & 1);
+          double x[nc];
+#pragma unroll
+          for (int q = 0; q < nc; ++q) x[q] = r2[l * nc + q];
+#pragma unroll
+          for (int k = 0; k < npd; ++k) {
+            if (even_ij && !(k & 1)) continue;
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < nc; ++q) acc = fma(Wc[k * nc + q], x[q], acc);
+            const double d = fabs(v[l * npd + k] - acc);
+            m = any ? nan_max(m, d) : d;
+            any = true;
+          }
         }
       }
     }
@@ -236,6 +276,8 @@ extern "C" int amr_wavelet_coeff(int dim, int npd, int64_t n, const double* valu
   const int nc = (npd + 1) / 2;
   int per_warp = 0;
   WvKernel kern = dim == 2 ? pick<2>(npd, &per_warp) : pick<3>(npd, &per_warp);
+  int woff = 0;
+  for (int q = 3; q < npd; q += 2) woff += q * ((q + 1) / 2);
   const size_t budget = 48 * 1024;  // per CTA: several CTAs resident per SM
   int warps = (int)((budget / sizeof(double) - npd * nc) / per_warp);
   warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
@@ -244,7 +286,10 @@ extern "C" int amr_wavelet_coeff(int dim, int npd, int64_t n, const double* valu
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int per_sm = 1;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaMemcpyToSymbolAsync(cW, W, sizeof(double) * npd * nc, sizeof(double) * woff,
+                                          cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
   if (e != cudaSuccess) {
     amr_set_error_internal((std::string("amr_wavelet_coeff: ") + cudaGetErrorString(e)).c_str());
