@@ -59,16 +59,14 @@ struct WvShape {
   static constexpr int NV = DIM == 2 ? NPD * NPD : NPD * NPD * NPD;
   static constexpr int N1 = DIM == 2 ? NPD * NC : NPD * NC * NC;  // after axis 0
   static constexpr int N2 = DIM == 2 ? 0 : NPD * NPD * NC;        // after axis 1 (3D)
-  static constexpr int PER_WARP = NV + N1 + N2;
+  static constexpr int PER_WARP = 2 * NV + N1 + N2;
   static constexpr int NW = NPD * NC;
-  static constexpr int PRE = (NV + 31) / 32;  // samples per lane
-  static constexpr bool PREFETCH = PRE <= 12;  // next octant held in registers
-  static constexpr int MINB = PREFETCH && DIM == 3 ? 4 : 1;  // 3D: 32 warps per SM
+  static constexpr int MINB = DIM == 3 && NPD <= 7 ? 3 : 1;
 };
 
-// One warp per octant; the next octant's samples are loaded into registers
-// while the current one is reduced from shared memory, so each warp keeps one
-// octant's HBM read in flight.  NPD is a template parameter: every index
+// One warp per octant; the next octant's samples are copied (cp.async) into
+// a second shared buffer while the current one is reduced, so each warp keeps
+// one octant's HBM read in flight.  NPD is a template parameter: every index
 // division is by a constant and every chain is unrolled.
 template <int DIM, int NPD>
 __global__ void __launch_bounds__(256, WvShape<DIM, NPD>::MINB) wavelet_kernel(int64_t n, const double* __restrict__ V,
@@ -83,39 +81,31 @@ __global__ void __launch_bounds__(256, WvShape<DIM, NPD>::MINB) wavelet_kernel(i
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* W = sm;  // [npd][nc]
   for (int i = threadIdx.x; i < S::NW; i += blockDim.x) W[i] = Wg[i];
-  double* v = sm + S::NW + warp * S::PER_WARP;
-  double* r1 = v + nv;
+  double* vb = sm + S::NW + warp * S::PER_WARP;  // two sample buffers
+  double* r1 = vb + 2 * nv;
   double* r2 = r1 + S::N1;
   __syncthreads();
 
+  // Samples move HBM -> shared memory by cp.async (no register staging), one
+  // octant ahead: while octant j is reduced from one buffer, octant j+stride
+  // lands in the other.
   const int64_t stride = (int64_t)gridDim.x * warps;
   int64_t oct = (int64_t)blockIdx.x * warps + warp;
-  double pre[S::PREFETCH ? S::PRE : 1];
-  if (S::PREFETCH && oct < n) {
-#pragma unroll
-    for (int q = 0; q < S::PRE; ++q) {
-      const int i = lane + 32 * q;
-      if (i < nv) pre[q] = __ldcs(V + oct * nv + i);
-    }
-  }
-  for (; oct < n; oct += stride) {
-    if (S::PREFETCH) {
-#pragma unroll
-      for (int q = 0; q < S::PRE; ++q) {
-        const int i = lane + 32 * q;
-        if (i < nv) v[i] = pre[q];
+  auto issue = [&](int64_t o, double* dst) {
+    if (o < n) {
+      const double* src = V + o * nv;
+      for (int i = lane; i < nv; i += 32) {
+        const unsigned d = (unsigned)__cvta_generic_to_shared(dst + i);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src + i) : "memory");
       }
-      const int64_t nxt = oct + stride;
-      if (nxt < n) {
-#pragma unroll
-        for (int q = 0; q < S::PRE; ++q) {
-          const int i = lane + 32 * q;
-          if (i < nv) pre[q] = __ldcs(V + nxt * nv + i);
-        }
-      }
-    } else {
-      for (int i = lane; i < nv; i += 32) v[i] = __ldcs(V + oct * nv + i);
     }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  issue(oct, vb);
+  for (int cur = 0; oct < n; oct += stride, cur ^= 1) {
+    issue(oct + stride, vb + (cur ^ 1) * nv);
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    const double* v = vb + cur * nv;
     __syncwarp();
     double m = 0.0;
     bool any = false;
@@ -278,7 +268,7 @@ extern "C" int amr_wavelet_coeff(int dim, int npd, int64_t n, const double* valu
   WvKernel kern = dim == 2 ? pick<2>(npd, &per_warp) : pick<3>(npd, &per_warp);
   int woff = 0;
   for (int q = 3; q < npd; q += 2) woff += q * ((q + 1) / 2);
-  const size_t budget = 48 * 1024;  // per CTA: several CTAs resident per SM
+  const size_t budget = 72 * 1024;  // per CTA: several CTAs resident per SM
   int warps = (int)((budget / sizeof(double) - npd * nc) / per_warp);
   warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
   const size_t smem = sizeof(double) * (npd * nc + (size_t)warps * per_warp);

@@ -324,6 +324,47 @@ class Mesh:
             out[:, a:b] = arr[:, zp[i]]
         return out
 
+    def leaf_lattice_device(self, zd, var: int = 0):
+        """(n_leaves, ppo^dim) CUDA tensor: every leaf's own ppo^dim lattice
+        nodes (ij order, last axis fastest) from a (nvars, n_nodes) CUDA zip
+        field.  Shared/owned nodes are copies, hanging nodes are the
+        reference's interpolation rows (0 + sum w*z in ascending-gid order,
+        mesh.py:355-398, amr_gather_rows), i.e. the interior of Mesh.unzip
+        restricted to the leaf.  Feeds the wavelet criterion on the solution
+        (wavelet.coefficients_from_values with nodes_per_dim = ppo)."""
+        import torch
+
+        dev = zd.device
+        lt = self.__dict__.get("_lattice_dev")
+        if lt is None or lt[0].device != dev:
+            td = self.tile_data()
+            NI = self.ppo ** self.dim
+            tab = td["table"][:, :NI].astype(np.int64)
+            hang = tab <= -2
+            rows = (-tab[hang] - 2)
+            iptr = td["interp_ptr"]
+            ptr = np.zeros(len(rows) + 1, dtype=np.int64)
+            np.cumsum(iptr[rows + 1] - iptr[rows], out=ptr[1:])
+            lens = iptr[rows + 1] - iptr[rows]
+            take = np.repeat(iptr[rows] - ptr[:-1], lens) + np.arange(int(ptr[-1]), dtype=np.int64)
+            col = td["interp_gid"][take].astype(np.int64)
+            w = td["interp_w"][take]
+            lt = (torch.from_numpy(np.where(hang, 0, tab)).to(dev), torch.from_numpy(hang).to(dev),
+                  torch.from_numpy(ptr).to(dev), torch.from_numpy(col).to(dev), torch.from_numpy(w).to(dev),
+                  len(rows))
+            self.__dict__["_lattice_dev"] = lt
+        tab_d, hang_d, ptr_d, col_d, w_d, nh = lt
+        row = zd[var].contiguous()
+        out = row[tab_d]
+        if nh:
+            hv = torch.empty(nh, dtype=torch.float64, device=dev)
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            _native.check(self._nm.lib.amr_gather_rows(nh, ptr_d.data_ptr(), col_d.data_ptr(), w_d.data_ptr(), 1,
+                                                       row.data_ptr(), row.numel(), hv.data_ptr(), nh, stream),
+                          "amr_gather_rows")
+            out[hang_d] = hv
+        return out
+
     # -- engine view ---------------------------------------------------------------
     def tile_data(self) -> dict:
         """Leaf-tile unzip tables for the stage kernel (see include/amr_b200.h)."""

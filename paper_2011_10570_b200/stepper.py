@@ -590,6 +590,22 @@ class Engine:
     def current_zip(self) -> np.ndarray:
         return self.current_zip_device().cpu().numpy()
 
+    def wavelet_flags(self, policy, var: int = 0):
+        """Remesh criterion on the evolved solution, on the device: the
+        wavelet coefficient (wavelet.py:70-105) of every leaf's own ppo^dim
+        lattice of variable ``var`` and refine_flags' decision
+        (wavelet.py:108-124).  Returns (coeff, codes) host arrays, codes
+        1 refine / 0 keep / -1 coarsen.  The paper remeshes only when all
+        blocks are synchronised (end of a coarse round)."""
+        import torch
+
+        from .wavelet import coefficients_from_values
+
+        lat = self.mesh.leaf_lattice_device(self.current_zip_device(), var)
+        lv = torch.from_numpy(self.mesh.tree.arrays()[1].astype(np.int32)).to(lat.device)
+        c, f = coefficients_from_values(lat, self.mesh.ppo, self.mesh.dim, lv, policy)
+        return c.cpu().numpy(), f.cpu().numpy()
+
     # -- correction algebra ----------------------------------------------------------------
     def _transfer(self, delta_units: int, from_units: int, to_units: int):
         if delta_units == 0 and from_units == to_units:

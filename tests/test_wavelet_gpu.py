@@ -183,3 +183,37 @@ def test_predicate_drives_construction():
             cx = -10.0 + (key.anchor[0] + key.side / 2) / 16 * 20
             cy = -10.0 + (key.anchor[1] + key.side / 2) / 16 * 20
             assert cx * cx + cy * cy < 30.0
+
+
+# --- the criterion on the evolved solution (remesh at synchronised times)
+
+def test_leaf_lattice_matches_unzip_and_engine_flags():
+    """Mesh.leaf_lattice_device equals the leaf's sub-box of Mesh.unzip (the
+    reference-pinned gather), and Engine.wavelet_flags equals the oracle's
+    coefficients and refine_flags rule on those samples."""
+    from helpers import config_mesh
+    from paper_2011_10570_b200.configs import CONFIGS
+    from paper_2011_10570_b200.stepper import Engine
+
+    mesh = config_mesh("cfg1")
+    c = CONFIGS["cfg1"]
+    eng = Engine(mesh, tableau="rk4", cfl=0.25, mode="lts", nonlinear=False, device=torch.device("cuda", 0))
+    eng.initialize(c.chi0())
+    eng.lts_coarse_step()
+    z = eng.current_zip()
+    lat = mesh.leaf_lattice_device(torch.from_numpy(z).cuda(), 0).cpu().numpy()
+    blocks = mesh.unzip(z)
+    ppo = mesh.ppo
+    an, lv = mesh.tree.arrays()
+    for i in range(0, len(an), 5):
+        b = mesh.blocks[mesh.leaf_block[i]]
+        org = mesh._block_org(b)
+        step = mesh.leaf_spacing(b.leaf_level)
+        off = [(int(an[i, d]) * mesh.scale - int(org[d])) // step for d in range(mesh.dim)]
+        sub = blocks[mesh.leaf_block[i]][0][tuple(slice(o, o + ppo) for o in off)]
+        assert np.array_equal(lat[i].reshape(sub.shape), sub + 0.0), i
+    pol = W.RefinePolicy(tolerance=1e-3, min_level=3, max_level=6)
+    coeff, codes = eng.wavelet_flags(pol)
+    want = O.wavelet_coeffs(lat, ppo, mesh.dim)
+    assert np.array_equal(coeff, want)
+    assert np.array_equal(codes, O.wavelet_flag_codes(want, lv, 1e-3, 0.1, 3, 6))
