@@ -117,9 +117,9 @@ def lib() -> C.CDLL:
     global _LIB
     if _LIB is not None:
         return _LIB
-    path = _build.LIB
+    path = os.environ.get("AMR_LIB_PATH") or _build.LIB  # override: kernel-variant experiments (tools/)
     nvcc = os.path.exists(_build.NVCC)
-    if nvcc and os.path.isdir(_build.CSRC):
+    if nvcc and os.path.isdir(_build.CSRC) and not os.environ.get("AMR_LIB_PATH"):
         _build.build()
     if not os.path.exists(path):
         raise NativeError(

@@ -1,8 +1,8 @@
 """Build the native library in-tree: paper_2011_10570_b200/_lib/libamr_b200.so.
 
-One nvcc invocation compiles the sm_100a kernels (amr_kernels.cu) and the host
-C++ mesh builder (amr_mesh.cpp) into a C-ABI shared library that Python loads
-with ctypes.  Flags that matter for parity:
+One nvcc per source (in parallel) compiles the sm_100a kernels (amr_kernels.cu,
+amr_wavelet.cu) and the host C++ mesh builder (amr_mesh.cpp); one link makes
+the C-ABI shared library that Python loads with ctypes.  Flags that matter for parity:
   -fmad=false            no FMA contraction in device code (numpy rounds every op)
   -ffp-contract=off      same for the host C++ (interpolation weights)
 """
@@ -38,17 +38,28 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     extra = os.environ.get("AMR_NVCC_FLAGS", "").split()
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-shared", *extra,
-           "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off,-O2",
-           "-I", INCLUDE, "-o", LIB + ".tmp",
-           *[os.path.join(CSRC, s) for s in SOURCES], "-lgomp"]
+    common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", *extra,
+              "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off,-O2", "-I", INCLUDE]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
+        common.insert(1, "-Xptxas=-v")
+    # one nvcc per source, in parallel, then one link
+    procs = []
+    for src in SOURCES:
+        obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + ".o")
+        cmd = [*common, "-c", os.path.join(CSRC, src), "-o", obj]
+        procs.append((cmd, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    objs = []
+    for cmd, obj, pr in procs:
+        out, err = pr.communicate()
+        if pr.returncode != 0:
+            raise RuntimeError(f"nvcc failed ({' '.join(cmd)}):\n{out}\n{err}")
+        if verbose:
+            sys.stderr.write(err)
+        objs.append(obj)
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lgomp"]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({' '.join(cmd)}):\n{proc.stdout}\n{proc.stderr}")
-    if verbose:
-        sys.stderr.write(proc.stderr)
+        raise RuntimeError(f"nvcc link failed ({' '.join(cmd)}):\n{proc.stdout}\n{proc.stderr}")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

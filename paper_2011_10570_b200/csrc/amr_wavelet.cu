@@ -21,6 +21,7 @@
 // against the reference in tests/test_wavelet.py.  The file is compiled with
 // -fmad=false; fma() appears only there.
 #include <cuda_runtime.h>
+#include <math_constants.h>
 
 #include <cmath>
 #include <cstdint>
@@ -33,12 +34,13 @@ extern "C" void amr_set_error_internal(const char* msg);
 namespace {
 
 constexpr int WV_MAX_NPD = 15;
+#ifndef WV_MINB  // resident 256-thread CTAs per SM the 3D npd<=7 kernels are register-capped for
+#define WV_MINB 2
+#endif
+#ifndef WV_INTMAX  // 1: residual max on the |d| bit patterns; 0: fmax + a NaN flag
+#define WV_INTMAX 1
+#endif
 
-__device__ __forceinline__ double nan_max(double m, double d) {
-  // np.max propagates NaN; otherwise the plain maximum
-  if (m != m) return m;
-  return (d != d || d > m) ? d : m;
-}
 
 // W per npd, back to back in constant memory (npd = 3, 5, ..., 15): the 3D
 // path reads it with warp-uniform indices.  Filled before each launch.
@@ -61,7 +63,7 @@ struct WvShape {
   static constexpr int N2 = DIM == 2 ? 0 : NPD * NPD * NC;        // after axis 1 (3D)
   static constexpr int PER_WARP = 2 * NV + N1 + N2;
   static constexpr int NW = NPD * NC;
-  static constexpr int MINB = DIM == 3 && NPD <= 7 ? 3 : 1;
+  static constexpr int MINB = DIM == 3 && NPD <= 7 ? WV_MINB : 1;
 };
 
 // One warp per octant; the next octant's samples are copied (cp.async) into
@@ -107,8 +109,12 @@ __global__ void __launch_bounds__(256, WvShape<DIM, NPD>::MINB) wavelet_kernel(i
     asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     const double* v = vb + cur * nv;
     __syncwarp();
+    // max of |v - rec| over odd nodes: every term is >= +0, so the running
+    // max starts at 0 and needs no "first term" state; NaN (np.max
+    // propagates it) is tracked apart so the max itself is a plain fmax
     double m = 0.0;
-    bool any = false;
+    bool bad = false;
+    unsigned long long mb = 0ull;
     if (DIM == 2) {
       // r1[i][b] = sum_a W[i][a] * v[2a][2b]   (axis 0)
 #pragma unroll
@@ -133,8 +139,8 @@ __global__ void __launch_bounds__(256, WvShape<DIM, NPD>::MINB) wavelet_kernel(i
 #pragma unroll
           for (int b = 0; b < nc; ++b) acc = fma(W[j * nc + b], r1[i * nc + b], acc);
           const double d = fabs(v[t] - acc);
-          m = any ? nan_max(m, d) : d;
-          any = true;
+          m = fmax(m, d);
+          bad |= d != d;
         }
       }
     } else {
@@ -143,76 +149,77 @@ __global__ void __launch_bounds__(256, WvShape<DIM, NPD>::MINB) wavelet_kernel(i
       // with compile-time output index, so W[i][a] is a warp-uniform
       // constant-bank operand (cW) and no index is divided at run time.
       const double* Wc = cW + WvOff<NPD>::value;
+      // Lines past the end are clamped onto the last line (a duplicate
+      // result, harmless for the stores and for the max), so no lane diverges.
       // axis 0: r1[i][b][c] = sum_a W[i][a] * v[2a][2b][2c]; lines (b, c)
 #pragma unroll
       for (int l0 = 0; l0 < nc * nc; l0 += 32) {
-        const int l = l0 + lane;
-        if (l < nc * nc) {
-          const int b = l / nc, c = l - b * nc;
-          double x[nc];
+        const int l = min(l0 + lane, nc * nc - 1);
+        const int b = l / nc, c = l - b * nc;
+        double x[nc];
 #pragma unroll
-          for (int q = 0; q < nc; ++q) x[q] = v[((2 * q) * npd + 2 * b) * npd + 2 * c];
+        for (int q = 0; q < nc; ++q) x[q] = v[((2 * q) * npd + 2 * b) * npd + 2 * c];
 #pragma unroll
-          for (int i = 0; i < npd; ++i) {
-            double acc = 0.0;
+        for (int i = 0; i < npd; ++i) {
+          double acc = 0.0;
 #pragma unroll
-            for (int q = 0; q < nc; ++q) acc = fma(Wc[i * nc + q], x[q], acc);
-            r1[i * nc * nc + l] = acc;
-          }
+          for (int q = 0; q < nc; ++q) acc = fma(Wc[i * nc + q], x[q], acc);
+          r1[i * nc * nc + l] = acc;
         }
       }
       __syncwarp();
       // axis 1: r2[i][j][c] = sum_b W[j][b] * r1[i][b][c]; lines (i, c)
-#pragma unroll
+#pragma unroll 1
       for (int l0 = 0; l0 < npd * nc; l0 += 32) {
-        const int l = l0 + lane;
-        if (l < npd * nc) {
-          const int i = l / nc, c = l - i * nc;
-          double x[nc];
+        const int l = min(l0 + lane, npd * nc - 1);
+        const int i = l / nc, c = l - i * nc;
+        double x[nc];
 #pragma unroll
-          for (int q = 0; q < nc; ++q) x[q] = r1[(i * nc + q) * nc + c];
+        for (int q = 0; q < nc; ++q) x[q] = r1[(i * nc + q) * nc + c];
 #pragma unroll
-          for (int j = 0; j < npd; ++j) {
-            double acc = 0.0;
+        for (int j = 0; j < npd; ++j) {
+          double acc = 0.0;
 #pragma unroll
-            for (int q = 0; q < nc; ++q) acc = fma(Wc[j * nc + q], x[q], acc);
-            r2[(i * npd + j) * nc + c] = acc;
-          }
+          for (int q = 0; q < nc; ++q) acc = fma(Wc[j * nc + q], x[q], acc);
+          r2[(i * npd + j) * nc + c] = acc;
         }
       }
       __syncwarp();
       // axis 2: rec[i][j][k] = sum_c W[k][c] * r2[i][j][c]; lines (i, j);
-      // residual at nodes with any odd index
-#pragma unroll
+      // residual at nodes with any odd index.  |d| >= +0, so its bits order
+      // like unsigned integers, and a NaN (sign cleared) sorts above +inf:
+      // an integer max is np.max's result, NaN propagation included.
+#pragma unroll 1
       for (int l0 = 0; l0 < npd * npd; l0 += 32) {
-        const int l = l0 + lane;
-        if (l < npd * npd) {
-          const int i = l / npd, j = l - i * npd;
-          const bool even_ij = !((i | j) & 1);
-          double x[nc];
+        const int l = min(l0 + lane, npd * npd - 1);
+        const int i = l / npd, j = l - i * npd;
+        const bool even_ij = !((i | j) & 1);
+        double x[nc];
 #pragma unroll
-          for (int q = 0; q < nc; ++q) x[q] = r2[l * nc + q];
+        for (int q = 0; q < nc; ++q) x[q] = r2[l * nc + q];
 #pragma unroll
-          for (int k = 0; k < npd; ++k) {
-            if (even_ij && !(k & 1)) continue;
-            double acc = 0.0;
+        for (int k = 0; k < npd; ++k) {
+          double acc = 0.0;
 #pragma unroll
-            for (int q = 0; q < nc; ++q) acc = fma(Wc[k * nc + q], x[q], acc);
-            const double d = fabs(v[l * npd + k] - acc);
-            m = any ? nan_max(m, d) : d;
-            any = true;
-          }
+          for (int q = 0; q < nc; ++q) acc = fma(Wc[k * nc + q], x[q], acc);
+#if WV_INTMAX
+          unsigned long long bits = (unsigned long long)__double_as_longlong(v[l * npd + k] - acc) & 0x7fffffffffffffffull;
+          if (!(k & 1)) bits = even_ij ? 0ull : bits;  // k is a compile-time constant
+          mb = max(mb, bits);
+#else
+          double d = fabs(v[l * npd + k] - acc);
+          if (!(k & 1)) d = even_ij ? 0.0 : d;
+          m = fmax(m, d);
+          bad |= d != d;
+#endif
         }
       }
     }
-    // warp max; lanes without an odd node contribute nothing
+    // warp max (lanes without an odd node hold 0)
+    if (DIM == 2 || !WV_INTMAX) mb = bad ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(m);
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const double o = __shfl_xor_sync(0xffffffffu, m, off);
-      const int oa = __shfl_xor_sync(0xffffffffu, (int)any, off);
-      if (oa) m = any ? nan_max(m, o) : o;
-      any = any || oa;
-    }
+    for (int off = 16; off > 0; off >>= 1) mb = max(mb, (unsigned long long)__shfl_xor_sync(0xffffffffu, mb, off));
+    m = __longlong_as_double((long long)mb);
     if (lane == 0) {
       if (coeff) coeff[oct] = m;
       if (flags) {
