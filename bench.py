@@ -373,6 +373,8 @@ def run_ours(args):
         "gpu_launches": int(lts["launches_per_step"] * args.steps),
         "clocks": clk.summary(),
     }
+    if rank == 0:
+        out["remesh_criterion"] = _remesh_criterion(eng)
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(args, rounds=1)
     if rank == 0:
@@ -408,6 +410,35 @@ def _oracle_units(m, e):
         el = cad >= (e.l_max - ((i & -i).bit_length() - 1 if i else e.l_max))
         tot += e.p * int(np.sum(counts[el]))
     return tot, R
+
+
+def _remesh_criterion(eng, reps=10):
+    """Wavelet remesh criterion on the evolved solution,
+    outside the timed region: the leaf-lattice gather + amr_wavelet_coeff
+    (nodes_per_dim = ppo) over every leaf, CUDA events on the current stream.
+    The full-size kernel roofline is tools/bench_wavelet.py's."""
+    import torch
+
+    from paper_2011_10570_b200.wavelet import RefinePolicy, coefficients_from_values
+
+    m = eng.mesh
+    pol = RefinePolicy(tolerance=1e-3, min_level=0, max_level=m.L)
+    lv = torch.from_numpy(m.tree.arrays()[1].astype(np.int32)).to(eng.device)
+    z = eng.current_zip_device()
+    lat = m.leaf_lattice_device(z, 0)
+    s, e, k = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    torch.cuda.synchronize()
+    s.record()
+    for _ in range(reps):
+        lat = m.leaf_lattice_device(z, 0)
+    k.record()
+    for _ in range(reps):
+        _, codes = coefficients_from_values(lat, m.ppo, m.dim, lv, pol)
+    e.record()
+    torch.cuda.synchronize()
+    hist = torch.bincount((codes.to(torch.int64) + 1), minlength=3).tolist()
+    return {"leaves": int(lat.shape[0]), "nodes_per_dim": m.ppo, "ms_leaf_lattice": s.elapsed_time(k) / reps,
+            "ms_wavelet_kernel": k.elapsed_time(e) / reps, "flags_coarsen_keep_refine": hist}
 
 
 def cpu_baseline(args, rounds=1):
