@@ -590,6 +590,26 @@ class Engine:
     def current_zip(self) -> np.ndarray:
         return self.current_zip_device().cpu().numpy()
 
+    def current_zip_to(self, out, copy_stream=None):
+        """Asynchronous current_zip: copy the live (2, n_nodes) field into the
+        pinned host tensor ``out`` on ``copy_stream`` (ordered after the work
+        already queued on the current stream) and return the CUDA event that
+        marks its completion.  The engine's buffers are free for the next
+        load_zip/step at once: the copy reads a snapshot, so the device->host
+        transfer of one step overlaps the host->device load of the next."""
+        import torch
+
+        cur = torch.cuda.current_stream(self.device)
+        snap = self.current_zip_device()
+        cs = copy_stream if copy_stream is not None else cur
+        cs.wait_stream(cur)
+        with torch.cuda.stream(cs):
+            out.copy_(snap, non_blocking=True)
+        snap.record_stream(cs)
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        return ev
+
     def wavelet_flags(self, policy, var: int = 0):
         """Remesh criterion on the evolved solution, on the device: the
         wavelet coefficient (wavelet.py:70-105) of every leaf's own ppo^dim

@@ -140,3 +140,22 @@ def test_unencodable_mesh_falls_back_to_table_kernel(cuda, monkeypatch):
     eng = _run_case(mesh, CONFIGS["cfg1"].chi0(), gd, "", "lts_rk4", results)
     assert eng._kernel == 0
     _assert_results(results)
+
+
+def test_async_current_zip_matches(cuda):
+    """Engine.current_zip_to (the pipelined e2e read-back) returns the same
+    bits as current_zip, and later load_zip/steps do not disturb a copy in
+    flight."""
+    import torch
+
+    c = CONFIGS["cfg1"]
+    eng = Engine(config_mesh("cfg1"), tableau="rk4", cfl=0.25, mode="lts", nonlinear=False, device=cuda)
+    eng.initialize(c.chi0())
+    eng.lts_coarse_step()
+    want = eng.current_zip()
+    out = torch.empty((2, eng.mesh.n_nodes), dtype=torch.float64).pin_memory()
+    ev = eng.current_zip_to(out, torch.cuda.Stream(cuda))
+    eng.load_zip(np.zeros_like(want))  # overwrite the live buffers right away
+    eng.lts_coarse_step()
+    ev.synchronize()
+    assert np.array_equal(out.numpy(), want)
