@@ -181,10 +181,39 @@ class _Launcher:
             flags.data_ptr() if flags is not None else None, stream), "amr_wavelet_coeff")
 
 
+def _device_samples(torch, f, anchors_d, levels_d, max_depth, domain_lo, domain_hi, npd):
+    """_sample_axes + _sample_values on the device: the same fp64 operations
+    one kernel each (no contraction), so the coordinates equal numpy's bit for
+    bit; ``f`` gets CUDA tensors (torch ops) and its values never leave HBM."""
+    n, dim = anchors_d.shape
+    top = float(1 << max_depth)
+    side = torch.bitwise_left_shift(torch.ones_like(levels_d, dtype=torch.int64), max_depth - levels_d.to(torch.int64))
+    ar = torch.arange(npd, dtype=torch.float64, device=anchors_d.device)
+    shape = (n,) + (npd,) * dim
+    grids = []
+    for d in range(dim):
+        a = anchors_d[:, d]
+        ext = domain_hi[d] - domain_lo[d]
+        # true divisions by tensors: torch turns "tensor / python scalar" into
+        # a multiplication by the reciprocal, which is not numpy's rounding
+        lo = (a.to(torch.float64) / torch.full_like(ar[:1], top)) * ext + domain_lo[d]
+        hi = ((a + side).to(torch.float64) / torch.full_like(ar[:1], top)) * ext + domain_lo[d]
+        step = (hi - lo) / torch.full_like(ar[:1], float(npd - 1))  # np.linspace: arange*step + start, last = stop
+        ax = ar[None, :] * step[:, None]
+        ax = ax + lo[:, None]
+        ax[:, -1] = hi
+        view = ax.reshape((n,) + tuple(npd if e == d else 1 for e in range(dim)))
+        grids.append(view.expand(shape).contiguous())
+    vals = f(*grids)
+    vals = torch.as_tensor(vals, dtype=torch.float64, device=anchors_d.device)
+    return vals.expand(shape).reshape(n, -1).contiguous()
+
+
 def _run(f: Callable, anchors: np.ndarray, levels: np.ndarray, max_depth: int, npd: int, domain_lo, domain_hi,
-         mode: int, policy, device=None):
+         mode: int, policy, device=None, device_eval: bool = False):
     """Stream f's samples to the device chunk by chunk; return (coeff, flags)
-    as host arrays (flags None without a policy)."""
+    as host arrays (flags None without a policy).  device_eval: sample on the
+    device, ``f`` called with CUDA tensors."""
     _check_npd(npd)
     n, dim = anchors.shape
     L = _Launcher(dim, npd, device)
@@ -195,6 +224,17 @@ def _run(f: Callable, anchors: np.ndarray, levels: np.ndarray, max_depth: int, n
     if policy is not None:
         flags = torch.empty(n, dtype=torch.int8, device=L.dev)
         lvl = torch.from_numpy(np.ascontiguousarray(levels, dtype=np.int32)).to(L.dev)
+    if device_eval:
+        stream = torch.cuda.current_stream(L.dev).cuda_stream
+        an_d = torch.from_numpy(np.ascontiguousarray(anchors, dtype=np.int64)).to(L.dev)
+        lv_d = torch.from_numpy(np.ascontiguousarray(levels, dtype=np.int32)).to(L.dev)
+        chunk = max(1, (_CHUNK_VALUES * 4) // nv)
+        for s in range(0, n, chunk):
+            e = min(n, s + chunk)
+            vals = _device_samples(torch, f, an_d[s:e], lv_d[s:e], max_depth, domain_lo, domain_hi, npd)
+            L.launch(vals, lvl[s:e] if lvl is not None else None, mode, policy, coeff[s:e],
+                     flags[s:e] if flags is not None else None, stream)
+        return coeff.cpu().numpy(), (flags.cpu().numpy() if flags is not None else None)
     chunk = max(1, _CHUNK_VALUES // nv)
     stream = torch.cuda.current_stream(L.dev)
     spans = [(s, min(n, s + chunk)) for s in range(0, n, chunk)]
@@ -234,7 +274,7 @@ def _run(f: Callable, anchors: np.ndarray, levels: np.ndarray, max_depth: int, n
 
 
 def wavelet_coefficients(f: Callable, anchors: np.ndarray, levels, max_depth: int, nodes_per_dim: int = 7,
-                         domain_lo=None, domain_hi=None) -> np.ndarray:
+                         domain_lo=None, domain_hi=None, *, device_eval: bool = False) -> np.ndarray:
     """wavelet_coefficient of many octants at once (anchors (n, dim) in
     finest-cell units, levels scalar or (n,)): fp64 array (n,)."""
     _check_npd(nodes_per_dim)
@@ -244,7 +284,7 @@ def wavelet_coefficients(f: Callable, anchors: np.ndarray, levels, max_depth: in
     anchors = anchors.reshape(len(anchors), -1)
     levels = np.broadcast_to(np.asarray(levels, dtype=np.int32), (len(anchors),))
     lo, hi = _domain(anchors.shape[1], max_depth, domain_lo, domain_hi)
-    return _run(f, anchors, levels, max_depth, nodes_per_dim, lo, hi, 0, None)[0]
+    return _run(f, anchors, levels, max_depth, nodes_per_dim, lo, hi, 0, None, device_eval=device_eval)[0]
 
 
 def wavelet_coefficient(f: Callable, key: OctKey, nodes_per_dim: int = 7, domain_lo=None,
@@ -257,31 +297,33 @@ def wavelet_coefficient(f: Callable, key: OctKey, nodes_per_dim: int = 7, domain
 
 
 def refine_flags(f: Callable, tree: LinearOctree, policy: RefinePolicy, nodes_per_dim: int = 7,
-                 domain_lo=None, domain_hi=None) -> list[Flag]:
+                 domain_lo=None, domain_hi=None, *, device_eval: bool = False) -> list[Flag]:
     """Per-leaf refine/keep/coarsen decision (wavelet.py:108-124), one launch
-    for the whole tree."""
-    codes = refine_codes(f, tree, policy, nodes_per_dim, domain_lo, domain_hi)
+    for the whole tree.  device_eval=True samples on the GPU and calls ``f``
+    with CUDA tensors (write ``f`` with torch ops)."""
+    codes = refine_codes(f, tree, policy, nodes_per_dim, domain_lo, domain_hi, device_eval=device_eval)
     return [_FLAG_OF_CODE[int(c)] for c in codes]
 
 
 def refine_codes(f: Callable, tree: LinearOctree, policy: RefinePolicy, nodes_per_dim: int = 7,
-                 domain_lo=None, domain_hi=None) -> np.ndarray:
+                 domain_lo=None, domain_hi=None, *, device_eval: bool = False) -> np.ndarray:
     """refine_flags as an int8 array: 1 refine, 0 keep, -1 coarsen."""
     _check_npd(nodes_per_dim)
     if len(tree) == 0:
         return np.zeros(0, dtype=np.int8)
     anchors, levels = tree.arrays()
     lo, hi = _domain(tree.dim, tree.max_depth, domain_lo, domain_hi)
-    return _run(f, anchors.astype(np.int64), levels, tree.max_depth, nodes_per_dim, lo, hi, 0, policy)[1]
+    return _run(f, anchors.astype(np.int64), levels, tree.max_depth, nodes_per_dim, lo, hi, 0, policy,
+                device_eval=device_eval)[1]
 
 
 class _WaveletPredicate:
     """refinement_predicate (wavelet.py:127-144) with the ``batch`` hook that
     octree.construct uses to test a whole level in one launch."""
 
-    def __init__(self, f, policy, nodes_per_dim, domain_lo, domain_hi):
+    def __init__(self, f, policy, nodes_per_dim, domain_lo, domain_hi, device_eval=False):
         _check_npd(nodes_per_dim)
-        self.f, self.policy, self.npd = f, policy, nodes_per_dim
+        self.f, self.policy, self.npd, self.device_eval = f, policy, nodes_per_dim, device_eval
         self.domain_lo, self.domain_hi = domain_lo, domain_hi
 
     def __call__(self, key: OctKey) -> bool:
@@ -298,14 +340,15 @@ class _WaveletPredicate:
         anchors = np.asarray(anchors, dtype=np.int64).reshape(n, -1)
         lo, hi = _domain(anchors.shape[1], max_depth, self.domain_lo, self.domain_hi)
         levels = np.full(n, level, dtype=np.int32)
-        return _run(self.f, anchors, levels, max_depth, self.npd, lo, hi, 1, p)[1].astype(bool)
+        return _run(self.f, anchors, levels, max_depth, self.npd, lo, hi, 1, p,
+                    device_eval=self.device_eval)[1].astype(bool)
 
 
 def refinement_predicate(f: Callable, policy: RefinePolicy, nodes_per_dim: int = 7, domain_lo=None,
-                         domain_hi=None) -> Callable[[OctKey], bool]:
+                         domain_hi=None, *, device_eval: bool = False) -> Callable[[OctKey], bool]:
     """Predicate for top-down construction driven by the coefficient
     (wavelet.py:127-144)."""
-    return _WaveletPredicate(f, policy, nodes_per_dim, domain_lo, domain_hi)
+    return _WaveletPredicate(f, policy, nodes_per_dim, domain_lo, domain_hi, device_eval)
 
 
 # ---------------------------------------------------------------------------

@@ -217,3 +217,41 @@ def test_leaf_lattice_matches_unzip_and_engine_flags():
     want = O.wavelet_coeffs(lat, ppo, mesh.dim)
     assert np.array_equal(coeff, want)
     assert np.array_equal(codes, O.wavelet_flag_codes(want, lv, 1e-3, 0.1, 3, 6))
+
+
+# --- device-side sampling (device_eval=True: f gets CUDA tensors)
+
+@pytest.mark.parametrize("dim,npd,L", [(2, 7, 7), (3, 5, 6), (3, 9, 5)])
+def test_device_sample_coordinates_bit_exact(dim, npd, L):
+    from paper_2011_10570_b200.octree import random_tree
+    rng = np.random.default_rng(dim * 10 + npd)
+    n = 300
+    lv = rng.integers(0, L + 1, n).astype(np.int32)
+    an = np.stack([(rng.integers(0, 1 << L, n) >> (L - lv)) << (L - lv) for _ in range(dim)], axis=1).astype(np.int64)
+    lo, hi = (-1.0, -0.5, -2.0)[:dim], (1.0, 3.0, 0.25)[:dim]
+    axes = W._sample_axes(an, lv, L, lo, hi, npd)
+    for d in range(dim):
+        host = W._sample_values(lambda *g: g[d], axes, npd)
+        dev = W._device_samples(torch, lambda *g: g[d], torch.from_numpy(an).cuda(), torch.from_numpy(lv).cuda(),
+                                L, lo, hi, npd)
+        assert np.array_equal(dev.cpu().numpy(), host)
+
+
+def test_device_eval_matches_host_path():
+    """Fields of products and sums only (no transcendental) round the same in
+    numpy and torch, so the device-sampled path must give the host path's bits."""
+    f = lambda x, y, z: x * x * y - 0.5 * z * x + y * z * z * z + 0.25  # noqa: E731
+    tree = uniform_tree(3, 4, 4)
+    pol = W.RefinePolicy(tolerance=1e-4, min_level=1, max_level=4)
+    host = W.refine_codes(f, tree, pol, 7, LO, HI)
+    dev = W.refine_codes(f, tree, pol, 7, LO, HI, device_eval=True)
+    assert np.array_equal(host, dev)
+    an, lv = tree.arrays()
+    assert np.array_equal(W.wavelet_coefficients(f, an, lv, 4, 7, LO, HI),
+                          W.wavelet_coefficients(f, an, lv, 4, 7, LO, HI, device_eval=True))
+    g = lambda x, y: x * y * y - 3.0 * x + y  # noqa: E731
+    p2 = W.RefinePolicy(tolerance=1e-6, min_level=0, max_level=5)
+    t_host = construct(W.refinement_predicate(g, p2, 5, LO[:2], HI[:2]), 2, 5, SfcOrdering("morton", 2, 5))
+    t_dev = construct(W.refinement_predicate(g, p2, 5, LO[:2], HI[:2], device_eval=True), 2, 5,
+                      SfcOrdering("morton", 2, 5))
+    assert [k for k in t_host.leaves] == [k for k in t_dev.leaves]

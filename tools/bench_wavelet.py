@@ -63,6 +63,14 @@ def main(steps=20, warmup=3, level=6, npd=7):
     for _ in range(reps):
         codes = W.refine_codes(f, tree, pol, npd, lo, hi)
     e2e_s = (time.perf_counter() - t0) / reps
+    # the same call with on-device sampling: f written with torch ops
+    ft = lambda x, y, z: torch.exp(-((x - 0.3) ** 2 + y ** 2 + (z + 0.1) ** 2) / 0.02)  # noqa: E731
+    W.refine_codes(ft, tree, pol, npd, lo, hi, device_eval=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        W.refine_codes(ft, tree, pol, npd, lo, hi, device_eval=True)
+    dev_s = (time.perf_counter() - t0) / reps
     out = {
         "metric": "wavelet coefficients + flags (octants/s)", "value": n / (ms * 1e-3), "unit": "octants/s",
         "ms_per_launch": ms, "octants": n, "nodes_per_dim": npd, "dim": dim,
@@ -70,6 +78,8 @@ def main(steps=20, warmup=3, level=6, npd=7):
                      "bytes_per_octant": bytes_per},
         "e2e": {"value": n / e2e_s, "unit": "octants/s", "s_per_call": e2e_s,
                 "h2d_bytes": int(vals.nbytes + 4 * n), "d2h_bytes": int(9 * n)},
+        "e2e_device_sampling": {"value": n / dev_s, "unit": "octants/s", "s_per_call": dev_s,
+                                "note": "refine_codes(device_eval=True): coordinates and f (torch ops) on the GPU"},
         "flags_hist": {str(k): int(v) for k, v in zip(*np.unique(codes, return_counts=True))},
     }
     if "--no-cpu" not in sys.argv:
