@@ -279,15 +279,24 @@ extern "C" int amr_wavelet_coeff(int dim, int npd, int64_t n, const double* valu
   int warps = (int)((budget / sizeof(double) - npd * nc) / per_warp);
   warps = warps < 1 ? 1 : (warps > 8 ? 8 : warps);
   const size_t smem = sizeof(double) * (npd * nc + (size_t)warps * per_warp);
-  int dev = 0, sms = 148;
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int per_sm = 1;
+  // per (device, dim, npd): SM count and resident CTAs, set up once
+  static int cache_sms[16][2][WV_MAX_NPD + 1] = {};
+  static int cache_per_sm[16][2][WV_MAX_NPD + 1] = {};
+  const int slot = dev & 15;
+  int& sms = cache_sms[slot][dim - 2][npd];
+  int& per_sm = cache_per_sm[slot][dim - 2][npd];
   cudaError_t e = cudaMemcpyToSymbolAsync(cW, W, sizeof(double) * npd * nc, sizeof(double) * woff,
                                           cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, warps * 32, smem);
+  if (e == cudaSuccess && per_sm == 0) {
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int b = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, warps * 32, smem);
+    if (e == cudaSuccess) per_sm = b < 1 ? 1 : b;
+  }
   if (e != cudaSuccess) {
     amr_set_error_internal((std::string("amr_wavelet_coeff: ") + cudaGetErrorString(e)).c_str());
     return AMR_ECUDA;

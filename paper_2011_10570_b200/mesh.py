@@ -349,11 +349,12 @@ class Mesh:
             take = np.repeat(iptr[rows] - ptr[:-1], lens) + np.arange(int(ptr[-1]), dtype=np.int64)
             col = td["interp_gid"][take].astype(np.int64)
             w = td["interp_w"][take]
-            lt = (torch.from_numpy(np.where(hang, 0, tab)).to(dev), torch.from_numpy(hang).to(dev),
+            hidx = np.flatnonzero(hang.reshape(-1)).astype(np.int64)  # integer index: no mask->nonzero sync
+            lt = (torch.from_numpy(np.where(hang, 0, tab)).to(dev), torch.from_numpy(hidx).to(dev),
                   torch.from_numpy(ptr).to(dev), torch.from_numpy(col).to(dev), torch.from_numpy(w).to(dev),
                   len(rows))
             self.__dict__["_lattice_dev"] = lt
-        tab_d, hang_d, ptr_d, col_d, w_d, nh = lt
+        tab_d, hidx_d, ptr_d, col_d, w_d, nh = lt
         row = zd[var].contiguous()
         out = row[tab_d]
         if nh:
@@ -362,7 +363,7 @@ class Mesh:
             _native.check(self._nm.lib.amr_gather_rows(nh, ptr_d.data_ptr(), col_d.data_ptr(), w_d.data_ptr(), 1,
                                                        row.data_ptr(), row.numel(), hv.data_ptr(), nh, stream),
                           "amr_gather_rows")
-            out[hang_d] = hv
+            out.view(-1).index_copy_(0, hidx_d, hv)
         return out
 
     # -- engine view ---------------------------------------------------------------

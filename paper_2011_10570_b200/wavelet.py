@@ -151,6 +151,23 @@ def _sample_values(f: Callable, axes: list[np.ndarray], npd: int) -> np.ndarray:
     return np.broadcast_to(vals, shape).reshape(n, -1)
 
 
+_LAUNCHERS: dict = {}
+
+
+def _launcher(dim: int, npd: int, device=None) -> "_Launcher":
+    """One _Launcher (and one upload of W) per (dim, npd, device)."""
+    import torch
+
+    dev = torch.device("cuda") if device is None else torch.device(device)
+    if dev.type == "cuda" and dev.index is None and torch.cuda.is_available():
+        dev = torch.device("cuda", torch.cuda.current_device())
+    key = (dim, npd, str(dev))
+    L = _LAUNCHERS.get(key)
+    if L is None:
+        L = _LAUNCHERS[key] = _Launcher(dim, npd, dev)
+    return L
+
+
 class _Launcher:
     """Device constants and the launch of amr_wavelet_coeff."""
 
@@ -216,18 +233,18 @@ def _run(f: Callable, anchors: np.ndarray, levels: np.ndarray, max_depth: int, n
     device, ``f`` called with CUDA tensors."""
     _check_npd(npd)
     n, dim = anchors.shape
-    L = _Launcher(dim, npd, device)
+    L = _launcher(dim, npd, device)
     torch = L.torch
     nv = npd ** dim
     coeff = torch.empty(n, dtype=torch.float64, device=L.dev)
     flags = lvl = None
     if policy is not None:
         flags = torch.empty(n, dtype=torch.int8, device=L.dev)
-        lvl = torch.from_numpy(np.ascontiguousarray(levels, dtype=np.int32)).to(L.dev)
+        lvl = torch.from_numpy(np.array(levels, dtype=np.int32)).to(L.dev)
     if device_eval:
         stream = torch.cuda.current_stream(L.dev).cuda_stream
         an_d = torch.from_numpy(np.ascontiguousarray(anchors, dtype=np.int64)).to(L.dev)
-        lv_d = torch.from_numpy(np.ascontiguousarray(levels, dtype=np.int32)).to(L.dev)
+        lv_d = torch.from_numpy(np.array(levels, dtype=np.int32)).to(L.dev)
         chunk = max(1, (_CHUNK_VALUES * 4) // nv)
         for s in range(0, n, chunk):
             e = min(n, s + chunk)
@@ -370,7 +387,7 @@ def coefficients_from_values(values, nodes_per_dim: int, dim: int, levels=None, 
     _check_npd(nodes_per_dim)
     if mode not in ("flags", "predicate"):
         raise ValueError("mode must be 'flags' or 'predicate'")
-    L = _Launcher(dim, nodes_per_dim, values.device)
+    L = _launcher(dim, nodes_per_dim, values.device)
     nv = nodes_per_dim ** dim
     if values.dtype != torch.float64 or not values.is_cuda or values.numel() % nv:
         raise ValueError("values must be a CUDA float64 tensor of n * nodes_per_dim**dim samples")
