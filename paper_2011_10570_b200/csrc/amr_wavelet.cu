@@ -37,6 +37,13 @@ constexpr int WV_MAX_NPD = 15;
 #ifndef WV_MINB  // resident 256-thread CTAs per SM the 3D npd<=7 kernels are register-capped for
 #define WV_MINB 2
 #endif
+#ifndef WV_U2  // unroll of the 3D axis-1 / axis-2 line loops
+#define WV_U2 2
+#endif
+#ifndef WV_U3
+#define WV_U3 2
+#endif
+constexpr int kUnroll2 = WV_U2, kUnroll3 = WV_U3;
 #ifndef WV_INTMAX  // 1: residual max on the |d| bit patterns; 0: fmax + a NaN flag
 #define WV_INTMAX 1
 #endif
@@ -169,7 +176,7 @@ __global__ void __launch_bounds__(256, WvShape<DIM, NPD>::MINB) wavelet_kernel(i
       }
       __syncwarp();
       // axis 1: r2[i][j][c] = sum_b W[j][b] * r1[i][b][c]; lines (i, c)
-#pragma unroll 1
+#pragma unroll(kUnroll2)
       for (int l0 = 0; l0 < npd * nc; l0 += 32) {
         const int l = min(l0 + lane, npd * nc - 1);
         const int i = l / nc, c = l - i * nc;
@@ -189,7 +196,7 @@ __global__ void __launch_bounds__(256, WvShape<DIM, NPD>::MINB) wavelet_kernel(i
       // residual at nodes with any odd index.  |d| >= +0, so its bits order
       // like unsigned integers, and a NaN (sign cleared) sorts above +inf:
       // an integer max is np.max's result, NaN propagation included.
-#pragma unroll 1
+#pragma unroll(kUnroll3)
       for (int l0 = 0; l0 < npd * npd; l0 += 32) {
         const int l = min(l0 + lane, npd * npd - 1);
         const int i = l / npd, j = l - i * npd;
