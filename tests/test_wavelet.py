@@ -83,3 +83,21 @@ def test_predicate_level_clamps_without_device():
 def test_abi_exports_wavelet():
     assert "amr_wavelet_coeff" in _native.SIGNATURES
     assert hasattr(_native.lib(), "amr_wavelet_coeff")
+
+
+@pytest.mark.parametrize("dim,npd,L", [(2, 7, 7), (3, 5, 6), (3, 9, 5)])
+def test_device_sampling_formula_on_cpu_tensors(dim, npd, L):
+    """The device_eval sampling (torch ops, tensor/tensor divisions) gives the
+    numpy coordinates bit for bit; checked here with CPU tensors."""
+    import torch
+
+    rng = np.random.default_rng(dim * 7 + npd)
+    n = 200
+    lv = rng.integers(0, L + 1, n).astype(np.int32)
+    an = np.stack([(rng.integers(0, 1 << L, n) >> (L - lv)) << (L - lv) for _ in range(dim)], axis=1).astype(np.int64)
+    lo, hi = (-1.0, -0.5, -2.0)[:dim], (1.0, 3.0, 0.25)[:dim]
+    axes = W._sample_axes(an, lv, L, lo, hi, npd)
+    for d in range(dim):
+        host = W._sample_values(lambda *g: g[d], axes, npd)
+        dev = W._device_samples(torch, lambda *g: g[d], torch.from_numpy(an), torch.from_numpy(lv), L, lo, hi, npd)
+        assert np.array_equal(dev.numpy(), host)
