@@ -44,6 +44,9 @@ constexpr int WV_MAX_NPD = 15;
 #define WV_U3 2
 #endif
 constexpr int kUnroll2 = WV_U2, kUnroll3 = WV_U3;
+#ifndef WV_SPLIT1  // 3D axis-0 pass over both half-warps when nc^2 <= 16
+#define WV_SPLIT1 0
+#endif
 #ifndef WV_INTMAX  // 1: residual max on the |d| bit patterns; 0: fmax + a NaN flag
 #define WV_INTMAX 1
 #endif
@@ -159,19 +162,40 @@ __global__ void __launch_bounds__(256, WvShape<DIM, NPD>::MINB) wavelet_kernel(i
       // Lines past the end are clamped onto the last line (a duplicate
       // result, harmless for the stores and for the max), so no lane diverges.
       // axis 0: r1[i][b][c] = sum_a W[i][a] * v[2a][2b][2c]; lines (b, c)
-#pragma unroll
-      for (int l0 = 0; l0 < nc * nc; l0 += 32) {
-        const int l = min(l0 + lane, nc * nc - 1);
+      if (WV_SPLIT1 && 2 * nc * nc <= 32) {
+        // nc^2 <= 16 lines: both half-warps take every line, each emits half
+        // of the outputs (i = h*H + t); the weights differ between the halves,
+        // so they come from shared memory (W) instead of the constant bank
+        constexpr int H = (npd + 1) / 2;
+        const int h = lane >= 16 ? 1 : 0;
+        const int l = min(lane & 15, nc * nc - 1);
         const int b = l / nc, c = l - b * nc;
         double x[nc];
 #pragma unroll
         for (int q = 0; q < nc; ++q) x[q] = v[((2 * q) * npd + 2 * b) * npd + 2 * c];
 #pragma unroll
-        for (int i = 0; i < npd; ++i) {
+        for (int t = 0; t < H; ++t) {
+          const int i = min(h * H + t, npd - 1);  // the upper half repeats its last output
           double acc = 0.0;
 #pragma unroll
-          for (int q = 0; q < nc; ++q) acc = fma(Wc[i * nc + q], x[q], acc);
+          for (int q = 0; q < nc; ++q) acc = fma(W[i * nc + q], x[q], acc);
           r1[i * nc * nc + l] = acc;
+        }
+      } else {
+#pragma unroll
+        for (int l0 = 0; l0 < nc * nc; l0 += 32) {
+          const int l = min(l0 + lane, nc * nc - 1);
+          const int b = l / nc, c = l - b * nc;
+          double x[nc];
+#pragma unroll
+          for (int q = 0; q < nc; ++q) x[q] = v[((2 * q) * npd + 2 * b) * npd + 2 * c];
+#pragma unroll
+          for (int i = 0; i < npd; ++i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < nc; ++q) acc = fma(Wc[i * nc + q], x[q], acc);
+            r1[i * nc * nc + l] = acc;
+          }
         }
       }
       __syncwarp();
