@@ -600,14 +600,27 @@ class Engine:
         import torch
 
         cur = torch.cuda.current_stream(self.device)
-        snap = self.current_zip_device()
+        # two preallocated device snapshots, alternating: no allocation (and
+        # no allocator-deferred frees) per call; a snapshot is rewritten only
+        # after the copy that read it two calls ago has finished
+        st = self.__dict__.get("_snap")
+        if st is None:
+            st = self.__dict__["_snap"] = [[torch.empty_like(self._U[0]), None] for _ in range(2)]
+            self.__dict__["_snap_i"] = 0
+        j = self.__dict__["_snap_i"]
+        self.__dict__["_snap_i"] = j ^ 1
+        buf, prev = st[j]
+        if prev is not None:
+            cur.wait_event(prev)
+        live = self.current_zip_device()
+        buf.copy_(live)
         cs = copy_stream if copy_stream is not None else cur
         cs.wait_stream(cur)
         with torch.cuda.stream(cs):
-            out.copy_(snap, non_blocking=True)
-        snap.record_stream(cs)
+            out.copy_(buf, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(cs)
+        st[j][1] = ev
         return ev
 
     def wavelet_flags(self, policy, var: int = 0):
