@@ -44,6 +44,9 @@ constexpr int WV_MAX_NPD = 15;
 #define WV_U3 2
 #endif
 constexpr int kUnroll2 = WV_U2, kUnroll3 = WV_U3;
+#ifndef WV_NACC  // partial maxima per lane in the 3D residual pass
+#define WV_NACC 1
+#endif
 #ifndef WV_SPLIT1  // 3D axis-0 pass over both half-warps when nc^2 <= 16
 #define WV_SPLIT1 0
 #endif
@@ -125,6 +128,9 @@ __global__ void __launch_bounds__(256, WvShape<DIM, NPD>::MINB) wavelet_kernel(i
     double m = 0.0;
     bool bad = false;
     unsigned long long mb = 0ull;
+    unsigned long long mbk[WV_NACC];  // independent partial maxima: short dependency chains
+#pragma unroll
+    for (int q = 0; q < WV_NACC; ++q) mbk[q] = 0ull;
     if (DIM == 2) {
       // r1[i][b] = sum_a W[i][a] * v[2a][2b]   (axis 0)
 #pragma unroll
@@ -236,7 +242,7 @@ __global__ void __launch_bounds__(256, WvShape<DIM, NPD>::MINB) wavelet_kernel(i
 #if WV_INTMAX
           unsigned long long bits = (unsigned long long)__double_as_longlong(v[l * npd + k] - acc) & 0x7fffffffffffffffull;
           if (!(k & 1)) bits = even_ij ? 0ull : bits;  // k is a compile-time constant
-          mb = max(mb, bits);
+          mbk[k % WV_NACC] = max(mbk[k % WV_NACC], bits);
 #else
           double d = fabs(v[l * npd + k] - acc);
           if (!(k & 1)) d = even_ij ? 0.0 : d;
@@ -247,6 +253,8 @@ __global__ void __launch_bounds__(256, WvShape<DIM, NPD>::MINB) wavelet_kernel(i
       }
     }
     // warp max (lanes without an odd node hold 0)
+#pragma unroll
+    for (int q = 0; q < WV_NACC; ++q) mb = max(mb, mbk[q]);
     if (DIM == 2 || !WV_INTMAX) mb = bad ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(m);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) mb = max(mb, (unsigned long long)__shfl_xor_sync(0xffffffffu, mb, off));
