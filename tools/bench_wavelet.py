@@ -82,6 +82,26 @@ def main(steps=20, warmup=3, level=6, npd=7):
                                 "note": "refine_codes(device_eval=True): coordinates and f (torch ops) on the GPU"},
         "flags_hist": {str(k): int(v) for k, v in zip(*np.unique(codes, return_counts=True))},
     }
+    # predicate-driven construction (wavelet.py:127-144 through octree.construct):
+    # one launch per level, samples on the device
+    from paper_2011_10570_b200.octree import SfcOrdering, construct
+
+    pp = W.RefinePolicy(tolerance=1e-6, min_level=2, max_level=8)
+    pred = W.refinement_predicate(ft, pp, npd, lo, hi, device_eval=True)
+    construct(pred, 3, 8, SfcOrdering("morton", 3, 8))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    built = construct(pred, 3, 8, SfcOrdering("morton", 3, 8))
+    tc = time.perf_counter() - t0
+    an_b, lv_b = built.arrays()
+    # octants visited by the level-synchronous construction: leaves + internal
+    # nodes of the complete octree ((leaves - 1) / 7)
+    hist = np.bincount(lv_b, minlength=9)
+    tested = int(len(lv_b) + (len(lv_b) - 1) // 7)
+    out["construct"] = {"leaves": int(len(lv_b)), "octants_tested": tested, "s": tc,
+                        "octants_per_s": tested / tc, "levels": [int(x) for x in hist],
+                        "note": "construct(refinement_predicate(gauss3 in torch, tol 1e-6, levels 2..8, npd 7, "
+                                "device_eval=True)), Morton order, one launch per level"}
     if "--no-cpu" not in sys.argv:
         from oracle import oracle as O
 
