@@ -148,7 +148,9 @@ def _sample_values(f: Callable, axes: list[np.ndarray], npd: int) -> np.ndarray:
         view = ax.reshape((n,) + tuple(npd if e == d else 1 for e in range(dim)))
         grids.append(np.ascontiguousarray(np.broadcast_to(view, shape)))
     vals = np.asarray(f(*grids), dtype=float)
-    return np.broadcast_to(vals, shape).reshape(n, -1)
+    if vals.shape != shape:  # f returned a broadcastable array (e.g. a constant)
+        vals = np.array(np.broadcast_to(vals, shape))
+    return vals.reshape(n, -1)
 
 
 _LAUNCHERS: dict = {}
