@@ -71,6 +71,20 @@ def main():
         out[f"{name}_tree_anchors"] = np.array([k.anchor for k in built.leaves], dtype=np.int32)
         out[f"{name}_tree_levels"] = np.array([k.level for k in built.leaves], dtype=np.int32)
         print(name, len(keys), "leaves;", np.bincount(codes + 1), "codes;", len(built.leaves), "built leaves")
+    # a larger case without the samples (the GPU test re-samples through the
+    # product's host path, pinned above): every leaf of a 3D random tree
+    f = FIELDS["trig3"]
+    L = 6
+    tree = random_tree(np.random.default_rng(11), 3, L, n_clusters=6, base_level=4,
+                       ordering=SfcOrdering("morton", 3, L))
+    keys = tree.leaves
+    pol = RefinePolicy(tolerance=6e-6, min_level=2, max_level=6)
+    out["scale_meta"] = np.array([3, L, 7, 2, 6], dtype=np.int64)
+    out["scale_anchors"] = np.array([k.anchor for k in keys], dtype=np.int32)
+    out["scale_levels"] = np.array([k.level for k in keys], dtype=np.int32)
+    out["scale_coeff"] = np.array([wavelet_coefficient(f, k, 7, lo, hi) for k in keys])
+    out["scale_codes"] = np.array([CODE[x] for x in refine_flags(f, tree, pol, 7, lo, hi)], dtype=np.int8)
+    print("scale", len(keys), "leaves;", np.bincount(out["scale_codes"] + 1), "codes")
     np.savez_compressed(os.path.join(HERE, "wavelet.npz"), **out)
 
 

@@ -10,7 +10,7 @@ from paper_2011_10570_b200 import wavelet as W
 from wavelet_fields import FIELDS
 
 G = golden("wavelet")
-CASES = sorted(k[: -len("_meta")] for k in G.files if k.endswith("_meta"))
+CASES = sorted(k[: -len("_meta")] for k in G.files if k.endswith("_meta") and not k.startswith("scale"))
 LO, HI = (-1.0, -1.0, -1.0), (1.0, 1.0, 1.0)
 
 
@@ -101,3 +101,15 @@ def test_device_sampling_formula_on_cpu_tensors(dim, npd, L):
         host = W._sample_values(lambda *g: g[d], axes, npd)
         dev = W._device_samples(torch, lambda *g: g[d], torch.from_numpy(an), torch.from_numpy(lv), L, lo, hi, npd)
         assert np.array_equal(dev.numpy(), host)
+
+
+def test_oracle_at_scale_pinned():
+    """4 278 leaves of a 3D random tree: the oracle's per-octant samples and
+    coefficients against the reference's (golden 'scale' case)."""
+    dim, L, npd, mnl, mxl = (int(x) for x in G["scale_meta"])
+    an, lv = G["scale_anchors"], G["scale_levels"]
+    vals = np.stack([O.wavelet_samples(FIELDS["trig3"], tuple(int(x) for x in a), int(l), L, npd, LO, HI).reshape(-1)
+                     for a, l in zip(an, lv)])
+    c = O.wavelet_coeffs(vals, npd, dim)
+    assert np.array_equal(c, G["scale_coeff"])
+    assert np.array_equal(O.wavelet_flag_codes(c, lv, 6e-6, 0.1, mnl, mxl), G["scale_codes"])

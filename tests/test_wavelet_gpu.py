@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 G = golden("wavelet")
-CASES = sorted(k[: -len("_meta")] for k in G.files if k.endswith("_meta"))
+CASES = sorted(k[: -len("_meta")] for k in G.files if k.endswith("_meta") and not k.startswith("scale"))
 LO, HI = (-1.0, -1.0, -1.0), (1.0, 1.0, 1.0)
 CODE = {W.Flag.REFINE: 1, W.Flag.KEEP: 0, W.Flag.COARSEN: -1}
 
@@ -255,3 +255,19 @@ def test_device_eval_matches_host_path():
     t_dev = construct(W.refinement_predicate(g, p2, 5, LO[:2], HI[:2], device_eval=True), 2, 5,
                       SfcOrdering("morton", 2, 5))
     assert [k for k in t_host.leaves] == [k for k in t_dev.leaves]
+
+
+def test_reference_coefficients_at_scale():
+    """4 278 leaves of a 3D random tree: the reference's own coefficients and
+    flags (no samples stored; the product's host sampling re-creates them)."""
+    dim, L, npd, mnl, mxl = (int(x) for x in G["scale_meta"])
+    an, lv = G["scale_anchors"], G["scale_levels"]
+    c = W.wavelet_coefficients(FIELDS["trig3"], an, lv, L, npd, LO, HI)
+    assert np.array_equal(c, G["scale_coeff"])
+    from paper_2011_10570_b200.octree import LinearOctree
+
+    tree = LinearOctree([OctKey(tuple(int(x) for x in a), int(l), L) for a, l in zip(an, lv)], dim, L,
+                        SfcOrdering("morton", dim, L))
+    codes = W.refine_codes(FIELDS["trig3"], tree, W.RefinePolicy(tolerance=6e-6, min_level=mnl, max_level=mxl),
+                           npd, LO, HI)
+    assert np.array_equal(codes, G["scale_codes"])
