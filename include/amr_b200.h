@@ -197,6 +197,8 @@ typedef struct {
   long long* dbg;              /* NULL, or per-warp phase cycle counters of kernel 1 (tools/phase_probe.py) */
   int dbg_skip;                /* ablation bits (results invalid; kernels 0/2 only with -DAMR_ABLATE,
                                   tools/ablate.py): 1 gathers, 2 rows, 4 RHS */
+  const uint16_t* tail;        /* kernel 3: per-tile hanging rows + taps (tileprog.py), 16-byte aligned */
+  int threads;                 /* kernel 3: threads per CTA (128 or 256) */
 } AmrStageParams;
 
 /* One RK stage over a prefix of the tile list: fused unzip (spatial + LTS time

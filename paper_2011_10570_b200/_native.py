@@ -67,6 +67,7 @@ class AmrStageParams(C.Structure):
         ("blob", _vp), ("blob_off", _vp), ("blob_head", _vp), ("heads", _vp), ("max_blob", C.c_int),
         ("kernel", C.c_int),
         ("cell_ent", _vp), ("ld", C.c_int64), ("dbg", _vp), ("dbg_skip", C.c_int),
+        ("tail", _vp), ("threads", C.c_int),
     ]
 
 

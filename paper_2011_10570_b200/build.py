@@ -18,7 +18,7 @@ LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libamr_b200.so")
 INCLUDE = os.path.abspath(os.path.join(HERE, "..", "include"))
 SOURCES = ["amr_kernels.cu", "amr_wavelet.cu", "amr_mesh.cpp"]
-HEADERS = ["amr_stage_pipe.cuh", "amr_stage_blob.cuh"]
+HEADERS = ["amr_stage_pipe.cuh", "amr_stage_blob.cuh", "amr_stage_cross.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -676,6 +676,7 @@ __global__ void __launch_bounds__(Tile<DIM, PPO>::THREADS, AMR_MIN_BLOCKS)
 
 #include "amr_stage_pipe.cuh"
 #include "amr_stage_blob.cuh"
+#include "amr_stage_cross.cuh"
 
 // --------------------------------------------------------------------------
 // Mesh.unzip over CSR rows
@@ -839,8 +840,40 @@ int launch_blob_one(const AmrStageParams* p, cudaStream_t st) {
   return AMR_OK;
 }
 
+template <int DIM, int PPO, bool LTS, int NT, int NTH>
+int launch_cross_one(const AmrStageParams* p, cudaStream_t st) {
+  using CK = CrossK<DIM, PPO>;
+  const size_t dyn = CK::smem_bytes(p->max_slots, p->max_blob);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static size_t configured[64] = {0};
+  if (dev < 64 && dyn > configured[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(stage_cross<DIM, PPO, LTS, NT, NTH>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(stage_cross)");
+    configured[dev] = dyn;
+  }
+  stage_cross<DIM, PPO, LTS, NT, NTH><<<(unsigned)p->n_tiles, NTH, dyn, st>>>(*p);
+  return AMR_OK;
+}
+
+template <int DIM, int PPO, bool LTS, int NTH>
+int launch_cross_nt(const AmrStageParams* p, cudaStream_t st) {
+  switch (p->n_vt) {
+    case 0: return launch_cross_one<DIM, PPO, LTS, 0, NTH>(p, st);
+    case 1: return launch_cross_one<DIM, PPO, LTS, 1, NTH>(p, st);
+    case 2: return launch_cross_one<DIM, PPO, LTS, 2, NTH>(p, st);
+    case 3: return launch_cross_one<DIM, PPO, LTS, 3, NTH>(p, st);
+    default: return AMR_EINVAL;
+  }
+}
+
 template <int DIM, int PPO, bool LTS>
 int launch_stage_nt(const AmrStageParams* p, cudaStream_t st) {
+  if (p->kernel == 3) {
+    if (p->threads == 256) return launch_cross_nt<DIM, PPO, LTS, 256>(p, st);
+    return launch_cross_nt<DIM, PPO, LTS, 128>(p, st);
+  }
   if (p->kernel == 2) {
     switch (p->n_vt) {
       case 0: return launch_blob_one<DIM, PPO, LTS, 0>(p, st);

@@ -260,9 +260,62 @@ class Engine:
         mine = np.nonzero(owners == self.rank)[0] if self._dist is not None else np.arange(n_leaves)
         order = np.lexsort((mine, -leaf_cad[mine]))
         tiles = mine[order].astype(np.int32)
+        lts_kernel = mode == "lts" or any(c != self.l_max for c in cadence)
+        self._kernel = int(os.environ.get("AMR_KERNEL", "3"))
+        self._ibuf = None
+        if self._kernel == 3:
+            self._init_programs(td, tiles, leaf_cad, node_cad, lts_kernel)
+        else:
+            self._init_tables(td, tiles, leaf_cad, node_cad, lts_kernel)
+        n = mesh.n_nodes
+        # the reference's (nvars, n_nodes) zip layout, SoA: chi row then phi row.
+        # Rows are padded to an even stride ld > n (16-byte aligned rows; the
+        # kernel bulk-prefetches 16-byte aligned supersets of a tile's owned range)
+        ld = (n + 2) // 2 * 2
+        self._ld = ld
+        dev = self.device
+        self._U_store = [torch.zeros((2, ld), dtype=torch.float64, device=dev) for _ in range(2)]
+        self._K_store = torch.zeros((self.p, 2, ld), dtype=torch.float64, device=dev)
+        self._U = [u[:, :n] for u in self._U_store]
+        self._K = self._K_store[:, :, :n]
+        # verbatim stage sources, double-buffered by stage parity
+        self._Y_store = torch.zeros((2, 2, ld), dtype=torch.float64, device=dev)
+        self._Y = self._Y_store[:, :, :n]
+        self._node_cad_t = self._d["node_cad"].long()
+        self._vt = [[j for j in range(s_) if self.tab.a[s_][j] != 0.0] for s_ in range(self.p)]
+        self._prm = self._make_params()
+        self._exchange = _EngineExchange(self) if self._dist is not None else None
+
+    def _init_programs(self, td, tiles, leaf_cad, node_cad, lts):
+        """Kernel 3: the owned-cross programs of tileprog.py."""
+        import torch
+
+        from . import tileprog
+
+        prog = tileprog.build_programs(td, tiles, leaf_cad, node_cad, lts)
         tcad = leaf_cad[tiles]
         self._prefix = {c: int(np.sum(tcad >= c)) for c in range(self.l_max + 1)}
-        lts_kernel = mode == "lts" or any(c != self.l_max for c in cadence)
+        n_iface = prog["n_iface"]
+        self._if_prefix = {c: int(np.sum((prog["if_cad"][:n_iface] & 0xFF) >= c)) for c in range(self.l_max + 1)}
+        self._n_iface = n_iface
+        dev = self.device
+        T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        pad = lambda a: a if len(a) else np.zeros(1, a.dtype)  # noqa: E731
+        self._d = dict(tiles=T(tiles.astype(np.int32)), node_cad=T(node_cad), heads=T(prog["heads"]),
+                       tail=T(prog["tail"]), wtab=T(prog["wtab"]), if_gid=T(pad(prog["if_gid"])),
+                       if_cad=T(pad(prog["if_cad"])))
+        self._max_slots = prog["max_slots"]
+        self._max_blob = prog["max_head"]
+        self._ibuf = torch.zeros((2, max(n_iface, 1)), dtype=torch.float64, device=dev)
+        self._threads = int(os.environ.get("AMR_THREADS", "128"))
+
+    def _init_tables(self, td, tiles, leaf_cad, node_cad, lts_kernel):
+        """Kernels 0-2 (round 1): int32 tile tables and blobs."""
+        import torch
+
+        mesh = self.mesh
+        tcad = leaf_cad[tiles]
+        self._prefix = {c: int(np.sum(tcad >= c)) for c in range(self.l_max + 1)}
         table, prog = self._tile_programs(td, tiles, node_cad, leaf_cad, lts=lts_kernel)
         n_iface = prog.pop("n_iface")
         blobs = self._build_blobs(table, prog, n_iface, td, mesh.dim, mesh.ppo)
@@ -281,23 +334,7 @@ class Engine:
                            cell_ent=T(blobs["cell_ent"]))
             self._max_blob = blobs["max_blob"]
         self._ibuf = torch.zeros((2, max(n_iface, 1)), dtype=torch.float64, device=dev)
-        n = mesh.n_nodes
-        # the reference's (nvars, n_nodes) zip layout, SoA: chi row then phi row.
-        # Rows are padded to an even stride ld > n (16-byte aligned rows; the
-        # kernel bulk-copies 16-byte aligned supersets of a tile's owned range)
-        ld = (n + 2) // 2 * 2
-        self._ld = ld
-        self._U_store = [torch.zeros((2, ld), dtype=torch.float64, device=dev) for _ in range(2)]
-        self._K_store = torch.zeros((self.p, 2, ld), dtype=torch.float64, device=dev)
-        self._U = [u[:, :n] for u in self._U_store]
-        self._K = self._K_store[:, :, :n]
-        # verbatim stage sources, double-buffered by stage parity
-        self._Y_store = torch.zeros((2, 2, ld), dtype=torch.float64, device=dev)
-        self._Y = self._Y_store[:, :, :n]
-        self._node_cad_t = self._d["node_cad"].long()
-        self._vt = [[j for j in range(s_) if self.tab.a[s_][j] != 0.0] for s_ in range(self.p)]
-        self._prm = self._make_params()
-        self._exchange = _EngineExchange(self) if self._dist is not None else None
+        self._threads = 0
 
     # -- setup -------------------------------------------------------------------------
     def _promoted_cadence(self, levels: list[int]) -> list[int]:
@@ -478,25 +515,16 @@ class Engine:
         P.n_nodes = m.n_nodes
         P.ld = self._ld
         d = self._d
-        P.tile_ids, P.tile_table = d["tiles"].data_ptr(), d["table"].data_ptr()
-        P.leaf_anchor, P.leaf_level = d["anchor"].data_ptr(), d["level"].data_ptr()
-        P.leaf_cadence, P.leaf_start = d["cadence"].data_ptr(), d["starts"].data_ptr()
-        P.node_cadence = d["node_cad"].data_ptr()
-        P.tile_slot_ptr, P.slot_gid = d["tile_slot_ptr"].data_ptr(), d["slot_gid"].data_ptr()
+        P.kernel = self._kernel
+        P.max_slots = self._max_slots
         P.if_gid, P.if_cad, P.ibuf = d["if_gid"].data_ptr(), d["if_cad"].data_ptr(), self._ibuf.data_ptr()
         P.n_iface_total = self._n_iface
-        P.tile_in_ptr, P.in_tap_ptr = d["tile_in_ptr"].data_ptr(), d["in_tap_ptr"].data_ptr()
-        P.tile_tap_ptr = d["tile_tap_ptr"].data_ptr()
-        P.in_cell, P.tile_meta, P.cross_cells = (d["in_cell"].data_ptr(), d["tile_meta"].data_ptr(),
-                                                 d["cross_cells"].data_ptr())
-        P.cross_pos = d["cross_pos"].data_ptr()
-        P.tap, P.wtab, P.n_wtab = d["tap"].data_ptr(), d["wtab"].data_ptr(), int(d["wtab"].numel())
-        P.max_slots = self._max_slots
-        P.kernel = self._kernel
-        if self._kernel:
-            P.blob, P.blob_off = d["blob"].data_ptr(), d["blob_off"].data_ptr()
-            P.blob_head, P.heads = d["blob_head"].data_ptr(), d["heads"].data_ptr()
-            P.cell_ent, P.max_blob = d["cell_ent"].data_ptr(), self._max_blob
+        P.wtab, P.n_wtab = d["wtab"].data_ptr(), int(d["wtab"].numel())
+        if self._kernel == 3:
+            P.heads, P.max_blob, P.tail = d["heads"].data_ptr(), self._max_blob, d["tail"].data_ptr()
+            P.threads = self._threads
+        else:
+            self._table_params(P)
         P.U0, P.U1, P.K = self._U[0].data_ptr(), self._U[1].data_ptr(), self._K.data_ptr()
         P.Y = self._Y.data_ptr()
         for s in range(self.p):
@@ -523,6 +551,28 @@ class Engine:
         P.k_chi, P.k_phi, P.f0_chi, P.f0_phi = self.k_chi, self.k_phi, 0.0, 0.0
         fill_weights(P)
         return P
+
+    def _table_params(self, P) -> None:
+        d = self._d
+        P.tile_ids, P.tile_table = d["tiles"].data_ptr(), d["table"].data_ptr()
+        P.leaf_anchor, P.leaf_level = d["anchor"].data_ptr(), d["level"].data_ptr()
+        P.leaf_cadence, P.leaf_start = d["cadence"].data_ptr(), d["starts"].data_ptr()
+        P.node_cadence = d["node_cad"].data_ptr()
+        P.tile_slot_ptr, P.slot_gid = d["tile_slot_ptr"].data_ptr(), d["slot_gid"].data_ptr()
+        P.if_gid, P.if_cad, P.ibuf = d["if_gid"].data_ptr(), d["if_cad"].data_ptr(), self._ibuf.data_ptr()
+        P.n_iface_total = self._n_iface
+        P.tile_in_ptr, P.in_tap_ptr = d["tile_in_ptr"].data_ptr(), d["in_tap_ptr"].data_ptr()
+        P.tile_tap_ptr = d["tile_tap_ptr"].data_ptr()
+        P.in_cell, P.tile_meta, P.cross_cells = (d["in_cell"].data_ptr(), d["tile_meta"].data_ptr(),
+                                                 d["cross_cells"].data_ptr())
+        P.cross_pos = d["cross_pos"].data_ptr()
+        P.tap, P.wtab, P.n_wtab = d["tap"].data_ptr(), d["wtab"].data_ptr(), int(d["wtab"].numel())
+        P.max_slots = self._max_slots
+        P.kernel = self._kernel
+        if self._kernel:
+            P.blob, P.blob_off = d["blob"].data_ptr(), d["blob_off"].data_ptr()
+            P.blob_head, P.heads = d["blob_head"].data_ptr(), d["heads"].data_ptr()
+            P.cell_ent, P.max_blob = d["cell_ent"].data_ptr(), self._max_blob
 
     # -- plans (API parity; built lazily: they need every block's gather support) --
     @property

@@ -1,273 +1,385 @@
-"""Per-tile program blobs of the blob stage kernels (amr_stage, AMR_KERNEL 1 and 2).
+"""Per-tile stage programs of the stage kernel (``amr_stage``, csrc/amr_stage_cross.cuh).
 
-One blob per leaf tile, in launch order, 16-byte aligned.  The kernel fetches
-its head (header, bases, runs, slot codes) with a single bulk copy
-(``cp.async.bulk``) into a shared-memory ring two tiles ahead; the tail (face
-entry codes, rows, taps) is bulk-prefetched into L2 and read from there.  It re-encodes the tile table and the
-tile's interpolation program (``Engine._tile_programs``) compactly:
+One leaf = one tile.  A tile computes the RHS only at the zip nodes it owns
+(its contiguous gid range ``leaf_slices[leaf]``), so it needs the stage input
+only on the **owned cross**: the owned nodes and the cells within two steps of
+one of them along a single axis (the 4th-order stencil's reach; the biased
+rows at physical faces stay inside the leaf).  Everything else of the
+reference's padded block is never read.  On cfg2 that is
+1 257 of the 1 701 stencil-cross cells of a tile and 70 of its 144 hanging
+rows.
 
-=========  =================================================================
-section    contents
-=========  =================================================================
-header     16 int32: g0, n_own, level | cadence<<8 | faces<<16, n_runs, n_slots,
-           n_rows, n_bases, blob length (uint16 units), anchor[3], the
-           uint16 offsets of the entry/slot/row/tap sections, and the blob's
-           own offset in the blob array (16-byte units)
-bases      int32 per source group: a source leaf's first gid (>= 0), or, for
-           LTS interface pairs, -(first pair of the (reader cadence, source
-           leaf) group) - 1
-runs       uint32 per copy run: smem cell | (length-1) << 12 | code << 16,
-           code = base index << 10 | offset of the first source; base index
-           63 is special: offset 0 = outside the domain (zeros).  Runs cover
-           every non-hanging stencil-cross entry, z-consecutive cells with
-           consecutive sources, longest first
-slots      uint16 per unique interpolation source, same code
-entries    face tiles only: uint16 code per stencil-cross entry (offset r+1
-           of base 63 = the tile's hanging row r), for the phi lookups of the
-           radiative rows
-rows       uint32 per hanging row: smem cell | n_quads << 12 | quad offset << 17
-taps       uint16 per tap: slot << 6 | weight id, rows padded to 4 taps with
-           (zero slot, weight 0) exactly as the int32 program
-=========  =================================================================
+The program of a tile is two byte strings:
 
-A source leaf owns at most ppo^D nodes (< 1024) and a (cadence, leaf) pair
-group at most as many, so every offset fits 10 bits.  Tables are static: the
-encoding is built once per mesh (all numpy, vectorised over tiles).
+* the **head** (fixed stride ``max_head`` bytes, so the kernel bulk-copies it
+  into shared memory with one ``cp.async.bulk`` and no offset lookup):
+
+  ========  ==============================================================
+  header    16 int32: g0, n_own, level | cadence<<8 | faces<<16, n_runs,
+            n_slots, n_rows, n_bases, tail bytes, anchor[3], run counts of the
+            8/4/2/1-lane buckets (two uint16 per word, words 11-12), tail
+            offset (16-byte units, word 14), taps offset inside the tail
+            (uint16 units, word 15)
+  bases     int32 per source group: a source leaf's first gid (>= 0), or,
+            for LTS interface pairs, -(first pair of the (reader cadence,
+            source leaf) group) - 1
+  runs      uint32 per copy run: box cell | (length-1) << 12 | code << 16,
+            code = base index << 10 | offset of the first source node.  A run
+            is z-consecutive box cells fed by consecutive nodes of one source
+            group, at most 8 long.  Runs are bucketed by length (5-8, 3-4, 2,
+            1 -> 8, 4, 2, 1 lanes per run) so a warp copies 32 nodes per
+            instruction with lanes walking along runs (coalesced, balanced)
+  slots     uint16 per unique interpolation source node, same code
+  ========  ==============================================================
+
+* the **tail** (read through L2, bulk-prefetched at tile start): hanging rows
+  (uint32: box cell | n_quads << 12 | quad offset << 17), longest first, and
+  their taps (uint16: slot << 6 | weight id), each row padded to a multiple of
+  4 taps with (zero slot, weight 0), which leaves the ascending-gid running
+  sum of ``_point_weights`` (mesh.py:316-351) unchanged.
+
+Unzip semantics (``Mesh.unzip``, mesh.py:413-420): a copy cell is a zip node,
+a hanging cell is an interpolation row ``0 + sum w_k src(g_k)`` in ascending
+gid order, and a cell outside the domain is never read by the owned stencils.
+At LTS level interfaces a source node whose cadence differs from the reader's
+is an **interface pair** (node, reader cadence): its stage source (transfer
+matrices, virtual substeps; ``Engine._stage_source``, stepper.py:274-314) is
+formed once per stage by ``iface_kernel`` and read like a copy.
+
+All numpy, vectorised over tiles; built once per mesh (Engine construction).
 """
 from __future__ import annotations
 
 import numpy as np
 
-IFACE_BASE = -(1 << 20)  # AMR_IFACE_BASE in amr_kernels.cu
-HDR_WORDS = 16           # int32 words in the header
-SPECIAL = 63             # base index of outside / hanging codes
-MAX_BASES = 63
+HDR_WORDS = 16        # int32 words in the header
+MAX_BASES = 63        # source groups per tile (6-bit base index)
+RUN_MAX = 8           # longest run
+BUCKET_LANES = (8, 4, 2, 1)
 
 
-def _pad8(n):
-    return (np.asarray(n, dtype=np.int64) + 7) // 8 * 8
+class ProgramError(ValueError):
+    """The mesh does not fit the compact per-tile encoding."""
 
 
-class BlobError(ValueError):
-    """The mesh does not fit the compact encoding (the kernel falls back to v17)."""
+def _r16(nbytes):
+    return (np.asarray(nbytes, dtype=np.int64) + 15) // 16 * 16
 
 
-def build_blobs(table: np.ndarray, prog: dict, n_iface: int, starts: np.ndarray, anchor3: np.ndarray,
-                n_interior: int, n_pad: int) -> dict:
-    """Blobs for every tile of ``table`` (launch order).
+def cross_cells(dim: int, ppo: int, pad: int = 2) -> np.ndarray:
+    """Padded-box cell of every stencil-cross entry, in the enumeration of the
+    mesh's tile table (amr_mesh.cpp cross_entry_local): the ppo^dim interior
+    in C order, then per axis the 2*pad layers below and above."""
+    NI, NF = ppo ** dim, ppo ** (dim - 1)
+    E = NI + dim * 2 * pad * NF
+    e = np.arange(E, dtype=np.int64)
+    loc = np.zeros((E, dim), dtype=np.int64)
+    inner = e < NI
+    r = e[inner].copy()
+    for d in range(dim - 1, -1, -1):
+        loc[inner, d] = pad + r % ppo
+        r //= ppo
+    h = ~inner
+    r = e[h] - NI
+    axis = r // (2 * pad * NF)
+    r = r % (2 * pad * NF)
+    layer = r // NF
+    within = r % NF
+    sub = np.zeros((len(r), dim), dtype=np.int64)
+    for d in range(dim - 1, -1, -1):
+        others = axis != d
+        sub[others, d] = pad + within[others] % ppo
+        within = np.where(others, within // ppo, within)
+    sub[np.arange(len(r)), axis] = np.where(layer < pad, layer, ppo + layer)
+    loc[h] = sub
+    NP = ppo + 2 * pad
+    cell = np.zeros(E, dtype=np.int64)
+    for d in range(dim):
+        cell = cell * NP + loc[:, d]
+    return cell
 
-    ``table``/``prog`` are the outputs of ``Engine._tile_programs``; ``starts``
-    the leaf gid offsets (leaf_slices), ``anchor3`` the leaf anchors,
-    ``n_interior`` = ppo^D and ``n_pad`` = ppo + 4 (the box edge)."""
-    cross_cells = prog["cross_cells"]
-    nt, E = table.shape
-    starts = np.asarray(starts, dtype=np.int64)
-    meta = prog["tile_meta"].astype(np.int64)
-    tsp = prog["tile_slot_ptr"].astype(np.int64)
-    tip = prog["tile_in_ptr"].astype(np.int64)
-    itp = prog["in_tap_ptr"].astype(np.int64)
-    ttp = prog["tile_tap_ptr"].astype(np.int64)
-    n_slot_tot = int(tsp[-1])
-    n_in = int(tip[-1])
-    n_tap = int(ttp[-1])
-    slot_gid = prog["slot_gid"][:n_slot_tot].astype(np.int64)
-    if len(prog["wtab"]) > 64:
-        raise BlobError("more than 64 distinct interpolation weights")
 
-    # -- interface pair groups: pairs sorted by (reader cadence desc, gid), so
-    #    the pairs of one (cadence, source leaf) are contiguous
-    if n_iface:
-        if_gid = prog["if_gid"][:n_iface].astype(np.int64)
-        if_cad = prog["if_cad"][:n_iface].astype(np.int64) & 0xFF  # reader cadence
-        if_leaf = np.searchsorted(starts, if_gid, side="right") - 1
-        gkey = (if_cad << 40) | if_leaf
-        new = np.ones(n_iface, dtype=bool)
-        new[1:] = gkey[1:] != gkey[:-1]
-        grp_start = np.maximum.accumulate(np.where(new, np.arange(n_iface), 0))
+def owned_cross(table: np.ndarray, g0: np.ndarray, g1: np.ndarray, faces: np.ndarray, dim: int,
+                ppo: int) -> np.ndarray:
+    """(n_tiles, E) mask of the cross entries the owned stencils read: the
+    centred rows' +-1, +-2 along each axis, and at a physical face the biased
+    rows' 6-point windows (wave.py:57-109; first-derivative rows read a subset)."""
+    cells = cross_cells(dim, ppo)
+    NP, NI = ppo + 4, ppo ** dim
+    cell2e = np.full(NP ** dim, -1, dtype=np.int64)
+    cell2e[cells] = np.arange(len(cells))
+    core = table[:, :NI]
+    own = (core >= g0[:, None]) & (core < g1[:, None])
+    need = np.zeros(table.shape, dtype=bool)
+    need[:, :NI] = own
+    k = np.arange(NI)
+    for d in range(dim):
+        stride = NP ** (dim - 1 - d)
+        pos = (k // ppo ** (dim - 1 - d)) % ppo
+        for o in (-2, -1, 1, 2):
+            tgt = cell2e[cells[:NI] + o * stride]
+            need[:, tgt] |= own
+        lo = ((faces >> (2 * d)) & 1).astype(bool)
+        hi = ((faces >> (2 * d + 1)) & 1).astype(bool)
+        for o in range(-5, 6):
+            inside = (pos + o >= 0) & (pos + o < ppo)
+            at_lo = inside & (pos <= 1)
+            at_hi = inside & (pos >= ppo - 2)
+            for sel, fl in ((at_lo, lo), (at_hi, hi)):
+                if not sel.any() or not fl.any():
+                    continue
+                src = np.nonzero(sel)[0]
+                tgt = cell2e[cells[src] + o * stride]
+                need[np.ix_(fl, tgt)] |= own[np.ix_(fl, src)]
+    return need
+
+
+def build_programs(td: dict, tiles: np.ndarray, leaf_cad: np.ndarray, node_cad: np.ndarray,
+                   lts: bool) -> dict:
+    """Programs of ``tiles`` (launch order) from the mesh's tile tables.
+
+    Returns heads (n_tiles, max_head) uint8, tail (uint16), max_head,
+    max_slots, the interface pairs (if_gid, if_cad = reader cadence | source
+    cadence << 8, sorted finest reader first) and the weight table wtab."""
+    dim, ppo, L = td["dim"], td["ppo"], td["max_depth"]
+    starts = np.asarray(td["starts"], dtype=np.int64)
+    tiles = np.asarray(tiles, dtype=np.int64)
+    nt = len(tiles)
+    table = td["table"][tiles].astype(np.int64)
+    E = table.shape[1]
+    g0, g1 = starts[tiles], starts[tiles + 1]
+    a3 = np.asarray(td["anchor3"], dtype=np.int64)[tiles]
+    faces = np.zeros(nt, dtype=np.int64)
+    side = 1 << (L - td["level"][tiles].astype(np.int64))
+    for d in range(dim):
+        faces |= (a3[:, d] == 0).astype(np.int64) << (2 * d)
+        faces |= ((a3[:, d] + side) == (1 << L)).astype(np.int64) << (2 * d + 1)
+    need = owned_cross(table, g0, g1, faces, dim, ppo)
+    cells = cross_cells(dim, ppo)
+    NP = ppo + 4
+    tcad = leaf_cad[tiles].astype(np.int64)
+
+    # ---- hanging rows (needed only), longest first within a tile
+    ptr, gid, w = td["interp_ptr"], td["interp_gid"], td["interp_w"]
+    t_idx, e_idx = np.nonzero((table <= -2) & need)
+    rows = -table[t_idx, e_idx] - 2
+    cnt = ptr[rows + 1] - ptr[rows]
+    o = np.lexsort((e_idx, -cnt, t_idx))
+    t_idx, e_idx, rows, cnt = t_idx[o], e_idx[o], rows[o], cnt[o]
+    n_in = len(rows)
+    tile_in_ptr = np.zeros(nt + 1, dtype=np.int64)
+    np.cumsum(np.bincount(t_idx, minlength=nt), out=tile_in_ptr[1:])
+    padded = (cnt + 3) // 4 * 4
+    in_tap_ptr = np.zeros(n_in + 1, dtype=np.int64)
+    np.cumsum(padded, out=in_tap_ptr[1:])
+    n_real = int(cnt.sum())
+    within = np.arange(n_real) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+    src_idx = np.repeat(ptr[rows], cnt) + within
+    dst_idx = np.repeat(in_tap_ptr[:-1], cnt) + within
+    tap_gid = gid[src_idx].astype(np.int64)
+    tap_tile = np.repeat(t_idx, cnt)
+    if n_real:
+        key, inv = np.unique((tap_tile << 32) | tap_gid, return_inverse=True)
     else:
+        key, inv = np.zeros(0, np.int64), np.zeros(0, np.int64)
+    slot_tile = key >> 32
+    slot_gid = key & 0xFFFFFFFF
+    tile_slot_ptr = np.zeros(nt + 1, dtype=np.int64)
+    np.cumsum(np.bincount(slot_tile, minlength=nt), out=tile_slot_ptr[1:])
+    n_slots = np.diff(tile_slot_ptr)
+    max_slots = int(n_slots.max()) if nt else 0
+    if max_slots >= 1023:
+        raise ProgramError(f"a tile reads {max_slots} interpolation sources (> 1022)")
+    local_slot = inv - tile_slot_ptr[tap_tile]
+    wtab, widx = np.unique(np.concatenate([w[src_idx], [0.0]]), return_inverse=True)
+    if len(wtab) > 64:
+        raise ProgramError(f"{len(wtab)} distinct interpolation weights (> 64)")
+    zero_w = int(widx[-1])
+    tap = np.zeros(int(in_tap_ptr[-1]), dtype=np.int64)
+    npad = padded - cnt
+    pad_in = np.repeat(np.arange(n_in), npad)
+    pad_pos = np.repeat(in_tap_ptr[:-1] + cnt, npad) + (
+        np.arange(int(npad.sum())) - np.repeat(np.cumsum(npad) - npad, npad))
+    tap[pad_pos] = (n_slots[t_idx[pad_in]] << 6) | zero_w
+    tap[dst_idx] = (local_slot << 6) | widx[:-1]
+
+    # ---- copy entries (needed, non-hanging, inside the domain) and slots;
+    #      LTS interface pairs where the source cadence differs from the reader's
+    ct, ce = np.nonzero((table >= 0) & need)
+    cg = table[ct, ce]
+    s_tile = slot_tile
+    if lts:
+        cm = node_cad[cg].astype(np.int64) != tcad[ct]
+        sm = node_cad[slot_gid].astype(np.int64) != tcad[s_tile] if len(slot_gid) else np.zeros(0, bool)
+        keys = np.concatenate([((31 - tcad[ct[cm]]) << 32) | cg[cm],
+                               ((31 - tcad[s_tile[sm]]) << 32) | slot_gid[sm]])
+    else:
+        cm = np.zeros(len(cg), bool)
+        sm = np.zeros(len(slot_gid), bool)
+        keys = np.zeros(0, np.int64)
+    if len(keys):
+        ukeys, pinv = np.unique(keys, return_inverse=True)
+        if_gid = ukeys & 0xFFFFFFFF
+        if_cad = (31 - (ukeys >> 32)) | (node_cad[if_gid].astype(np.int64) << 8)
+        ne = int(cm.sum())
+        c_pair = np.zeros(len(cg), np.int64)
+        c_pair[cm] = pinv[:ne]
+        s_pair = np.zeros(len(slot_gid), np.int64)
+        s_pair[sm] = pinv[ne:]
+        # pair groups: (reader cadence, source leaf); pairs of one group are contiguous
+        if_leaf = np.searchsorted(starts, if_gid, side="right") - 1
+        gkey = ((ukeys >> 32) << 40) | if_leaf
+        new = np.ones(len(ukeys), dtype=bool)
+        new[1:] = gkey[1:] != gkey[:-1]
+        grp_start = np.maximum.accumulate(np.where(new, np.arange(len(ukeys)), 0))
+    else:
+        if_gid = np.zeros(0, np.int64)
+        if_cad = np.zeros(0, np.int64)
+        c_pair = np.zeros(len(cg), np.int64)
+        s_pair = np.zeros(len(slot_gid), np.int64)
         grp_start = np.zeros(0, np.int64)
 
-    def encode_src(v: np.ndarray, is_pair: np.ndarray):
-        """(base value, offset) of gids (is_pair False) or interface pairs."""
+    def encode(v, is_pair, pair):
         base = np.empty(len(v), dtype=np.int64)
         off = np.empty(len(v), dtype=np.int64)
-        g = v[~is_pair]
-        lf = np.searchsorted(starts, g, side="right") - 1
+        lf = np.searchsorted(starts, v[~is_pair], side="right") - 1
         base[~is_pair] = starts[lf]
-        off[~is_pair] = g - starts[lf]
-        p = v[is_pair]
-        gs = grp_start[p]
+        off[~is_pair] = v[~is_pair] - starts[lf]
+        gs = grp_start[pair[is_pair]]
         base[is_pair] = -gs - 1
-        off[is_pair] = p - gs
+        off[is_pair] = pair[is_pair] - gs
         return base, off
 
-    # entries
-    ent = table.astype(np.int64)
-    t_e = np.repeat(np.arange(nt, dtype=np.int64), E)
-    flat = ent.reshape(-1)
-    is_copy = flat >= 0
-    is_pair = flat <= IFACE_BASE
-    is_src = is_copy | is_pair
-    src_v = np.where(is_pair, IFACE_BASE - flat, flat)[is_src]
-    e_base, e_off = encode_src(src_v, is_pair[is_src])
-    # slots
-    t_s = np.repeat(np.arange(nt, dtype=np.int64), np.diff(tsp))
-    s_pair = slot_gid < 0
-    s_base, s_off = encode_src(np.where(s_pair, -slot_gid - 1, slot_gid), s_pair)
+    e_base, e_off = encode(cg, cm, c_pair)
+    s_base, s_off = encode(slot_gid, sm, s_pair)
+    if (len(e_off) and e_off.max() >= 1024) or (len(s_off) and s_off.max() >= 1024):
+        raise ProgramError("source offset >= 1024")
 
-    # per-tile base tables
-    bkey = np.concatenate([(t_e[is_src] << 33) | (e_base + (1 << 32)),
-                           (t_s << 33) | (s_base + (1 << 32))])
-    ukey, inv = np.unique(bkey, return_inverse=True)
+    # ---- per-tile base tables
+    bkey = np.concatenate([(ct << 33) | (e_base + (1 << 32)), (s_tile << 33) | (s_base + (1 << 32))])
+    ukey, binv = np.unique(bkey, return_inverse=True)
     u_tile = ukey >> 33
     u_base = (ukey & ((1 << 33) - 1)) - (1 << 32)
     bptr = np.zeros(nt + 1, dtype=np.int64)
     np.cumsum(np.bincount(u_tile, minlength=nt), out=bptr[1:])
     nbase = np.diff(bptr)
     if nt and int(nbase.max()) > MAX_BASES:
-        raise BlobError(f"a tile reads {int(nbase.max())} source groups (> {MAX_BASES})")
-    local_b = np.arange(len(ukey)) - bptr[u_tile]
-    b_idx = local_b[inv]
-    ne_src = int(is_src.sum())
-    if (len(e_off) and e_off.max() >= 1024) or (len(s_off) and s_off.max() >= 1024):
-        raise BlobError("source offset >= 1024")
+        raise ProgramError(f"a tile reads {int(nbase.max())} source groups (> {MAX_BASES})")
+    b_idx = (np.arange(len(ukey)) - bptr[u_tile])[binv]
+    e_code = (b_idx[:len(cg)] << 10) | e_off
+    s_code = (b_idx[len(cg):] << 10) | s_off
 
-    code = np.full(nt * E, SPECIAL << 10, dtype=np.int64)  # outside by default
-    code[is_src] = (b_idx[:ne_src] << 10) | e_off
-    hang = (flat <= -2) & ~is_pair
-    row_local = -flat[hang] - 2
-    if len(row_local) and row_local.max() + 1 >= 1024:
-        raise BlobError("more than 1022 hanging rows in one tile")
-    code[hang] = (SPECIAL << 10) | (row_local + 1)
-    s_code = (b_idx[ne_src:] << 10) | s_off
-
-    # rows and taps
-    nrow = np.diff(tip)
-    faces = (meta[:, 2] >> 16) & 0x3F
-    if nt and int(nrow[faces != 0].max(initial=0)) > n_interior:
-        # face tiles keep the phi of their hanging rows in the owned-phi array
-        raise BlobError("face tile with more hanging rows than interior nodes")
-    t_r = np.repeat(np.arange(nt, dtype=np.int64), nrow)
-    cell = prog["in_cell"][:n_in].astype(np.int64)
-    nq = (itp[1:] - itp[:-1]) // 4
-    qoff = (itp[:-1] - ttp[t_r]) // 4 if n_in else np.zeros(0, np.int64)
-    if n_in and (nq.max() > 31 or qoff.max() >= (1 << 15) or cell.max() >= (1 << 12)):
-        raise BlobError("hanging row does not fit the packed row word")
-    row_word = (cell | (nq << 12) | (qoff << 17)).astype(np.uint32)
-    tap32 = prog["tap"][:n_tap].astype(np.int64)
-    t_slot = tap32 >> 16
-    t_w = tap32 & 0xFFFF
-    if n_tap and (t_slot.max() >= 1024 or t_w.max() >= 64):
-        raise BlobError("tap slot >= 1024 or weight id >= 64")
-    tap16 = ((t_slot << 6) | t_w).astype(np.uint16)
-    ntap = np.diff(ttp)
-
-    # copy runs: the non-hanging cross entries of a tile sorted by smem cell
-    # and cut into runs of z-consecutive cells whose sources are consecutive
-    # nodes of one source group (or zeros), at most 16 long; longest first
-    cross_cells = np.asarray(cross_cells, dtype=np.int64)
-    code2 = code.reshape(nt, E)
-    keep = ~hang.reshape(nt, E)
-    rt, re_ = np.nonzero(keep)
-    rc = cross_cells[re_]
-    rcode = code2[rt, re_]
-    o = np.lexsort((rc, rt))
-    rt, rc, rcode = rt[o], rc[o], rcode[o]
-    rb, ro = rcode >> 10, rcode & 1023
+    # ---- copy runs: sort by (tile, cell), cut where cells or sources stop
+    #      being consecutive (or a box row ends), at most RUN_MAX long
+    rc = cells[ce]
+    o = np.lexsort((rc, ct))
+    rt, rc, rcode = ct[o], rc[o], e_code[o]
     brk = np.ones(len(rt), dtype=bool)
-    brk[1:] = ((rt[1:] != rt[:-1]) | (rc[1:] != rc[:-1] + 1) | (rc[1:] % n_pad == 0) | (rb[1:] != rb[:-1])
-               | ((rb[1:] != SPECIAL) & (ro[1:] != ro[:-1] + 1)))
+    brk[1:] = ((rt[1:] != rt[:-1]) | (rc[1:] != rc[:-1] + 1) | (rc[1:] % NP == 0)
+               | ((rcode[1:] >> 10) != (rcode[:-1] >> 10)) | ((rcode[1:] & 1023) != (rcode[:-1] & 1023) + 1))
     rid = np.cumsum(brk) - 1
     first = np.nonzero(brk)[0]
     pos = np.arange(len(rt)) - first[rid]
-    brk |= (pos % 16) == 0
+    brk |= (pos % RUN_MAX) == 0
     first = np.nonzero(brk)[0]
     rlen = np.diff(np.append(first, len(rt)))
     r_tile = rt[first]
-    r_word = (rc[first] | ((rlen - 1) << 12) | (rcode[first] << 16)).astype(np.uint32)
-    o = np.lexsort((-rlen, r_tile))
-    r_tile, r_word = r_tile[o], r_word[o]
+    r_word = rc[first] | ((rlen - 1) << 12) | (rcode[first] << 16)
+    bucket = np.select([rlen > 4, rlen > 2, rlen > 1], [0, 1, 2], 3)
+    o = np.lexsort((rc[first], bucket, r_tile))
+    r_tile, r_word, bucket = r_tile[o], r_word[o], bucket[o]
     nrun = np.bincount(r_tile, minlength=nt)
     rptr = np.zeros(nt + 1, dtype=np.int64)
     np.cumsum(nrun, out=rptr[1:])
+    bcnt = np.zeros((nt, 4), dtype=np.int64)
+    np.add.at(bcnt, (r_tile, bucket), 1)
 
-    # section sizes in uint16 units
-    nslot = np.diff(tsp)
-    sz_hdr = 2 * HDR_WORDS
-    sz_base = _pad8(2 * nbase)
-    sz_run = _pad8(2 * nrun)
-    sz_ent = np.where(faces != 0, int(_pad8(E)), 0)  # entry codes: face tiles only (phi lookups)
-    sz_slot = _pad8(nslot)
-    sz_row = _pad8(2 * nrow)
-    sz_tap = _pad8(ntap)
-    off_base = np.full(nt, sz_hdr, dtype=np.int64)
-    off_run = off_base + sz_base
-    off_slot = off_run + sz_run
-    off_ent = off_slot + sz_slot
-    off_row = off_ent + sz_ent
-    off_tap = off_row + sz_row
-    length = off_tap + sz_tap
-    if nt and int(length.max()) >= (1 << 20):
-        raise BlobError("tile blob too large")
-    tstart = np.zeros(nt + 1, dtype=np.int64)
-    np.cumsum(length, out=tstart[1:])
-    blob = np.zeros(max(int(tstart[-1]), 8), dtype=np.uint16)
-    b32 = blob.view(np.uint32)
+    # ---- heads: header, bases, runs, slots (16-byte aligned sections)
+    off_base = 4 * HDR_WORDS
+    off_run = off_base + _r16(4 * nbase)
+    off_slot = off_run + _r16(4 * nrun)
+    head_len = off_slot + _r16(2 * n_slots)
+    max_head = int(head_len.max()) if nt else 64
+    # ---- tails: rows, taps
+    nrow = np.diff(tile_in_ptr)
+    cell_in = cells[e_idx]
+    nq = (in_tap_ptr[1:] - in_tap_ptr[:-1]) // 4
+    tile_tap0 = in_tap_ptr[tile_in_ptr[:-1]]
+    t_r = t_idx
+    qoff = (in_tap_ptr[:-1] - tile_tap0[t_r]) // 4 if n_in else np.zeros(0, np.int64)
+    if n_in and (nq.max() > 31 or qoff.max() >= (1 << 15) or cell_in.max() >= (1 << 12)):
+        raise ProgramError("hanging row does not fit the packed row word")
+    if nt and nrow.max() >= 1024:
+        raise ProgramError("more than 1023 hanging rows in one tile")
+    row_word = cell_in | (nq << 12) | (qoff << 17)
+    ntap = np.diff(np.append(tile_tap0, int(in_tap_ptr[-1])))
+    rows_b = _r16(4 * nrow)
+    tail_len = rows_b + _r16(2 * ntap)
+    tail_start = np.zeros(nt + 1, dtype=np.int64)
+    np.cumsum(tail_len, out=tail_start[1:])
+    if int(tail_start[-1]) // 16 >= (1 << 31):
+        raise ProgramError("tile tails exceed 32 GB")
 
-    # header
-    a3 = np.asarray(anchor3, dtype=np.int64)[meta[:, 3]]
-    hdr = np.stack([meta[:, 0], meta[:, 1] - meta[:, 0], meta[:, 2], nrun, nslot, nrow, nbase, length,
-                    a3[:, 0], a3[:, 1], a3[:, 2], off_ent, off_slot, off_row, off_tap,
-                    tstart[:nt] // 8], axis=1)
-    idx = (tstart[:nt, None] // 2 + np.arange(HDR_WORDS)[None, :]).reshape(-1)
-    b32[idx] = hdr.reshape(-1).astype(np.int64).astype(np.uint32)
-    # bases (int32)
-    if len(ukey):
-        b32[(tstart[u_tile] + off_base[u_tile]) // 2 + local_b] = u_base.astype(np.int32).view(np.uint32)
-    # entries
-    # runs
-    if len(r_word):
-        lr_ = np.arange(len(r_word)) - rptr[r_tile]
-        b32[(tstart[r_tile] + off_run[r_tile]) // 2 + lr_] = r_word
-    # entry codes of face tiles
-    ft = np.nonzero(faces != 0)[0]
-    if len(ft):
-        blob[(tstart[ft] + off_ent[ft])[:, None] + np.arange(E)[None, :]] = code2[ft].astype(np.uint16)
-    # slots
-    if n_slot_tot:
-        ls = np.arange(n_slot_tot) - tsp[t_s]
-        blob[tstart[t_s] + off_slot[t_s] + ls] = s_code.astype(np.uint16)
-    # rows
-    if n_in:
-        lr = np.arange(n_in) - tip[t_r]
-        b32[(tstart[t_r] + off_row[t_r]) // 2 + lr] = row_word
-    # taps
-    if n_tap:
-        t_t = np.repeat(np.arange(nt, dtype=np.int64), ntap)
-        lt = np.arange(n_tap) - ttp[t_t]
-        blob[tstart[t_t] + off_tap[t_t] + lt] = tap16
-    if int(tstart[-1]) // 8 >= (1 << 31):
-        raise BlobError("tile blobs exceed 32 GB")
-    head = (off_ent * 2).astype(np.int32)  # header, bases, runs, slots: staged in shared memory
-    tail = (length - off_ent) * 2          # face entry codes, rows, taps: read through L2
-    # the heads again at a fixed stride (the per-tile kernel copies without an offset lookup)
-    mh = int(head.max()) if nt else 16
-    hstart = tstart[:nt] * 2
-    heads = np.zeros((max(nt, 1), mh), dtype=np.uint8)
-    bb = blob.view(np.uint8)
+    heads = np.zeros((max(nt, 1), max_head // 4), dtype=np.uint32)
+    lmeta = td["level"][tiles].astype(np.int64) | (tcad << 8) | (faces << 16)
+    hdr = np.stack([g0, g1 - g0, lmeta, nrun, n_slots, nrow, nbase, tail_len,
+                    a3[:, 0], a3[:, 1], a3[:, 2], bcnt[:, 0] | (bcnt[:, 1] << 16), bcnt[:, 2] | (bcnt[:, 3] << 16),
+                    np.zeros(nt, np.int64), tail_start[:nt] // 16, rows_b // 2], axis=1)
     if nt:
-        within = np.arange(mh)[None, :]
-        src = np.minimum(hstart[:, None] + within, len(bb) - 1)
-        heads[:nt] = np.where(within < head[:, None], bb[src], 0)
-    return dict(blob=blob, blob_off=(tstart * 2).astype(np.int64), blob_head=head, heads=heads,
-                max_blob=int(head.max()) if nt else 16, max_tail=int(tail.max()) if nt else 0,  # tail: info
-                max_rows=int(nrow.max()) if nt else 0)
+        heads[:nt, :HDR_WORDS] = hdr.astype(np.int64).astype(np.uint32)
+        heads[u_tile, off_base // 4 + (np.arange(len(ukey)) - bptr[u_tile])] = \
+            u_base.astype(np.int32).view(np.uint32)
+        heads[r_tile, off_run[r_tile] // 4 + (np.arange(len(r_word)) - rptr[r_tile])] = r_word.astype(np.uint32)
+        h16 = heads.view(np.uint16)
+        ls = np.arange(len(s_code)) - tile_slot_ptr[s_tile]
+        h16[s_tile, off_slot[s_tile] // 2 + ls] = s_code.astype(np.uint16)
+    tail = np.zeros(max(int(tail_start[-1]) // 2, 8), dtype=np.uint16)
+    t32 = tail.view(np.uint32)
+    if n_in:
+        lr = np.arange(n_in) - tile_in_ptr[t_r]
+        t32[tail_start[t_r] // 4 + lr] = row_word.astype(np.uint32)
+    if len(tap):
+        t_t = np.repeat(np.arange(nt, dtype=np.int64), ntap)
+        lt = np.arange(len(tap)) - tile_tap0[t_t]
+        tail[(tail_start[t_t] + rows_b[t_t]) // 2 + lt] = tap.astype(np.uint16)
+    return dict(heads=heads.view(np.uint8), tail=tail, max_head=max_head, max_slots=max_slots,
+                if_gid=if_gid.astype(np.int32), if_cad=if_cad.astype(np.int32), n_iface=len(if_gid),
+                wtab=wtab.astype(np.float64), n_rows=n_in, n_cells=int(need.sum()))
 
 
-def cell_entries(cross_cells: np.ndarray, dim: int, ppo: int) -> np.ndarray:
-    """Inverse of the cross enumeration: stencil-cross entry of each padded-box
-    cell (0xFFFF off the cross)."""
-    NS = (ppo + 4) ** dim
-    out = np.full(NS, 0xFFFF, dtype=np.uint16)
-    out[np.asarray(cross_cells, dtype=np.int64)] = np.arange(len(cross_cells), dtype=np.uint16)
-    return out
+def decode(prog: dict, t: int) -> dict:
+    """A tile's program back as {box cell: source} (source = gid, or
+    ('pair', i) for interface pair i) plus its rows [(cell, [(slot source,
+    weight)...])] — the inverse of build_programs, for tests."""
+    h8 = prog["heads"][t]
+    h = h8.view(np.int32)
+    nrun, nslot, nrow, nbase = int(h[3]), int(h[4]), int(h[5]), int(h[6])
+    bases = h[HDR_WORDS:HDR_WORDS + nbase].astype(np.int64)
+    off_run = 4 * HDR_WORDS + int(_r16(4 * nbase))
+    off_slot = off_run + int(_r16(4 * nrun))
+    runs = h8[off_run:off_run + 4 * nrun].view(np.uint32).astype(np.int64)
+    slots = h8[off_slot:off_slot + 2 * nslot].view(np.uint16).astype(np.int64)
+
+    def src(code, i=0):
+        b, o = bases[code >> 10], (code & 1023) + i
+        return int(b + o) if b >= 0 else ("pair", int(-b - 1 + o))
+
+    cells = {}
+    for wd in runs:
+        for i in range(((wd >> 12) & 7) + 1):
+            cells[int((wd & 0xFFF) + i)] = src(wd >> 16, i)
+    slot_src = [src(c) for c in slots]
+    tail = prog["tail"]
+    t0 = int(h[14]) * 8
+    rw = tail[t0:t0 + 2 * nrow].view(np.uint32).astype(np.int64)
+    taps = tail[t0 + int(h[15]):].astype(np.int64)
+    wt = prog["wtab"]
+    rows = []
+    for wd in rw:
+        nq, q0 = (wd >> 12) & 31, wd >> 17
+        tt = taps[4 * q0: 4 * q0 + 4 * nq]
+        rows.append((int(wd & 0xFFF), [(slot_src[s] if s < nslot else None, float(wt[k]))
+                                       for s, k in zip(tt >> 6, tt & 63)]))
+    b = [int(x) & 0xFFFF for x in h[11:13]] + [int(x) >> 16 for x in h[11:13]]
+    return dict(g0=int(h[0]), n_own=int(h[1]), cells=cells, rows=rows,
+                buckets=(b[0], b[2], b[1], b[3]))

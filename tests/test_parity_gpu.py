@@ -111,35 +111,30 @@ def test_graph_replayed_rounds_equal_eager(cuda):
     assert exact, rel
 
 
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("threads", [128, 256])
 @pytest.mark.parametrize("cfg,tag", [("cfg1", "gts_rk4"), ("cfg1", "lts_rk4"), ("cfg1", "lts_sin"),
                                      ("mini3d", "lts_rk4"), ("mini3d", "lts_cubic"), ("mini3d", "gts_rk4")])
-def test_blob_kernels_match_reference(cuda, monkeypatch, cfg, tag, kernel):
-    """The stage kernels on the compact tile blobs (AMR_KERNEL=1: persistent
-    pipeline; 2: one CTA per tile, bulk-copied head, cp.async copy runs) are
-    held to the same goldens as the table kernel."""
-    monkeypatch.setenv("AMR_KERNEL", str(kernel))
+def test_stage_kernel_block_shapes_match_reference(cuda, monkeypatch, cfg, tag, threads):
+    """The owned-cross stage kernel with 128- and 256-thread CTAs (AMR_THREADS)
+    is held to the same goldens."""
+    monkeypatch.setenv("AMR_THREADS", str(threads))
     gd = golden(cfg)
     mesh = config_mesh(cfg)
     results = []
     eng = _run_case(mesh, CONFIGS[cfg].chi0(), gd, "", tag, results)
-    assert eng._kernel == kernel
-    print(results)
+    assert eng._threads == threads
     _assert_results(results)
 
 
-def test_unencodable_mesh_falls_back_to_table_kernel(cuda, monkeypatch):
-    """A mesh that does not fit the compact blob encoding (here: a forced
-    1-source-group limit) runs on the int32-table kernel, with the same bits."""
+def test_unencodable_mesh_raises(cuda, monkeypatch):
+    """A mesh that does not fit the compact per-tile encoding (here: a forced
+    1-source-group limit) is refused with a ValueError, never run on a fallback."""
     from paper_2011_10570_b200 import tileprog
 
     monkeypatch.setattr(tileprog, "MAX_BASES", 1)
-    gd = golden("cfg1")
     mesh = config_mesh("cfg1")
-    results = []
-    eng = _run_case(mesh, CONFIGS["cfg1"].chi0(), gd, "", "lts_rk4", results)
-    assert eng._kernel == 0
-    _assert_results(results)
+    with pytest.raises(ValueError, match="source groups"):
+        Engine(mesh, tableau="rk4", mode="lts")
 
 
 def test_async_current_zip_matches(cuda):

@@ -1,13 +1,13 @@
-"""CPU checks of the compact tile blobs of the pipelined stage kernel
-(paper_2011_10570_b200/tileprog.py): decoding every blob must give back the
-tile table and interpolation program it was built from, exactly."""
+"""CPU checks of the per-tile stage programs (paper_2011_10570_b200/tileprog.py):
+decoding a tile's program must give back, cell for cell, the mesh's unzip
+table on the owned cross — copies, LTS interface pairs and the hanging rows
+with their taps in ascending-gid order (mesh.py:316-351, 391-393)."""
 import numpy as np
 import pytest
 
 from helpers import config_mesh
 
 from paper_2011_10570_b200 import tileprog as TP
-from paper_2011_10570_b200.stepper import Engine
 
 
 def _programs(name, lts=True):
@@ -17,79 +17,104 @@ def _programs(name, lts=True):
     leaf_cad = td["level"].astype(np.int32)
     node_cad = np.repeat(leaf_cad.astype(np.uint8), np.diff(td["starts"]))
     mine = np.arange(n_leaves)
-    tiles = mine[np.lexsort((mine, -leaf_cad[mine]))].astype(np.int32)
-    table, prog = Engine._tile_programs(td, tiles, node_cad, leaf_cad, lts=lts)
-    n_iface = prog.pop("n_iface")
-    B = TP.build_blobs(table, prog, n_iface, td["starts"], td["anchor3"], mesh.ppo ** mesh.dim, mesh.ppo + 4)
-    return mesh, table, prog, B
+    tiles = mine[np.lexsort((mine, -leaf_cad[mine]))]
+    P = TP.build_programs(td, tiles, leaf_cad, node_cad, lts)
+    return mesh, td, tiles, leaf_cad, node_cad, P
 
 
-def _decode_source(base, off):
-    """table value of a (base, offset) source: a gid, or an interface pair code"""
-    return base + off if base >= 0 else TP.IFACE_BASE - (-base - 1 + off)
+@pytest.mark.parametrize("name,lts", [("cfg1", True), ("cfg1", False), ("mini3d", True)])
+def test_programs_decode_to_the_unzip_table(name, lts):
+    mesh, td, tiles, leaf_cad, node_cad, P = _programs(name, lts)
+    cells = TP.cross_cells(mesh.dim, mesh.ppo)
+    ptr, gid, w = td["interp_ptr"], td["interp_gid"], td["interp_w"]
+    starts = td["starts"]
+    NI = mesh.ppo ** mesh.dim
+    n_checked = 0
+    for t, leaf in enumerate(tiles):
+        dec = TP.decode(P, t)
+        g0, g1 = starts[leaf], starts[leaf + 1]
+        assert (dec["g0"], dec["n_own"]) == (g0, g1 - g0)
+        row = td["table"][leaf]
+        cell_src = dec["cells"]
+        cell_row = {c: taps for c, taps in dec["rows"]}
+        # every owned node is a copy of itself
+        own_cells = {int(cells[e]) for e in range(NI) if g0 <= row[e] < g1}
+        assert len(own_cells) == g1 - g0
+        cad = leaf_cad[leaf]
+        for e, c in enumerate(cells):
+            c = int(c)
+            v = int(row[e])
+            if c in cell_src:
+                s = cell_src[c]
+                if isinstance(s, tuple):  # interface pair: same node, reader cadence = this tile's
+                    assert lts and v >= 0 and node_cad[v] != cad
+                    assert P["if_gid"][s[1]] == v and (P["if_cad"][s[1]] & 0xFF) == cad
+                else:
+                    assert s == v and (not lts or node_cad[v] == cad)
+                n_checked += 1
+            elif c in cell_row:
+                assert v <= -2
+                r = -v - 2
+                want = list(zip(gid[ptr[r]:ptr[r + 1]].tolist(), w[ptr[r]:ptr[r + 1]].tolist()))
+                got = [(s, wt) for s, wt in cell_row[c] if s is not None]
+                pads = [(s, wt) for s, wt in cell_row[c] if s is None]
+                assert all(wt == 0.0 for _, wt in pads) and len(cell_row[c]) % 4 == 0
+                got_g = [(P["if_gid"][s[1]] if isinstance(s, tuple) else s) for s, _ in got]
+                assert got_g == [g for g, _ in want] and [wt for _, wt in got] == [wt for _, wt in want]
+            else:
+                assert v == -1 or c not in own_cells  # never read by an owned stencil
+        for c in own_cells:
+            assert cell_src[c] in range(g0, g1)
+    assert n_checked > 0
 
 
-@pytest.mark.parametrize("name", ["cfg1", "mini3d"])
-def test_blobs_decode_to_the_tile_programs(name):
-    mesh, table, prog, B = _programs(name)
-    blob, off = B["blob"], B["blob_off"]
-    nt, E = table.shape
-    cells = prog["cross_cells"].astype(np.int64)
-    cell_to_e = {int(c): e for e, c in enumerate(cells)}
-    assert B["max_blob"] == int(B["blob_head"].max())
-    heads = B["heads"]
-    assert heads.shape == (nt, B["max_blob"])
-    for t in range(nt):  # the fixed-stride copy of every head
-        hb = int(B["blob_head"][t])
-        assert np.array_equal(heads[t, :hb], blob.view(np.uint8)[off[t]:off[t] + hb])
-        assert not heads[t, hb:].any()
-    for t in range(nt):
-        b = blob[off[t] // 2: off[t + 1] // 2]
-        h = b[:32].view(np.int32)
-        g0, n_own, lmeta, nrun, nslot, nrow, nbase, ln = h[:8]
-        assert ln == len(b) and h[15] * 8 == off[t] // 2
-        assert B["blob_head"][t] == 2 * h[11]
-        bases = b[32:32 + 2 * nbase].view(np.int32)
-        runs = b[32 + ((2 * nbase + 7) // 8) * 8:][:2 * nrun].view(np.uint32)
-        got = np.full(E, -9, dtype=np.int64)
-        for w in runs.astype(np.int64):
-            cell, ln_, code = w & 0xFFF, ((w >> 12) & 15) + 1, w >> 16
-            bi, o = code >> 10, code & 1023
-            for i in range(ln_):
-                e = cell_to_e[cell + i]
-                got[e] = -1 if bi == 63 else _decode_source(int(bases[bi]), o + i)
-        want = table[t].astype(np.int64)
-        hang = (want <= -2) & (want > TP.IFACE_BASE)
-        assert np.array_equal(got[~hang], want[~hang]), t
-        assert np.all(got[hang] == -9)
-        faces = (lmeta >> 16) & 0x3F
-        if faces:  # face tiles keep per-entry codes (hanging row r -> offset r + 1)
-            ent = b[h[11]:h[11] + E].astype(np.int64)
-            r = ent[hang] & 1023
-            assert np.all(ent[hang] >> 10 == 63) and np.array_equal(r - 1, -want[hang] - 2)
-        # slots
-        sl = b[h[12]:h[12] + nslot].astype(np.int64)
-        sg = prog["slot_gid"][prog["tile_slot_ptr"][t]:prog["tile_slot_ptr"][t + 1]].astype(np.int64)
-        for k in range(nslot):
-            v = _decode_source(int(bases[sl[k] >> 10]), int(sl[k] & 1023))
-            assert (v if v >= 0 else -(TP.IFACE_BASE - v) - 1) == sg[k]
-        # rows and taps
-        rows = b[h[13]:h[13] + 2 * nrow].view(np.uint32)
-        taps = b[h[14]:].astype(np.int64)
-        i0 = prog["tile_in_ptr"][t]
-        for r in range(nrow):
-            w = int(rows[r])
-            assert (w & 0xFFF) == prog["in_cell"][i0 + r]
-            k0, k1 = prog["in_tap_ptr"][i0 + r], prog["in_tap_ptr"][i0 + r + 1]
-            nq, q0 = (w >> 12) & 31, w >> 17
-            assert 4 * nq == k1 - k0
-            tt = prog["tap"][k0:k1].astype(np.int64)
-            tw = taps[4 * q0: 4 * q0 + 4 * nq]
-            assert np.array_equal(tw >> 6, tt >> 16) and np.array_equal(tw & 63, tt & 0xFFFF)
+def test_program_buckets_and_needed_set():
+    mesh, td, tiles, leaf_cad, node_cad, P = _programs("mini3d")
+    h = P["heads"].view(np.int32)
+    for t in range(len(tiles)):
+        dec = TP.decode(P, t)
+        b8, b4, b2, b1 = dec["buckets"]
+        assert b8 + b4 + b2 + b1 == h[t, 3]
+    # the owned cross: at most the stencil cross, at least the owned nodes
+    assert P["n_cells"] < len(tiles) * TP.cross_cells(3, 9).size
+    assert P["n_cells"] >= mesh.n_nodes
 
 
-def test_cell_entries_inverts_the_cross():
-    cells = np.array([5, 0, 7], dtype=np.uint16)
-    inv = TP.cell_entries(cells, 2, 1)  # a 5x5 box
-    assert inv[5] == 0 and inv[0] == 1 and inv[7] == 2
-    assert np.all(np.delete(inv, [0, 5, 7]) == 0xFFFF)
+def test_needed_set_covers_every_stencil_read():
+    """Brute force on a 2D tile set: every cell any owned node's stencil (centred
+    or biased) reads is in the owned cross."""
+    mesh = config_mesh("cfg1")
+    td = mesh.tile_data()
+    n = len(mesh.tree.leaves)
+    tiles = np.arange(n)
+    starts = td["starts"]
+    table = td["table"].astype(np.int64)
+    ppo, L = mesh.ppo, mesh.L
+    a3 = td["anchor3"].astype(np.int64)
+    side = 1 << (L - td["level"].astype(np.int64))
+    faces = np.zeros(n, dtype=np.int64)
+    for d in range(2):
+        faces |= (a3[:, d] == 0).astype(np.int64) << (2 * d)
+        faces |= ((a3[:, d] + side) == (1 << L)).astype(np.int64) << (2 * d + 1)
+    need = TP.owned_cross(table, starts[:-1], starts[1:], faces, 2, ppo)
+    cells = TP.cross_cells(2, ppo)
+    NP = ppo + 4
+    for t in tiles:
+        have = set(cells[need[t]].tolist())
+        for e in range(ppo * ppo):
+            if not starts[t] <= table[t, e] < starts[t + 1]:
+                continue
+            pos = [cells[e] // NP - 2, cells[e] % NP - 2]
+            for d in range(2):
+                lo, hi = (faces[t] >> (2 * d)) & 1, (faces[t] >> (2 * d + 1)) & 1
+                p = pos[d]
+                if lo and p <= 1:
+                    offs = range(-p, 6 - p)
+                elif hi and p >= ppo - 2:
+                    offs = range(ppo - 6 - p, ppo - p)
+                else:
+                    offs = range(-2, 3)
+                for o in offs:
+                    q = list(pos)
+                    q[d] += o
+                    assert (q[0] + 2) * NP + q[1] + 2 in have, (t, e, d, o)
