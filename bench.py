@@ -364,7 +364,7 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note,
                      "peak_source": peak_src,
-                     "kernel": f"amr_stage ({ {0: 'stage_kernel', 1: 'stage_pipe', 2: 'stage_blob', 3: 'stage_cross'}[eng._kernel] }, {eng._threads} threads/CTA): fused unzip+time-interp+RHS+zip[+combine]",
+                     "kernel": f"amr_stage (stage_cross, {eng._threads} threads/CTA): fused unzip on the owned cross + RHS + zip [+ RK combine]",
                      "bytes_per_unit": BYTES_PER_UNIT,
                      "launches": len(per), "kernel_ms_per_round": k_ms,
                      "gts_achieved": g_ach, "gts_frac": g_ach / peak},

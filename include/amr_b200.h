@@ -95,12 +95,6 @@ int amr_mesh_blocks(const AmrMesh* m, int32_t* root_anchor, int32_t* root_level,
 int amr_mesh_block_gather(AmrMesh* m, int64_t block, int64_t* rows, int64_t* nnz,
                           int64_t* row_ptr, int64_t* col, double* val);
 
-/* Greedy packing of interpolation nodes (counts[i] taps, reader cadence
- * cads[i]) into chunks of <= `chunk` taps that never split a node or mix
- * cadences; returns the number of chunks (-1 on error). */
-int64_t amr_pack_chunks(int64_t n, const int64_t* counts, const int32_t* cads, int64_t chunk,
-                        int64_t* chunk_of, int64_t* pos_in_chunk);
-
 /* --------------------------------------------------------------- kernels -- */
 
 /* Per-slice LTS coefficient block (device memory, built by the host from
@@ -124,18 +118,22 @@ typedef struct {
   int stage, n_stages; /* s, p */
   int nonlinear;       /* 0 none, 1 sin(2chi)/r^2 (wave.py:162-163), 2 cubic chi^3 */
   int gts_cur;         /* GTS: u_curr buffer index */
-  int64_t n_tiles;
+  int64_t n_tiles;     /* tiles of this launch: a prefix of the launch order (finest cadence first) */
   int64_t n_nodes;
-  const int32_t* tile_ids;     /* leaf per CTA */
-  const int32_t* tile_table;   /* [n_tiles][entries], row t = tile t of the launch order */
-  const int64_t* interp_ptr;
-  const int32_t* interp_gid;
-  const double* interp_w;
-  const int32_t* leaf_anchor;  /* [n_leaves][3] */
-  const int32_t* leaf_level;   /* [n_leaves] octree level (spacing, faces) */
-  const int32_t* leaf_cadence; /* [n_leaves] time level (== level for LTS; promoted for single-stage) */
-  const int64_t* leaf_start;   /* [n_leaves+1] */
-  const uint8_t* node_cadence; /* [n_nodes] cadence of the owning leaf (LTS) */
+  int64_t ld;          /* row stride (elements) of U0/U1/K/Y: even, >= n_nodes + 1 */
+  /* per-tile stage programs in launch order (paper_2011_10570_b200/tileprog.py):
+   * heads (header, source bases, copy runs, slot codes) at a fixed stride of
+   * max_head bytes, bulk-copied into shared memory; tails (hanging rows, taps)
+   * 16-byte aligned, read through L2 */
+  const uint8_t* heads;
+  const uint16_t* tail;
+  int max_head;
+  int max_tail;                /* largest tail in bytes (bulk-copied into shared memory) */
+  int max_slots;               /* largest interpolation-source set of any tile (shared memory) */
+  int threads;                 /* threads per CTA: 128 or 256 */
+  long long* probe;            /* NULL, or [n_tiles][8] phase timestamps (builds with -DAMR_PHASE_PROBE) */
+  const double* wtab;          /* distinct interpolation weights (<= 64, device) */
+  int n_wtab;
   /* LTS interface pairs (zip node, reader cadence) whose source steps differently
    * from the reader: computed once per stage by amr_iface into ibuf */
   int64_t n_iface;             /* pairs of this launch (prefix: finest readers first) */
@@ -143,30 +141,13 @@ typedef struct {
   const int32_t* if_gid;
   const int32_t* if_cad;       /* reader cadence | source cadence << 8 */
   double* ibuf;                /* [2][n_iface_total] */
-  /* per-tile interpolation program: the hanging points of each tile (rows of
-   * mesh.py:316-351), summed from a per-tile set of unique source nodes */
-  const int64_t* tile_slot_ptr; /* [n_tiles+1] source slots of tile t: [ptr[t], ptr[t+1]) */
-  const int32_t* slot_gid;     /* zip node of each slot; < 0: LTS interface pair (-slot-1) */
-  const int64_t* tile_in_ptr;  /* [n_tiles+1] interpolation nodes of tile t */
-  const int64_t* in_tap_ptr;   /* [n_in+1] taps of node j, CSR (ascending gid) order */
-  const int64_t* tile_tap_ptr; /* [n_tiles+1] taps of tile t (= in_tap_ptr[tile_in_ptr[t]]) */
-  const uint16_t* in_cell;     /* [n_in] smem cell (padded ppo+4 box) the node fills */
-  const int32_t* tile_meta;    /* [n_tiles][4] {first gid, end gid, level | cadence<<8 | faces<<16, leaf} */
-  const uint16_t* cross_cells; /* [entries] padded-box cell of each stencil-cross entry */
-  const uint16_t* cross_pos;   /* [entries] interior position a0 | a1<<4 | a2<<8 (interior entries) */
-  const uint32_t* tap;         /* [n_taps] (tile-local slot << 16) | weight id; rows padded to a multiple of
-                                  4 taps with (zero slot = n_slots of the tile, weight 0) */
-  const double* wtab;          /* distinct interpolation weights */
-  int64_t n_wtab;
-  int max_slots;               /* largest slot set of any tile (dynamic shared memory) */
-  int64_t prefetch_dist;       /* tiles ahead to prefetch into L2 (resident CTAs of the launch; 0 = off) */
   int n_vt;                    /* verbatim stage-source terms of stage s+1 (a[s+1][j] != 0) */
   int vt_j[AMR_MAXP];          /* their j */
-  double* Y;                   /* [2 buffers][2][n_nodes]: verbatim sources; stage s reads buffer s&1 and its
+  double* Y;                   /* [2 buffers][2][ld]: verbatim sources; stage s reads buffer s&1 and its
                                   owners write stage s+1's into buffer (s+1)&1 */
-  double* U0;                  /* [2][n_nodes]: the reference's zip layout (chi row, phi row) */
+  double* U0;                  /* [2][ld]: the reference's zip layout (chi row, phi row) */
   double* U1;
-  double* K;                   /* [n_stages][2][n_nodes] */
+  double* K;                   /* [n_stages][2][ld] */
   const AmrSliceCoef* coef;    /* LTS only (device) */
   /* GTS coefficients */
   double g_cstage[AMR_MAXP][AMR_MAXP];
@@ -182,32 +163,22 @@ typedef struct {
   double k_chi, k_phi, f0_chi, f0_phi;
   /* stencil weights: the reference's Fornberg arrays, bit for bit (wave.py:49-54) */
   double d2c[5], d2e0[6], d2e1[6], d1c[5], d1e0[5], d1e1[5];
-  /* blob stage kernels (kernel 1, 2): one compact program blob per tile in
-   * launch order (paper_2011_10570_b200/tileprog.py).  Its head (header,
-   * source bases, copy runs, slot codes) is bulk-copied into shared memory;
-   * its tail (face entry codes, rows, taps) is read through L2 */
-  const uint16_t* blob;        /* all blobs, 16-byte aligned */
-  const int64_t* blob_off;     /* [n_tiles+1] byte offset of each tile's blob */
-  const int32_t* blob_head;    /* [n_tiles] bytes of each blob's head */
-  const uint8_t* heads;        /* [n_tiles][max_blob]: the heads again at a fixed stride (kernel 2) */
-  int max_blob;                /* largest blob head in bytes (the head stride / smem slot size) */
-  int kernel;                  /* 0: int32-table kernel, 1: persistent pipeline, 2: one CTA per tile on blobs */
-  const uint16_t* cell_ent;    /* [(ppo+4)^dim] cross entry of each padded-box cell (0xFFFF: none) */
-  int64_t ld;                  /* row stride (elements) of U0/U1/K/Y: even, >= n_nodes + 1 */
-  long long* dbg;              /* NULL, or per-warp phase cycle counters of kernel 1 (tools/phase_probe.py) */
-  int dbg_skip;                /* ablation bits (results invalid; kernels 0/2 only with -DAMR_ABLATE,
-                                  tools/ablate.py): 1 gathers, 2 rows, 4 RHS */
-  const uint16_t* tail;        /* kernel 3: per-tile hanging rows + taps (tileprog.py), 16-byte aligned */
-  int threads;                 /* kernel 3: threads per CTA (128 or 256) */
 } AmrStageParams;
 
-/* One RK stage over a prefix of the tile list: fused unzip (spatial + LTS time
- * interpolation, hanging rows summed in ascending-gid order from a per-tile
- * smem set of source values) + RHS stencil + zip of K_s; the last stage also
- * fuses the RK combine and record rotation.  Replaces Engine._stage_source +
+/* One RK stage over a prefix of the tile list: fused unzip on each tile's
+ * owned cross (copies, LTS interface sources, hanging rows summed in
+ * ascending-gid order) + RHS stencil + zip of K_s and the next stage's
+ * verbatim source; the last stage also fuses the RK combine and record
+ * rotation.  Replaces Engine._stage_source +
  * gathers[b].dot + wave_rhs + the K/state scatter (stepper.py:274-314,
  * 395-453). */
 int amr_stage(const AmrStageParams* p, void* stream);
+
+/* Layout self-check for bindings: out[0] = sizeof(AmrStageParams), then the
+ * byte offsets of n_tiles, heads, max_tail, probe, wtab, n_iface, ibuf, vt_j,
+ * Y, coef, g_cstage, g_comb, max_depth, top_nodes, lo, h2_pow2, inv_h2, r_eps,
+ * f0_phi, d2c, d1e1.  Returns the number of values written (<= cap). */
+int amr_stage_params_layout(int64_t* out, int cap);
 
 /* LTS interface pass of a stage (before amr_stage): ibuf[i] = stage source of
  * zip node if_gid[i] as seen by readers of cadence if_cad[i] — the delta=0

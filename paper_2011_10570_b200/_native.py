@@ -39,16 +39,10 @@ class AmrStageParams(C.Structure):
         ("dim", C.c_int), ("ppo", C.c_int), ("pad", C.c_int),
         ("lts", C.c_int), ("stage", C.c_int), ("n_stages", C.c_int),
         ("nonlinear", C.c_int), ("gts_cur", C.c_int),
-        ("n_tiles", C.c_int64), ("n_nodes", C.c_int64),
-        ("tile_ids", _vp), ("tile_table", _vp),
-        ("interp_ptr", _vp), ("interp_gid", _vp), ("interp_w", _vp),
-        ("leaf_anchor", _vp), ("leaf_level", _vp), ("leaf_cadence", _vp), ("leaf_start", _vp),
-        ("node_cadence", _vp),
+        ("n_tiles", C.c_int64), ("n_nodes", C.c_int64), ("ld", C.c_int64),
+        ("heads", _vp), ("tail", _vp), ("max_head", C.c_int), ("max_tail", C.c_int), ("max_slots", C.c_int), ("threads", C.c_int), ("probe", _vp),
+        ("wtab", _vp), ("n_wtab", C.c_int),
         ("n_iface", C.c_int64), ("n_iface_total", C.c_int64), ("if_gid", _vp), ("if_cad", _vp), ("ibuf", _vp),
-        ("tile_slot_ptr", _vp), ("slot_gid", _vp), ("tile_in_ptr", _vp),
-        ("in_tap_ptr", _vp), ("tile_tap_ptr", _vp), ("in_cell", _vp), ("tile_meta", _vp), ("cross_cells", _vp), ("cross_pos", _vp), ("tap", _vp), ("wtab", _vp), ("n_wtab", C.c_int64),
-        ("max_slots", C.c_int),
-        ("prefetch_dist", C.c_int64),
         ("n_vt", C.c_int), ("vt_j", C.c_int * AMR_MAXP), ("Y", _vp),
         ("U0", _vp), ("U1", _vp), ("K", _vp),
         ("coef", _vp),
@@ -64,10 +58,6 @@ class AmrStageParams(C.Structure):
         ("k_chi", C.c_double), ("k_phi", C.c_double), ("f0_chi", C.c_double), ("f0_phi", C.c_double),
         ("d2c", C.c_double * 5), ("d2e0", C.c_double * 6), ("d2e1", C.c_double * 6),
         ("d1c", C.c_double * 5), ("d1e0", C.c_double * 5), ("d1e1", C.c_double * 5),
-        ("blob", _vp), ("blob_off", _vp), ("blob_head", _vp), ("heads", _vp), ("max_blob", C.c_int),
-        ("kernel", C.c_int),
-        ("cell_ent", _vp), ("ld", C.c_int64), ("dbg", _vp), ("dbg_skip", C.c_int),
-        ("tail", _vp), ("threads", C.c_int),
     ]
 
 
@@ -93,9 +83,9 @@ SIGNATURES = {
     "amr_mesh_n_blocks": ([_vp], C.c_int64),
     "amr_mesh_blocks": ([_vp, _i32p, _i32p, _i32p, _i64p, _i32p], C.c_int),
     "amr_mesh_block_gather": ([_vp, C.c_int64, _i64p, _i64p, _i64p, _i64p, _f64p], C.c_int),
-    "amr_pack_chunks": ([C.c_int64, _i64p, _i32p, C.c_int64, _i64p, _i64p], C.c_int64),
     "amr_stage": ([C.POINTER(AmrStageParams), _vp], C.c_int),
     "amr_iface": ([C.POINTER(AmrStageParams), _vp], C.c_int),
+    "amr_stage_params_layout": ([_i64p, C.c_int], C.c_int),
     "amr_gather_rows": ([C.c_int64, _vp, _vp, _vp, C.c_int, _vp, C.c_int64, _vp, C.c_int64, _vp], C.c_int),
     "amr_block_rhs": ([C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_double, C.c_double, _vp, C.c_double,
                        C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
@@ -105,6 +95,9 @@ SIGNATURES = {
     "amr_wavelet_coeff": ([C.c_int, C.c_int, C.c_int64, _vp, _vp, _vp, C.c_int, C.c_double, C.c_double,
                            C.c_int, C.c_int, _vp, _vp, _vp], C.c_int),
 }
+
+LAYOUT_FIELDS = ["n_tiles", "heads", "max_tail", "probe", "wtab", "n_iface", "ibuf", "vt_j", "Y", "coef", "g_cstage",
+                 "g_comb", "max_depth", "top_nodes", "lo", "h2_pow2", "inv_h2", "r_eps", "f0_phi", "d2c", "d1e1"]
 
 _LIB = None
 

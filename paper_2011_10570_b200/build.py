@@ -18,7 +18,10 @@ LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libamr_b200.so")
 INCLUDE = os.path.abspath(os.path.join(HERE, "..", "include"))
 SOURCES = ["amr_kernels.cu", "amr_wavelet.cu", "amr_mesh.cpp"]
-HEADERS = ["amr_stage_pipe.cuh", "amr_stage_blob.cuh", "amr_stage_cross.cuh"]
+# the stage-kernel launcher, compiled once per (dim, ppo, lts) in parallel
+INSTANCES = [(d, p, l) for d in (2, 3) for p in (5, 7, 9) for l in (0, 1)]
+INST_SRC = "amr_stage_inst.cu"
+HEADERS = ["amr_common.cuh", "amr_async.cuh", "amr_stage_cross.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -27,42 +30,58 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(INCLUDE, "amr_b200.h")]
+    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS + [INST_SRC]] + [os.path.join(INCLUDE, "amr_b200.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile if stale.  AMR_NVCC_FLAGS adds flags (e.g. -DAMR_MIN_BLOCKS=2
-    for tuning experiments)."""
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    """Compile if stale.  AMR_NVCC_FLAGS adds flags (e.g. -DAMR_CROSS_MINB=5
+    for tuning experiments); ``out`` builds a variant library elsewhere (load
+    it with AMR_LIB_PATH)."""
+    lib_path = out or LIB
+    objdir = os.path.dirname(lib_path) if out else LIBDIR
+    if not force and not out and not _stale():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(objdir, exist_ok=True)
     extra = os.environ.get("AMR_NVCC_FLAGS", "").split()
     common = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false", *extra,
               "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off,-O2", "-I", INCLUDE]
     if verbose:
         common.insert(1, "-Xptxas=-v")
-    # one nvcc per source, in parallel, then one link
-    procs = []
-    for src in SOURCES:
-        obj = os.path.join(LIBDIR, os.path.splitext(src)[0] + ".o")
-        cmd = [*common, "-c", os.path.join(CSRC, src), "-o", obj]
-        procs.append((cmd, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
-    objs = []
-    for cmd, obj, pr in procs:
+    # one nvcc per source and per stage-kernel instance, in parallel, then one link
+    jobs = [([os.path.join(CSRC, src)], os.path.join(objdir, os.path.splitext(src)[0] + ".o")) for src in SOURCES]
+    for d, p, l in INSTANCES:
+        jobs.append(([f"-DAMR_INST_DIM={d}", f"-DAMR_INST_PPO={p}", f"-DAMR_INST_LTS={l}", os.path.join(CSRC, INST_SRC)],
+                     os.path.join(objdir, f"amr_stage_{d}_{p}_{l}.o")))
+    # heaviest first (3D ppo 9), at most one job per core
+    jobs.sort(key=lambda j: -sum(int(a.split("=")[1]) for a in j[0] if a.startswith("-DAMR_INST_")))
+    width = max(1, min(len(jobs), os.cpu_count() or 4))
+    objs, running = [], []
+
+    def reap(item):
+        cmd, obj, pr = item
         out, err = pr.communicate()
         if pr.returncode != 0:
             raise RuntimeError(f"nvcc failed ({' '.join(cmd)}):\n{out}\n{err}")
         if verbose:
             sys.stderr.write(err)
         objs.append(obj)
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lgomp"]
+
+    for srcs, obj in jobs:
+        while len(running) >= width:
+            reap(running.pop(0))
+        cmd = [*common, "-c", *srcs, "-o", obj]
+        running.append((cmd, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    for item in running:
+        reap(item)
+    cmd = [NVCC, *ARCH, "-shared", "-o", lib_path + ".tmp", *objs, "-lgomp"]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         raise RuntimeError(f"nvcc link failed ({' '.join(cmd)}):\n{proc.stdout}\n{proc.stderr}")
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib_path + ".tmp", lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    o = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=o[0] if o else None))

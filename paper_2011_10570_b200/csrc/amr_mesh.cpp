@@ -837,26 +837,3 @@ extern "C" int amr_mesh_block_gather(AmrMesh* m, int64_t block, int64_t* rows, i
   return AMR_OK;
 }
 
-// Greedy packing of interpolation nodes into CTA chunks of <= `chunk` taps that
-// never split a node and never mix reader cadences (host runtime helper for
-// the engine's interpolation program).  Returns the chunk count.
-extern "C" int64_t amr_pack_chunks(int64_t n, const int64_t* counts, const int32_t* cads, int64_t chunk,
-                                   int64_t* chunk_of, int64_t* pos_in_chunk) {
-  int64_t ch = -1, acc = 0;
-  int32_t cur = 0;
-  for (int64_t i = 0; i < n; ++i) {
-    if (counts[i] > chunk) {
-      fail(AMR_EINVAL, "interpolation row longer than one chunk");
-      return -1;
-    }
-    if (ch < 0 || acc + counts[i] > chunk || cads[i] != cur) {
-      ++ch;
-      acc = 0;
-      cur = cads[i];
-    }
-    chunk_of[i] = ch;
-    pos_in_chunk[i] = acc;
-    acc += counts[i];
-  }
-  return ch + 1;
-}

@@ -27,12 +27,12 @@
 template <int DIM, int PPO>
 struct CrossK {
   using T = Tile<DIM, PPO>;
-  static constexpr int HEAD = 16 + 64 * 8;                 // mbarrier, interpolation weights
-  static constexpr int BOXB = (T::NS * 8 + 15) / 16 * 16;  // the stencil box (chi; phi in step 5)
+  static constexpr int HEAD = 16 + 64 * 8;                 // 2 mbarriers, interpolation weights
+  static constexpr int BOXB = (T::BOX * 8 + 15) / 16 * 16;  // the stencil box (chi; phi in step 5)
   static constexpr int OWNB = (T::NI * 2 + 15) / 16 * 16;  // owned node -> box cell (uint16)
   __host__ __device__ static int slot_bytes(int max_slots) { return ((max_slots + 1) * 8 + 15) / 16 * 16; }
-  __host__ __device__ static size_t smem_bytes(int max_slots, int max_head) {
-    return HEAD + (size_t)max_head + BOXB + slot_bytes(max_slots) + OWNB;
+  __host__ __device__ static size_t smem_bytes(int max_slots, int max_head, int max_tail) {
+    return HEAD + (size_t)max_head + (size_t)max_tail + BOXB + slot_bytes(max_slots) + OWNB;
   }
 };
 
@@ -83,26 +83,26 @@ __device__ __forceinline__ void cross_gather(const int* __restrict__ h, double* 
   if (threadIdx.x == 0) slot[nslot] = 0.0;  // zero slot of the padding taps
 }
 
-// step 3: hanging rows into the box.  Two quads of taps per step: their 8
-// products first, then the 8 ordered adds; the next tap words in flight.
+// step 3: hanging rows into the box, from the tile's tail in shared memory.
+// Two quads of taps per step: their 8 products first, then the 8 ordered adds.
 template <int NTH>
-__device__ __forceinline__ void cross_rows(const uint16_t* __restrict__ tl, int nrow, int taps_off,
-                                           const double* s_w, const double* slot, double* box) {
+__device__ __forceinline__ void cross_rows(const uint16_t* tl, int nrow, int taps_off, const double* s_w,
+                                           const double* slot, double* box) {
   const uint32_t* rows = reinterpret_cast<const uint32_t*>(tl);
   const uint2* taps = reinterpret_cast<const uint2*>(tl + taps_off);
   for (int r = threadIdx.x; r < nrow; r += NTH) {
-    const uint32_t w = __ldg(rows + r);
+    const uint32_t w = rows[r];
     const int nq = (w >> 12) & 31;
     const uint2* tq = taps + (w >> 17);
     double ax = 0.0;
-    uint2 a = nq > 0 ? __ldg(tq) : make_uint2(0u, 0u);
-    uint2 b = nq > 1 ? __ldg(tq + 1) : make_uint2(0u, 0u);
+    uint2 a = nq > 0 ? tq[0] : make_uint2(0u, 0u);
+    uint2 b = nq > 1 ? tq[1] : make_uint2(0u, 0u);
     int q = 0;
     for (; q + 2 <= nq; q += 2) {
       const uint32_t t8[8] = {a.x & 0xFFFF, a.x >> 16, a.y & 0xFFFF, a.y >> 16,
                               b.x & 0xFFFF, b.x >> 16, b.y & 0xFFFF, b.y >> 16};
-      if (q + 2 < nq) a = __ldg(tq + q + 2);
-      if (q + 3 < nq) b = __ldg(tq + q + 3);
+      if (q + 2 < nq) a = tq[q + 2];
+      if (q + 3 < nq) b = tq[q + 3];
       double pr[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) pr[u] = s_w[t8[u] & 63] * slot[t8[u] >> 6];
@@ -131,18 +131,19 @@ struct BoxLine {
 
 template <int DIM, int PPO>
 __device__ __forceinline__ int box_stride(int d) {
-  constexpr int NP = Tile<DIM, PPO>::NP;
-  return (DIM == 3) ? (d == 0 ? NP * NP : (d == 1 ? NP : 1)) : (d == 0 ? NP : 1);
+  using T = Tile<DIM, PPO>;
+  return (DIM == 3) ? (d == 0 ? T::NP * T::RS : (d == 1 ? T::RS : 1)) : (d == 0 ? T::RS : 1);
 }
 
 template <int DIM, int PPO>
 __device__ __forceinline__ void cell_pos(int cell, int* pos) {
-  constexpr int NP = Tile<DIM, PPO>::NP;
-  int c = cell;
+  using T = Tile<DIM, PPO>;
+  pos[DIM - 1] = cell % T::RS - 2;
+  int c = cell / T::RS;
 #pragma unroll
-  for (int d = DIM - 1; d >= 0; --d) {
-    pos[d] = c % NP - 2;
-    c /= NP;
+  for (int d = DIM - 2; d >= 0; --d) {
+    pos[d] = c % T::NP - 2;
+    c /= T::NP;
   }
 }
 
@@ -155,145 +156,176 @@ __device__ __forceinline__ bool on_face_of(const int* pos, int n, int faces) {
   return f;
 }
 
-template <int DIM, int PPO, bool LTS, int NT, int NTH>
-__global__ void __launch_bounds__(NTH, (NTH <= 128 ? 8 : 4)) stage_cross(const __grid_constant__ AmrStageParams P) {
-  using T = Tile<DIM, PPO>;
-  using CK = CrossK<DIM, PPO>;
-  constexpr int OPT = (T::NI + NTH - 1) / NTH;
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  double* s_w = reinterpret_cast<double*>(smem + 16);
-  unsigned char* head = smem + CK::HEAD;
-  double* box = reinterpret_cast<double*>(head + P.max_blob);
-  double* slot = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(box) + CK::BOXB);
-  uint16_t* own = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(slot) + CK::slot_bytes(P.max_slots));
-  const int tid = threadIdx.x;
-  const int64_t tile = blockIdx.x;
+// A tile's decoded header and stage context.
+struct TileCtx {
+  const int* h;           // head in shared memory
+  const uint16_t* tl;     // tail in global memory
+  int g0, n_own, nrow, taps_off, lvl, cad, faces;
+  const double* Ucur;     // u_curr buffer of the tile's cadence
+  const double* V;        // verbatim stage source (u at stage 0, Y after)
+  double* Unew;           // the other u buffer (RK combine target)
+};
+
+__device__ __forceinline__ TileCtx tile_ctx(const AmrStageParams& P, const unsigned char* head, bool lts) {
+  TileCtx c;
+  c.h = reinterpret_cast<const int*>(head);
+  c.g0 = c.h[0];
+  c.n_own = c.h[1];
+  const int lmeta = c.h[2];
+  c.nrow = c.h[5];
+  c.lvl = lmeta & 0xFF;
+  c.cad = (lmeta >> 8) & 0xFF;
+  c.faces = (lmeta >> 16) & 0x3F;
+  c.tl = P.tail + (int64_t)c.h[14] * 8;
+  c.taps_off = c.h[15];
+  const int cur = lts ? P.coef->cur[c.cad] : P.gts_cur;
+  c.Ucur = cur ? P.U1 : P.U0;
+  c.Unew = cur ? P.U0 : P.U1;
+  c.V = (P.stage == 0) ? c.Ucur : P.Y + (int64_t)(P.stage & 1) * 2 * P.ld;
+  return c;
+}
+
+// one thread: on the last stage, L2 prefetch of the combine's K_j over the
+// owned range
+__device__ __forceinline__ void tile_prefetch(const AmrStageParams& P, const TileCtx& c) {
+  if (P.stage == P.n_stages - 1) {
+    const int64_t n = P.ld;
+    const int64_t a16 = c.g0 & ~1, e16 = (c.g0 + c.n_own + 1) & ~1;
+    const uint32_t bytes = (uint32_t)(e16 - a16) * 8;
+    for (int jj = 0; jj < P.stage; ++jj) {
+      bulk_prefetch_l2(P.K + (int64_t)jj * 2 * n + a16, bytes);
+      bulk_prefetch_l2(P.K + (int64_t)jj * 2 * n + n + a16, bytes);
+    }
+  }
+}
+
+// this thread's owned nodes (k = tid + r*NTH): phi of the stage source and u
+template <int OPT, int NTH>
+__device__ __forceinline__ void owned_loads(const AmrStageParams& P, const TileCtx& c, double* pc, double* u0,
+                                            double* u1) {
+  const int64_t n = P.ld;
+#pragma unroll
+  for (int r = 0; r < OPT; ++r) {
+    const int k = threadIdx.x + r * NTH;
+    const int64_t g = c.g0 + (k < c.n_own ? k : 0);
+    pc[r] = __ldg(c.V + n + g);
+    u0[r] = __ldg(c.Ucur + g);
+    u1[r] = __ldg(c.Ucur + n + g);
+  }
+}
+
+// K_s, the next stage's verbatim source, or the RK combine of owned node k
+template <bool LTS, int NT>
+__device__ __forceinline__ void tile_epilogue(const AmrStageParams& P, const TileCtx& c, int k, double2 ks,
+                                              double2 uor) {
   const int64_t n = P.ld;
   const int s = P.stage;
   const bool last = (s == P.n_stages - 1);
   const AmrSliceCoef* C = P.coef;
-
-  // ---- 1: the head (one bulk copy at a fixed stride), weights meanwhile
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    const uint32_t hb = (uint32_t)P.max_blob;
-    mbar_expect_tx(bar, hb);
-    bulk_g2s(head, P.heads + tile * (int64_t)hb, hb, bar);
-  }
-  for (int i = tid; i < P.n_wtab; i += NTH) s_w[i] = __ldg(P.wtab + i);
-  __syncthreads();  // mbarrier initialised before anyone waits on it
-  mbar_wait(bar, 0);
-  const int* h = reinterpret_cast<const int*>(head);
-  const int g0 = h[0], n_own = h[1], lmeta = h[2], nrow = h[5];
-  const int lvl = lmeta & 0xFF;
-  const int cad = (lmeta >> 8) & 0xFF;
-  const int faces = (lmeta >> 16) & 0x3F;
-  const uint16_t* tl = P.tail + (int64_t)h[14] * 8;
-  const int taps_off = h[15];
-  const int cur = LTS ? C->cur[cad] : P.gts_cur;
-  const double* Ucur = cur ? P.U1 : P.U0;
-  const double* V = (s == 0) ? Ucur : P.Y + (int64_t)(s & 1) * 2 * n;
-  if (tid == 0) {
-    if (h[7]) bulk_prefetch_l2(tl, (uint32_t)h[7]);
-    // owned ranges the RHS and epilogue read: u (chi, phi), the stage
-    // source's phi row, and on the last stage the combine's K_j
-    const int64_t a16 = g0 & ~1, e16 = (g0 + n_own + 1) & ~1;
-    const uint32_t bytes = (uint32_t)(e16 - a16) * 8;
-    bulk_prefetch_l2(Ucur + a16, bytes);
-    bulk_prefetch_l2(Ucur + n + a16, bytes);
-    if (s) bulk_prefetch_l2(V + n + a16, bytes);
-    if (last)
-      for (int jj = 0; jj < s; ++jj) {
-        bulk_prefetch_l2(P.K + (int64_t)jj * 2 * n + a16, bytes);
-        bulk_prefetch_l2(P.K + (int64_t)jj * 2 * n + n + a16, bytes);
-      }
-  }
-
-  // ---- 2, 3: chi on the owned cross
-  cross_gather<LTS, NTH>(h, box, slot, own, V, P.ibuf, 0, 0, g0, true);
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  cross_rows<NTH>(tl, nrow, taps_off, s_w, slot, box);
-  __syncthreads();
-
-  // ---- 4: RHS at the owned nodes
-  const Weights& W = P;
-  const double h_l = P.h[lvl], h2 = P.h2[lvl], inv_h2 = P.inv_h2[lvl];
-  const bool pow2 = P.h2_pow2[lvl] != 0;
-  const bool face = faces != 0;
-  const bool need_x = face || P.nonlinear == 1;
-  double* Unew = cur ? P.U0 : P.U1;
+  const int64_t g = c.g0 + k;
   double* Ks = P.K + (int64_t)s * 2 * n;
-  const int64_t side_len = (int64_t)1 << (P.max_depth - lvl);
-
-  // K_s, the next stage's verbatim source, or the RK combine of owned node k
-  auto epilogue = [&](int k, double2 ks) {
-    const int64_t g = g0 + k;
-    const double2 uor = make_double2(__ldg(Ucur + g), __ldg(Ucur + n + g));
-    if (!last || LTS) {
-      Ks[g] = ks.x;
-      Ks[n + g] = ks.y;
-    }
-    if (!last) {
-      double yx = 0.0 + uor.x, yy = 0.0 + uor.y;
+  if (!last || LTS) {
+    Ks[g] = ks.x;
+    Ks[n + g] = ks.y;
+  }
+  if (!last) {
+    double yx = 0.0 + uor.x, yy = 0.0 + uor.y;
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        const int jv = P.vt_j[t];
-        const double c = LTS ? C->cstage[cad][s + 1][jv] : P.g_cstage[s + 1][jv];
-        const double kx = (jv == s) ? ks.x : __ldg(P.K + (int64_t)jv * 2 * n + g);
-        const double ky = (jv == s) ? ks.y : __ldg(P.K + (int64_t)jv * 2 * n + n + g);
-        yx = yx + c * kx;
-        yy = yy + c * ky;
+    for (int t = 0; t < NT; ++t) {
+      const int jv = P.vt_j[t];
+      const double cf = LTS ? C->cstage[c.cad][s + 1][jv] : P.g_cstage[s + 1][jv];
+      const double kx = (jv == s) ? ks.x : __ldg(P.K + (int64_t)jv * 2 * n + g);
+      const double ky = (jv == s) ? ks.y : __ldg(P.K + (int64_t)jv * 2 * n + n + g);
+      yx = yx + cf * kx;
+      yy = yy + cf * ky;
+    }
+    double* Yout = P.Y + (int64_t)((s + 1) & 1) * 2 * n;
+    Yout[g] = yx;
+    Yout[n + g] = yy;
+  } else {
+    // every K_j (j < s) in flight at once, then the ordered combine
+    double kx[AMR_MAXP], ky[AMR_MAXP];
+#pragma unroll
+    for (int jj = 0; jj < AMR_MAXP; ++jj) {
+      if (jj < s) {
+        kx[jj] = __ldg(P.K + (int64_t)jj * 2 * n + g);
+        ky[jj] = __ldg(P.K + (int64_t)jj * 2 * n + n + g);
+      } else {
+        kx[jj] = ks.x;
+        ky[jj] = ks.y;
       }
-      double* Yout = P.Y + (int64_t)((s + 1) & 1) * 2 * n;
-      Yout[g] = yx;
-      Yout[n + g] = yy;
-    } else {
-      double ux = 0.0 + uor.x, uy = 0.0 + uor.y;
-      for (int jj = 0; jj < P.n_stages; ++jj) {
-        const double c = LTS ? C->comb[cad][jj] : P.g_comb[jj];
-        if (c == 0.0) continue;
-        const double kx = (jj == s) ? ks.x : __ldg(P.K + (int64_t)jj * 2 * n + g);
-        const double ky = (jj == s) ? ks.y : __ldg(P.K + (int64_t)jj * 2 * n + n + g);
-        ux = ux + c * kx;
-        uy = uy + c * ky;
-      }
-      Unew[g] = ux;
-      Unew[n + g] = uy;
     }
-  };
-  auto coords = [&](const int* pos, double* x) {
+    double ux = 0.0 + uor.x, uy = 0.0 + uor.y;
 #pragma unroll
-    for (int d = 0; d < DIM; ++d) {
-      const int64_t lat = (int64_t)h[8 + d] * (PPO - 1) + side_len * pos[d];
-      x[d] = P.lo[d] + ((double)lat / (double)P.top_nodes) * P.extent[d];
+    for (int jj = 0; jj < AMR_MAXP; ++jj) {
+      if (jj >= P.n_stages) break;
+      const double cf = LTS ? C->comb[c.cad][jj] : P.g_comb[jj];
+      if (cf == 0.0) continue;
+      ux = ux + cf * kx[jj];
+      uy = uy + cf * ky[jj];
     }
-  };
-  auto radius = [&](const double* x) {
-    double r2 = x[0] * x[0];
-#pragma unroll
-    for (int d = 1; d < DIM; ++d) r2 = r2 + x[d] * x[d];
-    const double r = sqrt(r2);
-    return r > P.r_eps ? r : P.r_eps;
-  };
+    c.Unew[g] = ux;
+    c.Unew[n + g] = uy;
+  }
+}
 
+template <int DIM, int PPO>
+__device__ __forceinline__ void tile_coords(const AmrStageParams& P, const TileCtx& c, const int* pos, double* x) {
+  const int64_t side_len = (int64_t)1 << (P.max_depth - c.lvl);
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) {
+    const int64_t lat = (int64_t)c.h[8 + d] * (PPO - 1) + side_len * pos[d];
+    x[d] = P.lo[d] + ((double)lat / (double)P.top_nodes) * P.extent[d];
+  }
+}
+
+template <int DIM>
+__device__ __forceinline__ double face_radius(const AmrStageParams& P, const double* x) {
+  double r2 = x[0] * x[0];
+#pragma unroll
+  for (int d = 1; d < DIM; ++d) r2 = r2 + x[d] * x[d];
+  const double r = sqrt(r2);
+  return r > P.r_eps ? r : P.r_eps;
+}
+
+// radiative row of one variable at an on-face node (wave.py:173-201):
+// (sum_d x_d * d1_d f) / max(r, r_eps), from the box holding that variable
+template <int DIM, int PPO>
+__device__ __forceinline__ double radial_term(const AmrStageParams& P, const double* box, int cell, const int* pos,
+                                              int faces, const double* x, double h_l) {
+  double a = 0.0;
+#pragma unroll
+  for (int d = 0; d < DIM; ++d) {
+    BoxLine<DIM, PPO> get{box, cell, box_stride<DIM, PPO>(d)};
+    const double gd = deriv(get, 1, pos[d], PPO, faces & (1 << (2 * d)), faces & (2 << (2 * d)), P, h_l, false, 0.0);
+    const double term = x[d] * gd;
+    a = (d == 0) ? term : a + term;
+  }
+  return a / face_radius<DIM>(P, x);
+}
+
+// step 4: RHS at the owned nodes from the chi box; on-face nodes of a
+// physical-face tile store their dchi in K_s and defer the rest to step 5
+template <int DIM, int PPO, bool LTS, int NT, int NTH, int OPT>
+__device__ __forceinline__ void rhs_pass1(const AmrStageParams& P, const TileCtx& c, const double* box,
+                                          const uint16_t* own, const double* pc, const double* u0, const double* u1) {
+  const double h2 = P.h2[c.lvl], inv_h2 = P.inv_h2[c.lvl];
+  const bool pow2 = P.h2_pow2[c.lvl] != 0;
+  const bool need_x = c.faces != 0 || P.nonlinear == 1;
 #pragma unroll
   for (int r = 0; r < OPT; ++r) {
-    const int k = tid + r * NTH;
-    if (k >= n_own) break;
+    const int k = threadIdx.x + r * NTH;
+    if (k >= c.n_own) break;
     const int cell = own[k];
-    const double phi_c = __ldg(V + n + g0 + k);
+    const double phi_c = pc[r];
     if (!need_x) {  // centred 4th-order Laplacian (+ cubic), dchi = phi (wave.py:147-170)
       double lap = 0.0;
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
         const int S = box_stride<DIM, PPO>(d);
-        double t = W.d2c[0] * box[cell - 2 * S];
+        double t = P.d2c[0] * box[cell - 2 * S];
 #pragma unroll
-        for (int q = 1; q < 5; ++q) t = t + W.d2c[q] * box[cell + (q - 2) * S];
+        for (int q = 1; q < 5; ++q) t = t + P.d2c[q] * box[cell + (q - 2) * S];
         t = pow2 ? t * inv_h2 : t / h2;
         lap = (d == 0) ? t : lap + t;
       }
@@ -302,21 +334,20 @@ __global__ void __launch_bounds__(NTH, (NTH <= 128 ? 8 : 4)) stage_cross(const _
         const double chi = box[cell];
         dphi = dphi - (chi * chi) * chi;
       }
-      epilogue(k, make_double2(phi_c, dphi));
+      tile_epilogue<LTS, NT>(P, c, k, make_double2(phi_c, dphi), make_double2(u0[r], u1[r]));
       continue;
     }
     int pos[3] = {0, 0, 0};
     cell_pos<DIM, PPO>(cell, pos);
     double x[3] = {0.0, 0.0, 0.0};
-    coords(pos, x);
-    const bool of = on_face_of<DIM>(pos, PPO, faces);
+    tile_coords<DIM, PPO>(P, c, pos, x);
     const double chi = box[cell];
-    if (!of) {
+    if (!on_face_of<DIM>(pos, PPO, c.faces)) {
       double lap = 0.0;
 #pragma unroll
       for (int d = 0; d < DIM; ++d) {
         BoxLine<DIM, PPO> get{box, cell, box_stride<DIM, PPO>(d)};
-        const double t = deriv(get, 2, pos[d], PPO, faces & (1 << (2 * d)), faces & (2 << (2 * d)), W, h2, pow2,
+        const double t = deriv(get, 2, pos[d], PPO, c.faces & (1 << (2 * d)), c.faces & (2 << (2 * d)), P, h2, pow2,
                                inv_h2);
         lap = (d == 0) ? t : lap + t;
       }
@@ -330,52 +361,126 @@ __global__ void __launch_bounds__(NTH, (NTH <= 128 ? 8 : 4)) stage_cross(const _
       } else if (P.nonlinear == 2) {
         dphi = dphi - (chi * chi) * chi;
       }
-      epilogue(k, make_double2(phi_c, dphi));
-    } else {  // radiative row, chi part (wave.py:173-201); phi part in step 5
-      double a = 0.0;
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) {
-        BoxLine<DIM, PPO> get{box, cell, box_stride<DIM, PPO>(d)};
-        const double gd = deriv(get, 1, pos[d], PPO, faces & (1 << (2 * d)), faces & (2 << (2 * d)), W, h_l, false,
-                                0.0);
-        const double term = x[d] * gd;
-        a = (d == 0) ? term : a + term;
-      }
-      Ks[g0 + k] = a / radius(x) - P.k_chi * (chi - P.f0_chi);
+      tile_epilogue<LTS, NT>(P, c, k, make_double2(phi_c, dphi), make_double2(u0[r], u1[r]));
+    } else {  // radiative row, chi part; the phi part in step 5
+      P.K[(int64_t)P.stage * 2 * P.ld + c.g0 + k] =
+          radial_term<DIM, PPO>(P, box, cell, pos, c.faces, x, P.h[c.lvl]) - P.k_chi * (chi - P.f0_chi);
     }
   }
-  if (!face) return;
+}
 
-  // ---- 5: physical-face tiles: phi on the owned cross, radiative phi rows
-  __syncthreads();  // everyone is done reading chi from the box
-  cross_gather<LTS, NTH>(h, box, slot, own, V, P.ibuf, n, P.n_iface_total, g0, false);
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  cross_rows<NTH>(tl, nrow, taps_off, s_w, slot, box);
-  __syncthreads();
+// step 5 (after phi replaced chi in the box): radiative phi rows of the
+// on-face nodes and their deferred epilogue
+template <int DIM, int PPO, bool LTS, int NT, int NTH, int OPT>
+__device__ __forceinline__ void rhs_pass2(const AmrStageParams& P, const TileCtx& c, const double* box,
+                                          const uint16_t* own, const double* u0, const double* u1) {
 #pragma unroll
   for (int r = 0; r < OPT; ++r) {
-    const int k = tid + r * NTH;
-    if (k >= n_own) break;
+    const int k = threadIdx.x + r * NTH;
+    if (k >= c.n_own) break;
     const int cell = own[k];
     int pos[3] = {0, 0, 0};
     cell_pos<DIM, PPO>(cell, pos);
-    if (!on_face_of<DIM>(pos, PPO, faces)) continue;
+    if (!on_face_of<DIM>(pos, PPO, c.faces)) continue;
     double x[3] = {0.0, 0.0, 0.0};
-    coords(pos, x);
-    double a = 0.0;
-#pragma unroll
-    for (int d = 0; d < DIM; ++d) {
-      BoxLine<DIM, PPO> get{box, cell, box_stride<DIM, PPO>(d)};
-      const double gd = deriv(get, 1, pos[d], PPO, faces & (1 << (2 * d)), faces & (2 << (2 * d)), W, h_l, false,
-                              0.0);
-      const double term = x[d] * gd;
-      a = (d == 0) ? term : a + term;
-    }
+    tile_coords<DIM, PPO>(P, c, pos, x);
     const double phi_c = box[cell];
-    const double dphi = a / radius(x) - P.k_phi * (phi_c - P.f0_phi);
-    const double dchi = *(volatile const double*)(Ks + g0 + k);  // written by this thread in step 4
-    epilogue(k, make_double2(dchi, dphi));
+    const double dphi = radial_term<DIM, PPO>(P, box, cell, pos, c.faces, x, P.h[c.lvl]) - P.k_phi * (phi_c - P.f0_phi);
+    // dchi was written by this thread in step 4
+    const double dchi = *(volatile const double*)(P.K + (int64_t)P.stage * 2 * P.ld + c.g0 + k);
+    tile_epilogue<LTS, NT>(P, c, k, make_double2(dchi, dphi), make_double2(u0[r], u1[r]));
   }
+}
+
+#ifndef AMR_CROSS_MINB
+#define AMR_CROSS_MINB 4  // resident 256-thread CTAs per SM the register budget is sized for
+#endif
+
+#ifdef AMR_PHASE_PROBE
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define AMR_PROBE(i) \
+  if (P.probe && threadIdx.x == 0) P.probe[(int64_t)blockIdx.x * 8 + (i)] = gtimer()
+#else
+#define AMR_PROBE(i)
+#endif
+
+// One CTA per tile.
+template <int DIM, int PPO, bool LTS, int NT, int NTH>
+__global__ void __launch_bounds__(NTH, (NTH <= 128 ? 2 * AMR_CROSS_MINB : AMR_CROSS_MINB))
+    stage_cross(const __grid_constant__ AmrStageParams P) {
+  using T = Tile<DIM, PPO>;
+  using CK = CrossK<DIM, PPO>;
+  constexpr int OPT = (T::NI + NTH - 1) / NTH;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+  double* s_w = reinterpret_cast<double*>(smem + 16);
+  unsigned char* head = smem + CK::HEAD;
+  uint16_t* s_tail = reinterpret_cast<uint16_t*>(head + P.max_head);
+  double* box = reinterpret_cast<double*>(head + P.max_head + P.max_tail);
+  double* slot = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(box) + CK::BOXB);
+  uint16_t* own = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(slot) + CK::slot_bytes(P.max_slots));
+  const int tid = threadIdx.x;
+  AMR_PROBE(0);
+
+  // ---- 1: the head (one bulk copy at a fixed stride), weights meanwhile
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    const uint32_t hb = (uint32_t)P.max_head;
+    mbar_expect_tx(bar, hb);
+    bulk_g2s(head, P.heads + (int64_t)blockIdx.x * hb, hb, bar);
+  }
+  // interpolation weights: in flight with the gathers (waited for with them)
+  for (int i = tid; i < P.n_wtab; i += NTH) cp_async8(s_w + i, P.wtab + i);
+  __syncthreads();  // mbarrier initialised before anyone waits on it
+  mbar_wait(bar, 0);
+  AMR_PROBE(1);
+  const TileCtx c = tile_ctx(P, head, LTS);
+  const uint32_t tail_bytes = (uint32_t)c.h[7];
+  if (tid == 0) {
+    // the tail (hanging rows, taps): one bulk copy, lands during the gathers
+    if (tail_bytes) {
+      mbar_expect_tx(bar + 1, tail_bytes);
+      bulk_g2s(s_tail, c.tl, tail_bytes, bar + 1);
+    }
+    tile_prefetch(P, c);
+  }
+
+  // ---- 2, 3: chi on the owned cross; owned-node loads in flight meanwhile
+  cross_gather<LTS, NTH>(c.h, box, slot, own, c.V, P.ibuf, 0, 0, c.g0, true);
+  cp_async_commit();
+  AMR_PROBE(2);
+  double pc[OPT], u0[OPT], u1[OPT];
+  owned_loads<OPT, NTH>(P, c, pc, u0, u1);
+  cp_async_wait<0>();
+  __syncthreads();
+  AMR_PROBE(3);
+  if (tail_bytes) mbar_wait(bar + 1, 0);
+  cross_rows<NTH>(s_tail, c.nrow, c.taps_off, s_w, slot, box);
+  __syncthreads();
+  AMR_PROBE(4);
+
+  // ---- 4: RHS at the owned nodes
+  rhs_pass1<DIM, PPO, LTS, NT, NTH, OPT>(P, c, box, own, pc, u0, u1);
+  AMR_PROBE(5);
+#ifdef AMR_PHASE_PROBE
+  __syncthreads();
+  AMR_PROBE(6);
+#endif
+  if (c.faces == 0) return;
+
+  // ---- 5: physical-face tiles: phi on the owned cross, radiative phi rows
+  __syncthreads();  // everyone is done reading chi from the box
+  cross_gather<LTS, NTH>(c.h, box, slot, own, c.V, P.ibuf, P.ld, P.n_iface_total, c.g0, false);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  cross_rows<NTH>(s_tail, c.nrow, c.taps_off, s_w, slot, box);
+  __syncthreads();
+  rhs_pass2<DIM, PPO, LTS, NT, NTH, OPT>(P, c, box, own, u0, u1);
 }

@@ -143,37 +143,6 @@ class WorkCounters:
         return out
 
 
-_IFACE_BASE = -(1 << 20)  # AMR_IFACE_BASE in amr_kernels.cu
-
-
-def _cross_local(e: np.ndarray, dim: int, ppo: int, pad: int = 2) -> np.ndarray:
-    """Padded local coordinates of stencil-cross entries (the enumeration of
-    cross_entry_local in amr_mesh.cpp)."""
-    e = np.asarray(e, dtype=np.int64)
-    NI, NF = ppo ** dim, ppo ** (dim - 1)
-    loc = np.zeros((len(e), dim), dtype=np.int64)
-    inner = e < NI
-    r = e[inner].copy()
-    for d in range(dim - 1, -1, -1):
-        loc[inner, d] = pad + r % ppo
-        r //= ppo
-    h = ~inner
-    r = e[h] - NI
-    axis = r // (2 * pad * NF)
-    r = r % (2 * pad * NF)
-    layer = r // NF
-    within = r % NF
-    lp = np.where(layer < pad, layer, ppo + layer)
-    sub = np.zeros((len(r), dim), dtype=np.int64)
-    for d in range(dim - 1, -1, -1):
-        others = axis != d
-        sub[others, d] = pad + within[others] % ppo
-        within = np.where(others, within // ppo, within)
-    sub[np.arange(len(r)), axis] = lp
-    loc[h] = sub
-    return loc
-
-
 def _pow2_exact(x: float) -> bool:
     m, _ = np.frexp(x)
     return x > 0 and m == 0.5
@@ -261,12 +230,7 @@ class Engine:
         order = np.lexsort((mine, -leaf_cad[mine]))
         tiles = mine[order].astype(np.int32)
         lts_kernel = mode == "lts" or any(c != self.l_max for c in cadence)
-        self._kernel = int(os.environ.get("AMR_KERNEL", "3"))
-        self._ibuf = None
-        if self._kernel == 3:
-            self._init_programs(td, tiles, leaf_cad, node_cad, lts_kernel)
-        else:
-            self._init_tables(td, tiles, leaf_cad, node_cad, lts_kernel)
+        self._init_programs(td, tiles, leaf_cad, node_cad, lts_kernel)
         n = mesh.n_nodes
         # the reference's (nvars, n_nodes) zip layout, SoA: chi row then phi row.
         # Rows are padded to an even stride ld > n (16-byte aligned rows; the
@@ -287,7 +251,7 @@ class Engine:
         self._exchange = _EngineExchange(self) if self._dist is not None else None
 
     def _init_programs(self, td, tiles, leaf_cad, node_cad, lts):
-        """Kernel 3: the owned-cross programs of tileprog.py."""
+        """The stage kernel's per-tile programs (tileprog.py) on the device."""
         import torch
 
         from . import tileprog
@@ -305,36 +269,12 @@ class Engine:
                        tail=T(prog["tail"]), wtab=T(prog["wtab"]), if_gid=T(pad(prog["if_gid"])),
                        if_cad=T(pad(prog["if_cad"])))
         self._max_slots = prog["max_slots"]
-        self._max_blob = prog["max_head"]
+        self._max_head = prog["max_head"]
+        self._max_tail = prog["max_tail"]
         self._ibuf = torch.zeros((2, max(n_iface, 1)), dtype=torch.float64, device=dev)
-        self._threads = int(os.environ.get("AMR_THREADS", "128"))
+        self._threads = int(os.environ.get("AMR_THREADS", "256"))
 
-    def _init_tables(self, td, tiles, leaf_cad, node_cad, lts_kernel):
-        """Kernels 0-2 (round 1): int32 tile tables and blobs."""
-        import torch
 
-        mesh = self.mesh
-        tcad = leaf_cad[tiles]
-        self._prefix = {c: int(np.sum(tcad >= c)) for c in range(self.l_max + 1)}
-        table, prog = self._tile_programs(td, tiles, node_cad, leaf_cad, lts=lts_kernel)
-        n_iface = prog.pop("n_iface")
-        blobs = self._build_blobs(table, prog, n_iface, td, mesh.dim, mesh.ppo)
-        self._if_prefix = {c: int(np.sum((prog["if_cad"][:n_iface] & 0xFF) >= c)) for c in range(self.l_max + 1)}
-        self._n_iface = n_iface
-        dev = self.device
-        T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
-        self._d = dict(tiles=T(tiles), table=T(table), anchor=T(td["anchor3"]), level=T(td["level"]),
-                       cadence=T(leaf_cad), starts=T(td["starts"]), node_cad=T(node_cad),
-                       **{k: T(v) for k, v in prog.items() if k != "max_slots"})
-        self._max_slots = prog["max_slots"]
-        self._kernel = blobs["kernel"] if blobs is not None else 0
-        if blobs is not None:
-            self._d.update(blob=T(blobs["blob"]), blob_off=T(blobs["blob_off"]), blob_head=T(blobs["blob_head"]),
-                           heads=T(blobs["heads"]),
-                           cell_ent=T(blobs["cell_ent"]))
-            self._max_blob = blobs["max_blob"]
-        self._ibuf = torch.zeros((2, max(n_iface, 1)), dtype=torch.float64, device=dev)
-        self._threads = 0
 
     # -- setup -------------------------------------------------------------------------
     def _promoted_cadence(self, levels: list[int]) -> list[int]:
@@ -354,155 +294,6 @@ class Engine:
                     cadence[i] = max(cadence[i], levels[j])
         return cadence
 
-    @staticmethod
-    def _tile_programs(td: dict, tiles: np.ndarray, node_cad: np.ndarray, leaf_cad: np.ndarray, lts: bool = False):
-        """Tile tables in launch order plus each tile's interpolation program.
-
-        A tile's hanging points (table entries <= -2, one interpolation row
-        each) become its own rows, numbered tile-locally in the table.  Their
-        taps refer to a per-tile set of unique source nodes ("slots") that the
-        kernel gathers once into shared memory; taps keep the row's CSR
-        (ascending gid) order and a 16-bit weight id.  Rows are padded to a
-        multiple of 4 taps with weight 0 on the tile's zero slot (index
-        n_slots), which leaves the running sum unchanged."""
-        dim, ppo = td["dim"], td["ppo"]
-        table = td["table"][tiles].copy()
-        ptr, gid, w = td["interp_ptr"], td["interp_gid"], td["interp_w"]
-        nt, E = table.shape
-        NP = ppo + 4
-        loc = _cross_local(np.arange(E), dim, ppo)
-        cross_cells = np.zeros(E, dtype=np.int64)
-        cross_pos = np.zeros(E, dtype=np.int64)
-        for d in range(dim):
-            cross_cells = cross_cells * NP + loc[:, d]
-            cross_pos |= np.clip(loc[:, d] - 2, 0, 15) << (4 * d)
-        t_idx, e_idx = np.nonzero(table <= -2)  # row-major: by tile, then entry
-        rows = (-table[t_idx, e_idx] - 2).astype(np.int64)
-        # within a tile, longest rows first: thread t sums rows t, t+256, ... so
-        # this balances the sequential sums across threads (any order is exact)
-        cnt0 = ptr[rows + 1] - ptr[rows]
-        order = np.lexsort((e_idx, -cnt0, t_idx))
-        t_idx, e_idx, rows = t_idx[order], e_idx[order], rows[order]
-        n_in = len(rows)
-        tile_in_ptr = np.zeros(nt + 1, dtype=np.int64)
-        np.cumsum(np.bincount(t_idx, minlength=nt), out=tile_in_ptr[1:])
-        local_in = np.arange(n_in) - tile_in_ptr[t_idx]
-        table[t_idx, e_idx] = (-(local_in + 2)).astype(np.int32)
-        counts = (ptr[rows + 1] - ptr[rows]).astype(np.int64)
-        padded = (counts + 3) // 4 * 4
-        in_tap_ptr = np.zeros(n_in + 1, dtype=np.int64)
-        np.cumsum(padded, out=in_tap_ptr[1:])
-        n_real = int(counts.sum())
-        within = np.arange(n_real) - np.repeat(np.cumsum(counts) - counts, counts)
-        src_idx = np.repeat(ptr[rows], counts) + within
-        dst_idx = np.repeat(in_tap_ptr[:-1], counts) + within
-        tap_gid = gid[src_idx].astype(np.int64)
-        tap_tile = np.repeat(t_idx.astype(np.int64), counts)
-        key, inv = np.unique((tap_tile << 32) | tap_gid, return_inverse=True) if n_real else \
-            (np.zeros(0, np.int64), np.zeros(0, np.int64))
-        slot_tile = key >> 32
-        tile_slot_ptr = np.zeros(nt + 1, dtype=np.int64)
-        np.cumsum(np.bincount(slot_tile, minlength=nt), out=tile_slot_ptr[1:])
-        n_slots = np.diff(tile_slot_ptr)
-        local_slot = inv - tile_slot_ptr[tap_tile]
-        max_slots = int(n_slots.max()) if nt else 0
-        if max_slots >= (1 << 16) - 1:
-            raise ValueError("more than 65534 interpolation sources in one tile")
-        wtab, widx = np.unique(np.concatenate([w[src_idx], [0.0]]), return_inverse=True)
-        if len(wtab) > 1 << 16:
-            raise ValueError("more than 65536 distinct interpolation weights")
-        zero_w = int(widx[-1])
-        tap = np.zeros(max(int(in_tap_ptr[-1]), 4), dtype=np.uint32)
-        # padding taps: (tile's zero slot, weight 0)
-        pad_in = np.repeat(np.arange(n_in), padded - counts)
-        pad_pos = np.repeat(in_tap_ptr[:-1] + counts, padded - counts) + (
-            np.arange(int((padded - counts).sum())) - np.repeat(np.cumsum(padded - counts) - (padded - counts),
-                                                                padded - counts))
-        tap[pad_pos] = ((n_slots[t_idx[pad_in]].astype(np.uint32) << 16) | np.uint32(zero_w)).astype(np.uint32)
-        tap[dst_idx] = ((local_slot.astype(np.uint32) << 16) | widx[:-1].astype(np.uint32)).astype(np.uint32)
-        slot_gid = (key & 0xFFFFFFFF).astype(np.int32)
-        # LTS interface pairs: copies and slots whose source leaf steps with another
-        # cadence than the reading tile get the stage source the interface pass
-        # computes once per (node, reader cadence)
-        if_gid = np.zeros(0, np.int32)
-        if_cad = np.zeros(0, np.int32)
-        if lts:
-            tcad = leaf_cad[tiles].astype(np.int64)
-            ct, ce = np.nonzero(table >= 0)
-            cg = table[ct, ce].astype(np.int64)
-            cm = node_cad[cg].astype(np.int64) != tcad[ct]
-            s_cad = tcad[slot_tile] if len(slot_tile) else np.zeros(0, np.int64)
-            sm = node_cad[slot_gid].astype(np.int64) != s_cad if len(slot_gid) else np.zeros(0, bool)
-            keys = np.concatenate([((31 - tcad[ct[cm]]) << 32) | cg[cm],
-                                   ((31 - s_cad[sm]) << 32) | slot_gid[sm].astype(np.int64)])
-            if len(keys):
-                ukeys, pinv = np.unique(keys, return_inverse=True)
-                ne = int(cm.sum())
-                table[ct[cm], ce[cm]] = (_IFACE_BASE - pinv[:ne]).astype(np.int32)
-                slot_gid = slot_gid.copy()
-                slot_gid[sm] = (-pinv[ne:] - 1).astype(np.int32)
-                if_gid = (ukeys & 0xFFFFFFFF).astype(np.int32)
-                # reader cadence | source cadence << 8: the interface pass needs
-                # no dependent node-cadence lookup
-                if_cad = ((31 - (ukeys >> 32)) | (node_cad[if_gid].astype(np.int64) << 8)).astype(np.int32)
-        # per-tile metadata in launch order: {g0, g1, level | cadence<<8 | faces<<16, leaf}
-        starts, levels, a3 = td["starts"], td["level"], td["anchor3"]
-        L = td["max_depth"]
-        side = (1 << (L - levels[tiles].astype(np.int64)))
-        faces = np.zeros(nt, dtype=np.int64)
-        for d in range(dim):
-            faces |= (a3[tiles, d] == 0).astype(np.int64) << (2 * d)
-            faces |= ((a3[tiles, d] + side) == (1 << L)).astype(np.int64) << (2 * d + 1)
-        meta = np.stack([starts[tiles], starts[tiles + 1],
-                         levels[tiles] | (leaf_cad[tiles].astype(np.int64) << 8) | (faces << 16),
-                         tiles], axis=1).astype(np.int32)
-        pad = lambda a, dt: a.astype(dt) if len(a) else np.zeros(1, dt)  # noqa: E731
-        prog = dict(tile_slot_ptr=tile_slot_ptr, slot_gid=pad(slot_gid, np.int32),
-                    if_gid=pad(if_gid, np.int32), if_cad=pad(if_cad, np.int32), n_iface=len(if_gid),
-                    tile_in_ptr=tile_in_ptr, in_tap_ptr=in_tap_ptr, tile_tap_ptr=in_tap_ptr[tile_in_ptr],
-                    in_cell=pad(cross_cells[e_idx], np.uint16), tap=tap, wtab=wtab.astype(np.float64),
-                    tile_meta=meta, cross_cells=cross_cells.astype(np.uint16),
-                    cross_pos=cross_pos.astype(np.uint16), max_slots=max_slots)
-        return table, prog
-
-    # shared memory of one CTA of the persistent kernel (amr_stage_pipe.cuh, Pipe::smem_bytes)
-    @staticmethod
-    def _pipe_smem(dim: int, ppo: int, max_slots: int, max_head: int) -> int:
-        NS, NI = (ppo + 4) ** dim, ppo ** dim
-        r16 = lambda b: (b + 15) // 16 * 16  # noqa: E731
-        g = r16(NS * 8) + r16(NI * 8) + 2 * r16((max_slots + 1) * 8) + r16(NI * 4) + (16 + 64) * 4
-        return 64 + 64 * 8 + 3 * g + 2 * max_head
-
-    PIPE_SMEM_LIMIT = 113 * 1024  # two CTAs per SM (228 KB per SM, 1 KB reserved per CTA)
-
-    def _build_blobs(self, table, prog, n_iface, td, dim, ppo):
-        """Compact per-tile programs (tileprog.py) for the blob kernels, or None
-        (the int32-table kernel then runs).
-
-        AMR_KERNEL selects the stage kernel: 2 (default) one CTA per tile with
-        the blob front-end (bulk-copied head, cp.async copy runs); 1 the
-        persistent pipelined kernel (experimental); 0 the int32-table kernel.
-        A mesh that does not fit the compact encoding (or kernel 1's shared
-        memory) falls back to kernel 0.  Measured on cfg2 (round 1, LTS / GTS
-        G updates/s): kernel 2 23.9 / 25.9, kernel 0 20.4 / 25.5, kernel 1
-        15-21 / 14-20 (profiles/README.md)."""
-        import os
-
-        from . import tileprog
-
-        kernel = os.environ.get("AMR_KERNEL", "2")
-        if kernel not in ("1", "2"):
-            return None
-        try:
-            b = tileprog.build_blobs(table, prog, n_iface, td["starts"], td["anchor3"], ppo ** dim, ppo + 4)
-        except tileprog.BlobError:
-            return None
-        if kernel == "1" and self._pipe_smem(dim, ppo, prog["max_slots"], b["max_blob"]) > self.PIPE_SMEM_LIMIT:
-            return None
-        b["kernel"] = int(kernel)
-        b["cell_ent"] = tileprog.cell_entries(prog["cross_cells"], dim, ppo)
-        return b
-
     def _make_params(self) -> _native.AmrStageParams:
         m = self.mesh
         P = _native.AmrStageParams()
@@ -510,21 +301,16 @@ class Engine:
         P.lts = 1 if self.mode == "lts" or any(c != self.l_max for c in self.cadence) else 0
         P.n_stages = self.p
         P.nonlinear = self._nl
-        # L2 prefetch of the tile one wave of CTAs ahead (-1: one wave, 0: off)
-        P.prefetch_dist = int(os.environ.get("AMR_PREFETCH_DIST", "0"))
         P.n_nodes = m.n_nodes
         P.ld = self._ld
         d = self._d
-        P.kernel = self._kernel
         P.max_slots = self._max_slots
         P.if_gid, P.if_cad, P.ibuf = d["if_gid"].data_ptr(), d["if_cad"].data_ptr(), self._ibuf.data_ptr()
         P.n_iface_total = self._n_iface
         P.wtab, P.n_wtab = d["wtab"].data_ptr(), int(d["wtab"].numel())
-        if self._kernel == 3:
-            P.heads, P.max_blob, P.tail = d["heads"].data_ptr(), self._max_blob, d["tail"].data_ptr()
-            P.threads = self._threads
-        else:
-            self._table_params(P)
+        P.heads, P.max_head, P.tail = d["heads"].data_ptr(), self._max_head, d["tail"].data_ptr()
+        P.threads = self._threads
+        P.max_tail = self._max_tail
         P.U0, P.U1, P.K = self._U[0].data_ptr(), self._U[1].data_ptr(), self._K.data_ptr()
         P.Y = self._Y.data_ptr()
         for s in range(self.p):
@@ -551,28 +337,6 @@ class Engine:
         P.k_chi, P.k_phi, P.f0_chi, P.f0_phi = self.k_chi, self.k_phi, 0.0, 0.0
         fill_weights(P)
         return P
-
-    def _table_params(self, P) -> None:
-        d = self._d
-        P.tile_ids, P.tile_table = d["tiles"].data_ptr(), d["table"].data_ptr()
-        P.leaf_anchor, P.leaf_level = d["anchor"].data_ptr(), d["level"].data_ptr()
-        P.leaf_cadence, P.leaf_start = d["cadence"].data_ptr(), d["starts"].data_ptr()
-        P.node_cadence = d["node_cad"].data_ptr()
-        P.tile_slot_ptr, P.slot_gid = d["tile_slot_ptr"].data_ptr(), d["slot_gid"].data_ptr()
-        P.if_gid, P.if_cad, P.ibuf = d["if_gid"].data_ptr(), d["if_cad"].data_ptr(), self._ibuf.data_ptr()
-        P.n_iface_total = self._n_iface
-        P.tile_in_ptr, P.in_tap_ptr = d["tile_in_ptr"].data_ptr(), d["in_tap_ptr"].data_ptr()
-        P.tile_tap_ptr = d["tile_tap_ptr"].data_ptr()
-        P.in_cell, P.tile_meta, P.cross_cells = (d["in_cell"].data_ptr(), d["tile_meta"].data_ptr(),
-                                                 d["cross_cells"].data_ptr())
-        P.cross_pos = d["cross_pos"].data_ptr()
-        P.tap, P.wtab, P.n_wtab = d["tap"].data_ptr(), d["wtab"].data_ptr(), int(d["wtab"].numel())
-        P.max_slots = self._max_slots
-        P.kernel = self._kernel
-        if self._kernel:
-            P.blob, P.blob_off = d["blob"].data_ptr(), d["blob_off"].data_ptr()
-            P.blob_head, P.heads = d["blob_head"].data_ptr(), d["heads"].data_ptr()
-            P.cell_ent, P.max_blob = d["cell_ent"].data_ptr(), self._max_blob
 
     # -- plans (API parity; built lazily: they need every block's gather support) --
     @property

@@ -50,11 +50,14 @@ All numpy, vectorised over tiles; built once per mesh (Engine construction).
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 HDR_WORDS = 16        # int32 words in the header
 MAX_BASES = 63        # source groups per tile (6-bit base index)
 RUN_MAX = 8           # longest run
+ROW_STRIDE = 13       # box row stride in doubles (amr_common.cuh Tile::RS; AMR_RS overrides both, for experiments)
 BUCKET_LANES = (8, 4, 2, 1)
 
 
@@ -92,11 +95,23 @@ def cross_cells(dim: int, ppo: int, pad: int = 2) -> np.ndarray:
         within = np.where(others, within // ppo, within)
     sub[np.arange(len(r)), axis] = np.where(layer < pad, layer, ppo + layer)
     loc[h] = sub
-    NP = ppo + 2 * pad
+    strides = box_strides(dim, ppo)
     cell = np.zeros(E, dtype=np.int64)
     for d in range(dim):
-        cell = cell * NP + loc[:, d]
+        cell += loc[:, d] * strides[d]
     return cell
+
+
+def box_strides(dim: int, ppo: int, pad: int = 2) -> tuple:
+    """Strides of the shared-memory stencil box (the kernel's Tile::RS):
+    rows of the last axis padded to ROW_STRIDE doubles."""
+    NP = ppo + 2 * pad
+    rs = max(int(os.environ.get("AMR_RS", ROW_STRIDE)), NP)
+    return (NP * rs, rs, 1) if dim == 3 else (rs, 1)
+
+
+def box_cells(dim: int, ppo: int, pad: int = 2) -> int:
+    return (ppo + 2 * pad) ** (dim - 2) * box_strides(dim, ppo, pad)[-2] * (ppo + 2 * pad)
 
 
 def owned_cross(table: np.ndarray, g0: np.ndarray, g1: np.ndarray, faces: np.ndarray, dim: int,
@@ -105,8 +120,9 @@ def owned_cross(table: np.ndarray, g0: np.ndarray, g1: np.ndarray, faces: np.nda
     centred rows' +-1, +-2 along each axis, and at a physical face the biased
     rows' 6-point windows (wave.py:57-109; first-derivative rows read a subset)."""
     cells = cross_cells(dim, ppo)
-    NP, NI = ppo + 4, ppo ** dim
-    cell2e = np.full(NP ** dim, -1, dtype=np.int64)
+    NI = ppo ** dim
+    bs = box_strides(dim, ppo)
+    cell2e = np.full(box_cells(dim, ppo), -1, dtype=np.int64)
     cell2e[cells] = np.arange(len(cells))
     core = table[:, :NI]
     own = (core >= g0[:, None]) & (core < g1[:, None])
@@ -114,7 +130,7 @@ def owned_cross(table: np.ndarray, g0: np.ndarray, g1: np.ndarray, faces: np.nda
     need[:, :NI] = own
     k = np.arange(NI)
     for d in range(dim):
-        stride = NP ** (dim - 1 - d)
+        stride = bs[d]
         pos = (k // ppo ** (dim - 1 - d)) % ppo
         for o in (-2, -1, 1, 2):
             tgt = cell2e[cells[:NI] + o * stride]
@@ -156,7 +172,6 @@ def build_programs(td: dict, tiles: np.ndarray, leaf_cad: np.ndarray, node_cad: 
         faces |= ((a3[:, d] + side) == (1 << L)).astype(np.int64) << (2 * d + 1)
     need = owned_cross(table, g0, g1, faces, dim, ppo)
     cells = cross_cells(dim, ppo)
-    NP = ppo + 4
     tcad = leaf_cad[tiles].astype(np.int64)
 
     # ---- hanging rows (needed only), longest first within a tile
@@ -275,7 +290,7 @@ def build_programs(td: dict, tiles: np.ndarray, leaf_cad: np.ndarray, node_cad: 
     o = np.lexsort((rc, ct))
     rt, rc, rcode = ct[o], rc[o], e_code[o]
     brk = np.ones(len(rt), dtype=bool)
-    brk[1:] = ((rt[1:] != rt[:-1]) | (rc[1:] != rc[:-1] + 1) | (rc[1:] % NP == 0)
+    brk[1:] = ((rt[1:] != rt[:-1]) | (rc[1:] != rc[:-1] + 1) | (rc[1:] % box_strides(dim, ppo)[-2] == 0)
                | ((rcode[1:] >> 10) != (rcode[:-1] >> 10)) | ((rcode[1:] & 1023) != (rcode[:-1] & 1023) + 1))
     rid = np.cumsum(brk) - 1
     first = np.nonzero(brk)[0]
@@ -343,6 +358,7 @@ def build_programs(td: dict, tiles: np.ndarray, leaf_cad: np.ndarray, node_cad: 
         lt = np.arange(len(tap)) - tile_tap0[t_t]
         tail[(tail_start[t_t] + rows_b[t_t]) // 2 + lt] = tap.astype(np.uint16)
     return dict(heads=heads.view(np.uint8), tail=tail, max_head=max_head, max_slots=max_slots,
+                max_tail=int(tail_len.max()) if nt else 0,
                 if_gid=if_gid.astype(np.int32), if_cad=if_cad.astype(np.int32), n_iface=len(if_gid),
                 wtab=wtab.astype(np.float64), n_rows=n_in, n_cells=int(need.sum()))
 

@@ -43,3 +43,19 @@ def test_native_errors_map_to_valueerror():
         Mesh(uniform_tree(2, 2, 1), points_per_octant=6)
     with pytest.raises(ValueError):
         Mesh(uniform_tree(2, 2, 1), points_per_octant=5, pad=3)
+
+
+def test_stage_params_layout_matches_ctypes():
+    """The ctypes mirror of AmrStageParams has the compiled struct's size and
+    field offsets (a silent mismatch would feed the kernel garbage)."""
+    import ctypes
+
+    import numpy as np
+
+    out = np.zeros(64, dtype=np.int64)
+    n = _native.lib().amr_stage_params_layout(_native.ptr(out, ctypes.c_int64), 64)
+    assert n == 1 + len(_native.LAYOUT_FIELDS)
+    S = _native.AmrStageParams
+    assert out[0] == ctypes.sizeof(S)
+    for i, f in enumerate(_native.LAYOUT_FIELDS):
+        assert out[1 + i] == getattr(S, f).offset, f

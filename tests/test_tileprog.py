@@ -98,13 +98,13 @@ def test_needed_set_covers_every_stencil_read():
         faces |= ((a3[:, d] + side) == (1 << L)).astype(np.int64) << (2 * d + 1)
     need = TP.owned_cross(table, starts[:-1], starts[1:], faces, 2, ppo)
     cells = TP.cross_cells(2, ppo)
-    NP = ppo + 4
+    RS = TP.box_strides(2, ppo)[0]
     for t in tiles:
         have = set(cells[need[t]].tolist())
         for e in range(ppo * ppo):
             if not starts[t] <= table[t, e] < starts[t + 1]:
                 continue
-            pos = [cells[e] // NP - 2, cells[e] % NP - 2]
+            pos = [cells[e] // RS - 2, cells[e] % RS - 2]
             for d in range(2):
                 lo, hi = (faces[t] >> (2 * d)) & 1, (faces[t] >> (2 * d + 1)) & 1
                 p = pos[d]
@@ -117,4 +117,4 @@ def test_needed_set_covers_every_stencil_read():
                 for o in offs:
                     q = list(pos)
                     q[d] += o
-                    assert (q[0] + 2) * NP + q[1] + 2 in have, (t, e, d, o)
+                    assert (q[0] + 2) * RS + q[1] + 2 in have, (t, e, d, o)

@@ -9,7 +9,7 @@ UNIT = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msec
 
 
 def key_of(name: str) -> str:
-    m = re.search(r"(stage_blob|stage_pipe|stage_kernel|iface_kernel|gather_rows_kernel|block_rhs_kernel|pack_kernel)", name)
+    m = re.search(r"(stage_cross|iface_kernel|gather_rows_kernel|block_rhs_kernel|pack_kernel)", name)
     if m:
         k = m.group(1)
         if k.startswith("stage"):

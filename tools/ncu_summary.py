@@ -7,7 +7,7 @@ import sys
 
 def _is_lts(name: str) -> bool:
     """stage_{kernel,blob,pipe}<DIM, PPO, LTS, NT> as ncu prints it (demangled forms vary)."""
-    m = re.search(r"stage_(?:kernel|blob|pipe)<\(?\w*\)?(\d+), \(?\w*\)?(\d+), \(?\w*\)?(\w+)", name)
+    m = re.search(r"stage_(?:kernel|blob|pipe|cross)<\(?\w*\)?(\d+), \(?\w*\)?(\d+), \(?\w*\)?(\w+)", name)
     return bool(m) and m.group(3) in ("1", "true")
 
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",

@@ -10,7 +10,7 @@ import sys
 
 def _is_lts(name: str) -> bool:
     """stage_{kernel,blob,pipe}<DIM, PPO, LTS, NT> as ncu prints it (demangled forms vary)."""
-    m = re.search(r"stage_(?:kernel|blob|pipe)<\(?\w*\)?(\d+), \(?\w*\)?(\d+), \(?\w*\)?(\w+)", name)
+    m = re.search(r"stage_(?:kernel|blob|pipe|cross)<\(?\w*\)?(\d+), \(?\w*\)?(\d+), \(?\w*\)?(\w+)", name)
     return bool(m) and m.group(3) in ("1", "true")
 
 import numpy as np

@@ -3,7 +3,7 @@
 # Summaries land in gpurun_out/ (copy the ones to keep into profiles/).
 cd ${GRAFT_REPO_ROOT:-.}
 TAG=${1:-r1}
-K=${KREGEX:-stage_blob}
+K=${KREGEX:-stage_cross}
 bash tests/gpu_parity.sh > gpurun_out/parity_$TAG.log 2>&1; grep -E "passed|failed" gpurun_out/parity_$TAG.log | tail -3
 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_$TAG.log 2>&1; tail -1 gpurun_out/bench_$TAG.log | cut -c1-300
 python bench.py --steps 1 --warmup 1 --no-cpu > gpurun_out/bench_small_$TAG.log 2>&1 && \
