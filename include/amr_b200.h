@@ -86,6 +86,21 @@ int64_t amr_mesh_interp_nnz(const AmrMesh* m);
  * tensor-product Lagrange resolution (mesh.py:316-351) */
 int amr_mesh_interp_csr(const AmrMesh* m, int64_t* row_ptr, int32_t* gid, double* w);
 
+/* Per-tile stage programs (the native builder of paper_2011_10570_b200/
+ * tileprog.py, byte-identical to it): tiles = leaves in launch order,
+ * leaf_cad = each leaf's cadence (time level), lts = 1 to form LTS interface
+ * pairs, row_stride = the stencil box's row stride (Tile::RS).  info[9]:
+ * n_tiles, max_head, max_tail, max_slots, n_iface, n_wtab, tail uint16
+ * count, hanging rows, owned-cross cells.  fetch fills heads
+ * [n_tiles][max_head], tail, if_gid/if_cad [n_iface], wtab [n_wtab]. */
+typedef struct AmrProg AmrProg;
+AmrProg* amr_programs_build(const AmrMesh* m, int64_t n_tiles, const int32_t* tiles, const int32_t* leaf_cad,
+                            int lts, int row_stride, int n_threads);
+int amr_programs_info(const AmrProg* p, int64_t* info);
+int amr_programs_fetch(const AmrProg* p, uint8_t* heads, uint16_t* tail, int32_t* if_gid, int32_t* if_cad,
+                       double* wtab);
+void amr_programs_free(AmrProg* p);
+
 /* Public maximal blocks (decompose_blocks, mesh.py:87-135) */
 int64_t amr_mesh_n_blocks(const AmrMesh* m);
 int amr_mesh_blocks(const AmrMesh* m, int32_t* root_anchor, int32_t* root_level,

@@ -81,6 +81,10 @@ SIGNATURES = {
     "amr_mesh_interp_nnz": ([_vp], C.c_int64),
     "amr_mesh_interp_csr": ([_vp, _i64p, _i32p, _f64p], C.c_int),
     "amr_mesh_n_blocks": ([_vp], C.c_int64),
+    "amr_programs_build": ([_vp, C.c_int64, _i32p, _i32p, C.c_int, C.c_int, C.c_int], _vp),
+    "amr_programs_info": ([_vp, _i64p], C.c_int),
+    "amr_programs_fetch": ([_vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "amr_programs_free": ([_vp], None),
     "amr_mesh_blocks": ([_vp, _i32p, _i32p, _i32p, _i64p, _i32p], C.c_int),
     "amr_mesh_block_gather": ([_vp, C.c_int64, _i64p, _i64p, _i64p, _i64p, _f64p], C.c_int),
     "amr_stage": ([C.POINTER(AmrStageParams), _vp], C.c_int),

@@ -721,6 +721,26 @@ extern "C" AmrMesh* amr_mesh_build(int dim, int L, int ppo, int pad, int64_t n_l
 }
 
 extern "C" void amr_mesh_free(AmrMesh* m) { delete m; }
+
+// read-only views for the program builder (amr_programs.cpp)
+extern "C" int amr_mesh_view(const AmrMesh* m, int* dim, int* L, int* ppo, int64_t* n_leaves, int64_t* E,
+                             const int32_t** table, const int64_t** starts, const int32_t** anchor,
+                             const int32_t** level, const int64_t** iptr, const int32_t** igid, const double** iw) {
+  if (!m || m->table.empty()) return AMR_ESTATE;
+  *dim = m->dim;
+  *L = m->L;
+  *ppo = m->ppo;
+  *n_leaves = m->n_leaves;
+  *E = m->E;
+  *table = m->table.data();
+  *starts = m->starts.data();
+  *anchor = m->anchor.data();
+  *level = m->level.data();
+  *iptr = m->iptr.data();
+  *igid = m->igid.data();
+  *iw = m->iw.data();
+  return AMR_OK;
+}
 extern "C" int64_t amr_mesh_n_nodes(const AmrMesh* m) { return m ? m->n_nodes : -1; }
 
 extern "C" int amr_mesh_leaf_starts(const AmrMesh* m, int64_t* starts) {

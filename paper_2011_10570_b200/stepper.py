@@ -256,7 +256,7 @@ class Engine:
 
         from . import tileprog
 
-        prog = tileprog.build_programs(td, tiles, leaf_cad, node_cad, lts)
+        prog = tileprog.build_programs_native(self.mesh, tiles, leaf_cad, lts)  # == tileprog.build_programs
         tcad = leaf_cad[tiles]
         self._prefix = {c: int(np.sum(tcad >= c)) for c in range(self.l_max + 1)}
         n_iface = prog["n_iface"]

@@ -399,3 +399,36 @@ def decode(prog: dict, t: int) -> dict:
     b = [int(x) & 0xFFFF for x in h[11:13]] + [int(x) >> 16 for x in h[11:13]]
     return dict(g0=int(h[0]), n_own=int(h[1]), cells=cells, rows=rows,
                 buckets=(b[0], b[2], b[1], b[3]))
+
+
+def build_programs_native(mesh, tiles: np.ndarray, leaf_cad: np.ndarray, lts: bool, n_threads: int = 0) -> dict:
+    """build_programs through the native builder (csrc/amr_programs.cpp), from
+    the mesh's own leaf tables (no host copy of the n_leaves x E table); the
+    same dict, byte for byte (tests/test_programs_native.py)."""
+    import ctypes as C
+
+    from . import _native
+
+    L = _native.lib()
+    tiles = np.ascontiguousarray(tiles, dtype=np.int32)
+    cad = np.ascontiguousarray(leaf_cad, dtype=np.int32)
+    h = L.amr_programs_build(mesh._nm.h, len(tiles), _native.ptr(tiles, C.c_int32), _native.ptr(cad, C.c_int32),
+                             1 if lts else 0, box_strides(mesh.dim, mesh.ppo)[-2], n_threads)
+    if not h:
+        raise ProgramError(_native.last_error())
+    try:
+        info = np.zeros(9, dtype=np.int64)
+        L.amr_programs_info(h, _native.ptr(info, C.c_int64))
+        nt, max_head, max_tail, max_slots, n_iface, n_wtab, n_tail, n_rows, n_cells = (int(x) for x in info)
+        heads = np.empty((max(nt, 1), max_head), dtype=np.uint8)
+        tail = np.empty(n_tail, dtype=np.uint16)
+        if_gid = np.empty(max(n_iface, 1), dtype=np.int32)
+        if_cad = np.empty(max(n_iface, 1), dtype=np.int32)
+        wtab = np.empty(n_wtab, dtype=np.float64)
+        L.amr_programs_fetch(h, heads.ctypes.data, tail.ctypes.data, if_gid.ctypes.data, if_cad.ctypes.data,
+                             wtab.ctypes.data)
+    finally:
+        L.amr_programs_free(h)
+    return dict(heads=heads, tail=tail, max_head=max_head, max_slots=max_slots, max_tail=max_tail,
+                if_gid=if_gid[:n_iface], if_cad=if_cad[:n_iface], n_iface=n_iface, wtab=wtab, n_rows=n_rows,
+                n_cells=n_cells)

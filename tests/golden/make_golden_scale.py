@@ -106,7 +106,7 @@ def make_fields(names):
         an, lv = O.balance(c.dim, c.max_depth, an, lv)
         m = O.OracleMesh(c.dim, c.max_depth, an, lv, c.ppo, c.pad, c.domain_lo, c.domain_hi)
         print(name, "oracle mesh", len(lv), "leaves", m.n_nodes, "nodes", round(time.time() - t0, 1), "s", flush=True)
-        stride = max(1, m.n_nodes // 40000)
+        stride = max(1, m.n_nodes // 10000)
         data = {"n_nodes": np.int64(m.n_nodes), "n_leaves": np.int64(len(lv)), "stride": np.int64(stride),
                 "leaf_slices_sha": np.array(hashlib.sha256(
                     np.ascontiguousarray(m.leaf_slices, dtype=np.int64).tobytes()).hexdigest())}

@@ -1,0 +1,111 @@
+"""Parity at BASELINE scale, against committed goldens (no oracle run on the GPU box).
+
+* Trees (CPU): for cfg2..cfg5, the leaf keys and levels before and after 2:1
+  balance, and the R = 2, 4, 8 weighted partitions (LTS and GTS weights), equal
+  to the UNMODIFIED reference's ``construct`` / ``balance_2to1`` /
+  ``weighted_partition`` (octree.py:249-330, partition.py:20-91), stored as
+  digests by tests/golden/make_golden_scale.py.
+* Fields (GPU): the engine's zip field after one GTS step, one LTS coarse
+  round, a pre-boundary time and (cfg2) the final time T = 1.0 must be the C
+  oracle's bit for bit (sha256 of the bytes, -0 -> +0).  The oracle is pinned
+  to the reference in tests/test_oracle.py.  On a mismatch the relative L-inf
+  error on a strided sample is reported against the north_star tolerances
+  (<= 1e-12 after one step, <= 1e-10 at final time).
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, field_digest, rel_linf
+
+from paper_2011_10570_b200.configs import CONFIGS
+
+TREES = json.load(open(os.path.join(GOLDEN, "scale_trees.json")))
+
+
+def _tree_digest(anchors, levels):
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(anchors, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(levels, dtype=np.int64).tobytes())
+    return h.hexdigest()
+
+
+def _build_tree(name):
+    from paper_2011_10570_b200.octree import SfcOrdering, balance_2to1, construct
+
+    c = CONFIGS[name]
+    raw = construct(c.refine, c.dim, c.max_depth, SfcOrdering("morton", c.dim, c.max_depth))
+    return raw, balance_2to1(raw)
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4", "cfg5"])
+def test_trees_and_partitions_match_reference(name):
+    from paper_2011_10570_b200.partition import tree_weights, weighted_partition
+
+    want = TREES[name]
+    raw, bal = _build_tree(name)
+    for tag, tr in (("raw", raw), ("balanced", bal)):
+        a, lv = tr.arrays()
+        assert len(lv) == want[tag]["n"], tag
+        assert _tree_digest(a, lv) == want[tag]["sha"], tag
+    for mode in ("lts", "gts"):
+        w = tree_weights(bal, mode)
+        for R in (2, 4, 8):
+            pm = weighted_partition(bal, w, R)
+            assert [list(r) for r in pm.rank_ranges] == want["partitions"][f"{mode}{R}"], (mode, R)
+
+
+def _golden(name):
+    return np.load(os.path.join(GOLDEN, f"scale_{name}.npz"), allow_pickle=False)
+
+
+def _check(got, gd, key):
+    if field_digest(got) == str(gd[key + "__sha"]):
+        return
+    st = int(gd["stride"])
+    err = max(rel_linf(got[v, ::st], gd[key + "__sample"][v]) for v in range(2))
+    raise AssertionError(f"{key}: not bit-identical to the oracle (sampled relative L-inf {err:.3e})")
+
+
+def _mesh(name):
+    from helpers import config_mesh
+
+    return config_mesh(name)
+
+
+SNAP = {
+    "cfg2": [("gts", False, [1, 1024, 2048]), ("lts", False, [16, 1024, 2048]), ("lts-cubic", "cubic", [16])],
+    "cfg3": [("gts", None, [1]), ("lts", None, [32, 256])],
+    "cfg4": [("gts", None, [1]), ("lts", None, [1024])],
+    "cfg5": [("gts", None, [1]), ("lts", None, [4])],
+}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4", "cfg5"])
+def test_fields_match_oracle_at_scale(cuda, name):
+    from paper_2011_10570_b200.stepper import Engine
+
+    path = os.path.join(GOLDEN, f"scale_{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"no committed golden for {name}")
+    gd = _golden(name)
+    c = CONFIGS[name]
+    mesh = _mesh(name)
+    assert mesh.n_nodes == int(gd["n_nodes"])
+    assert hashlib.sha256(np.ascontiguousarray(mesh.leaf_slices, dtype=np.int64).tobytes()).hexdigest() == \
+        str(gd["leaf_slices_sha"])
+    for spec, nl, slices in SNAP[name]:
+        mode = spec.split("-")[0]
+        eng = Engine(mesh, tableau=c.tableau, cfl=c.cfl, mode=mode, nonlinear=c.nonlinear if nl is None else nl)
+        eng.initialize(c.chi0())
+        for s in slices:
+            if mode == "lts":
+                while eng.i_fine + eng.schedule.slices_per_round <= s:
+                    eng.lts_coarse_step()
+            eng.run_to(s)
+            _check(eng.current_zip(), gd, f"{spec}_{s}")
+        del eng
