@@ -295,7 +295,7 @@ def run_ours(args):
     _, per = time_rounds(eng, 1, torch, None if dist is None else dist, per_launch=True)
     counts = np.diff(mesh.leaf_starts)
     # algorithmic bytes per launch = 68 B x owned nodes of the launched tiles
-    tiles = eng._d["tiles"].cpu().numpy()
+    tiles = eng._rank_list[0].tiles
     cum = np.concatenate([[0], np.cumsum(counts[tiles])])
     k_ms = sum(m for m, _ in per)
     k_bytes = sum(BYTES_PER_UNIT * cum[n] for _, n in per)

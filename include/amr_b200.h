@@ -163,7 +163,11 @@ typedef struct {
   double* U0;                  /* [2][ld]: the reference's zip layout (chi row, phi row) */
   double* U1;
   double* K;                   /* [n_stages][2][ld] */
-  const AmrSliceCoef* coef;    /* LTS only (device) */
+  const AmrSliceCoef* coef;    /* LTS only (device): read by amr_iface */
+  /* LTS values the stage kernel reads, by value (copies of coef's entries for this slice and stage) */
+  uint32_t l_cur_mask;                 /* bit c: u_curr buffer of cadence c (coef->cur) */
+  double l_cnext[AMR_MAXL][AMR_MAXP];  /* coef->cstage[c][stage + 1][j] */
+  double l_comb[AMR_MAXL][AMR_MAXP];   /* coef->comb[c][j] */
   /* GTS coefficients */
   double g_cstage[AMR_MAXP][AMR_MAXP];
   double g_comb[AMR_MAXP];
@@ -216,15 +220,28 @@ int amr_block_rhs(int dim, int n, int pad, const double* y, double* out, double 
                   double k_chi, double k_phi, double f0_chi, double f0_phi,
                   const AmrStageParams* weights, void* stream);
 
-/* Ghost exchange pack/unpack of contiguous zip ranges (the byte-level
- * exchange of partition.py:182-207 / stepper.py:318-361): buf holds the
- * ranges back to back, each node `width` doubles. */
-int amr_pack_ranges(int64_t n_ranges, const int64_t* range_start, const int64_t* range_len,
-                    const int64_t* range_off, int width, const double* src, double* buf,
-                    int64_t total, void* stream);
-int amr_unpack_ranges(int64_t n_ranges, const int64_t* range_start, const int64_t* range_len,
-                      const int64_t* range_off, int width, const double* buf, double* dst,
-                      int64_t total, void* stream);
+/* Ghost-leaf records between ranks (Engine._ship, stepper.py:318-361;
+ * exchange, partition.py:182-207).  A shipment is a list of whole-leaf zip
+ * ranges, finest cadence first, so the leaves that stepped at a slice are a
+ * prefix (n_ranges, total).  pack writes buf[row * buf_ld + node]; unpack reads
+ * it back into the receiver's rows.  Each row has two base pointers: a range
+ * uses row1 when par[its cadence] is 1 (the two u buffers, selected per
+ * cadence by the step parity); K and Y rows pass the same pointer twice. */
+#define AMR_GHOST_ROWS 8
+typedef struct {
+  int64_t n_ranges;       /* ranges moved: a prefix of the list */
+  int64_t total;          /* zip nodes in that prefix */
+  const int64_t* start;   /* first node of each range in the rank's rows (device) */
+  const int64_t* off;     /* exclusive prefix sum of the range lengths (device) */
+  const int32_t* cad;     /* cadence of each range (device) */
+  int n_rows;             /* field rows moved per node (<= AMR_GHOST_ROWS) */
+  int64_t buf_ld;         /* row stride of buf in doubles; 0 = total (rows back to back) */
+  double* row0[AMR_GHOST_ROWS];
+  double* row1[AMR_GHOST_ROWS];
+  int32_t par[AMR_MAXL];  /* parity per cadence */
+} AmrGhostMove;
+int amr_ghost_pack(const AmrGhostMove* m, double* buf, void* stream);
+int amr_ghost_unpack(const AmrGhostMove* m, const double* buf, void* stream);
 
 /* -------------------------------------------------------------- wavelet -- */
 

@@ -46,6 +46,9 @@ class AmrStageParams(C.Structure):
         ("n_vt", C.c_int), ("vt_j", C.c_int * AMR_MAXP), ("Y", _vp),
         ("U0", _vp), ("U1", _vp), ("K", _vp),
         ("coef", _vp),
+        ("l_cur_mask", C.c_uint32),
+        ("l_cnext", (C.c_double * AMR_MAXP) * AMR_MAXL),
+        ("l_comb", (C.c_double * AMR_MAXP) * AMR_MAXL),
         ("g_cstage", (C.c_double * AMR_MAXP) * AMR_MAXP),
         ("g_comb", C.c_double * AMR_MAXP),
         ("max_depth", C.c_int),
@@ -58,6 +61,19 @@ class AmrStageParams(C.Structure):
         ("k_chi", C.c_double), ("k_phi", C.c_double), ("f0_chi", C.c_double), ("f0_phi", C.c_double),
         ("d2c", C.c_double * 5), ("d2e0", C.c_double * 6), ("d2e1", C.c_double * 6),
         ("d1c", C.c_double * 5), ("d1e0", C.c_double * 5), ("d1e1", C.c_double * 5),
+    ]
+
+
+AMR_GHOST_ROWS = 8
+
+
+class AmrGhostMove(C.Structure):
+    _fields_ = [
+        ("n_ranges", C.c_int64), ("total", C.c_int64),
+        ("start", _vp), ("off", _vp), ("cad", _vp),
+        ("n_rows", C.c_int), ("buf_ld", C.c_int64),
+        ("row0", _vp * AMR_GHOST_ROWS), ("row1", _vp * AMR_GHOST_ROWS),
+        ("par", C.c_int32 * AMR_MAXL),
     ]
 
 
@@ -94,8 +110,8 @@ SIGNATURES = {
     "amr_block_rhs": ([C.c_int, C.c_int, C.c_int, _vp, _vp, C.c_double, C.c_double, _vp, C.c_double,
                        C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
                        C.POINTER(AmrStageParams), _vp], C.c_int),
-    "amr_pack_ranges": ([C.c_int64, _vp, _vp, _vp, C.c_int, _vp, _vp, C.c_int64, _vp], C.c_int),
-    "amr_unpack_ranges": ([C.c_int64, _vp, _vp, _vp, C.c_int, _vp, _vp, C.c_int64, _vp], C.c_int),
+    "amr_ghost_pack": ([C.POINTER(AmrGhostMove), _vp, _vp], C.c_int),
+    "amr_ghost_unpack": ([C.POINTER(AmrGhostMove), _vp, _vp], C.c_int),
     "amr_wavelet_coeff": ([C.c_int, C.c_int, C.c_int64, _vp, _vp, _vp, C.c_int, C.c_double, C.c_double,
                            C.c_int, C.c_int, _vp, _vp, _vp], C.c_int),
 }

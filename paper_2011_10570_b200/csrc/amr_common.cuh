@@ -117,6 +117,35 @@ __device__ __forceinline__ double2 lts_source(const double* __restrict__ U0, con
   return y;
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// before the previous kernel on the stream has finished and must call
+// griddepcontrol.wait before touching that kernel's output.  AMR_PDL=0 turns
+// it off (plain stream order).
+inline bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = std::getenv("AMR_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+template <class Kern, class Params>
+int pdl_launch(Kern kern, dim3 grid, dim3 block, size_t dyn, cudaStream_t st, const Params& p) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
+  return e == cudaSuccess ? AMR_OK : cuda_fail(e, "cudaLaunchKernelEx");
+}
+
 // --------------------------------------------------------------------------
 // RHS at one interior point (wave.py:57-201), generic over the data accessor
 // --------------------------------------------------------------------------

@@ -31,10 +31,12 @@ namespace {
 // stage kernel reads it like a copy.  Pairs are sorted finest reader first:
 // the eligible readers of a slice are a prefix.
 __global__ void __launch_bounds__(256) iface_kernel(const AmrStageParams P) {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the stage kernel may fetch its tile heads meanwhile
   const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
   if (i >= P.n_iface) return;
   const int g = __ldg(P.if_gid + i);
   const int cc = __ldg(P.if_cad + i);  // reader cadence | source cadence << 8 (no dependent lookup)
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");              // the fields are the previous stage kernel's output
   const double2 v = lts_source(P.U0, P.U1, P.K, P.ld, P.n_stages, g, P.stage, cc & 0xFF, cc >> 8, P.coef);
   P.ibuf[i] = v.x;
   P.ibuf[P.n_iface_total + i] = v.y;
@@ -99,22 +101,30 @@ __global__ void block_rhs_kernel(int n, int pad, const double* __restrict__ y, d
   out[total + t] = v.y;
 }
 
-__global__ void pack_kernel(int64_t n_ranges, const int64_t* __restrict__ start,
-                            const int64_t* __restrict__ len, const int64_t* __restrict__ off, int width,
-                            const double* __restrict__ src, double* __restrict__ buf, int64_t total,
-                            bool unpack) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= total) return;
-  int64_t node = t / width, c = t % width;
-  // binary search the range holding `node` (off = exclusive prefix of len)
-  int64_t lo = 0, hi = n_ranges - 1;
+// Ghost records between ranks: whole-leaf zip ranges <-> one packed buffer
+// buf[row][node].  One thread per packed node; its range by binary search in
+// the exclusive prefix `off`.  A range's rows come from the parity-0 or the
+// parity-1 base pointers according to its cadence (the u buffers; K and Y rows
+// pass the same pointer twice).
+template <bool UNPACK>
+__global__ void __launch_bounds__(256) ghost_move_kernel(const AmrGhostMove M, double* __restrict__ buf) {
+  const int64_t node = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (node >= M.total) return;
+  int64_t lo = 0, hi = M.n_ranges - 1;
   while (lo < hi) {
-    int64_t mid = (lo + hi + 1) >> 1;
-    if (off[mid] <= node) lo = mid; else hi = mid - 1;
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (__ldg(M.off + mid) <= node) lo = mid; else hi = mid - 1;
   }
-  int64_t g = start[lo] + (node - off[lo]);
-  if (!unpack) buf[t] = src[g * width + c];
-  else const_cast<double*>(src)[g * width + c] = buf[t];
+  const int64_t g = __ldg(M.start + lo) + (node - __ldg(M.off + lo));
+  const int par = M.par[__ldg(M.cad + lo) & (AMR_MAXL - 1)];
+  const int64_t bld = M.buf_ld > 0 ? M.buf_ld : M.total;
+#pragma unroll
+  for (int r = 0; r < AMR_GHOST_ROWS; ++r) {
+    if (r >= M.n_rows) break;
+    double* row = par ? M.row1[r] : M.row0[r];
+    if (UNPACK) row[g] = buf[(int64_t)r * bld + node];
+    else buf[(int64_t)r * bld + node] = row[g];
+  }
 }
 
 }  // namespace
@@ -163,9 +173,7 @@ extern "C" int amr_stage_params_layout(int64_t* out, int cap) {
 
 extern "C" int amr_iface(const AmrStageParams* p, void* stream) {
   if (p->n_iface <= 0) return AMR_OK;
-  iface_kernel<<<(unsigned)((p->n_iface + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*p);
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? AMR_OK : cuda_fail(e, "amr_iface launch");
+  return pdl_launch(iface_kernel, dim3((unsigned)((p->n_iface + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, *p);
 }
 
 extern "C" int amr_gather_rows(int64_t n_rows, const int64_t* row_ptr, const int64_t* col, const double* val,
@@ -211,24 +219,22 @@ extern "C" int amr_block_rhs(int dim, int n, int pad, const double* y, double* o
   return e == cudaSuccess ? AMR_OK : cuda_fail(e, "amr_block_rhs launch");
 }
 
-extern "C" int amr_pack_ranges(int64_t n_ranges, const int64_t* range_start, const int64_t* range_len,
-                               const int64_t* range_off, int width, const double* src, double* buf,
-                               int64_t total, void* stream) {
-  if (total <= 0) return AMR_OK;
-  unsigned blocks = (unsigned)((total * width + 255) / 256);
-  pack_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n_ranges, range_start, range_len, range_off, width,
-                                                        src, buf, total * width, false);
+static int ghost_move(const AmrGhostMove* m, double* buf, void* stream, bool unpack) {
+  if (m->total <= 0 || m->n_ranges <= 0 || m->n_rows <= 0) return AMR_OK;
+  if (m->n_rows > AMR_GHOST_ROWS) return AMR_EINVAL;
+  const unsigned blocks = (unsigned)((m->total + 255) / 256);
+  if (unpack)
+    ghost_move_kernel<true><<<blocks, 256, 0, (cudaStream_t)stream>>>(*m, buf);
+  else
+    ghost_move_kernel<false><<<blocks, 256, 0, (cudaStream_t)stream>>>(*m, buf);
   cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? AMR_OK : cuda_fail(e, "amr_pack_ranges launch");
+  return e == cudaSuccess ? AMR_OK : cuda_fail(e, unpack ? "amr_ghost_unpack launch" : "amr_ghost_pack launch");
 }
 
-extern "C" int amr_unpack_ranges(int64_t n_ranges, const int64_t* range_start, const int64_t* range_len,
-                                 const int64_t* range_off, int width, const double* buf, double* dst,
-                                 int64_t total, void* stream) {
-  if (total <= 0) return AMR_OK;
-  unsigned blocks = (unsigned)((total * width + 255) / 256);
-  pack_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(n_ranges, range_start, range_len, range_off, width,
-                                                        dst, const_cast<double*>(buf), total * width, true);
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? AMR_OK : cuda_fail(e, "amr_unpack_ranges launch");
+extern "C" int amr_ghost_pack(const AmrGhostMove* m, double* buf, void* stream) {
+  return ghost_move(m, buf, stream, false);
+}
+
+extern "C" int amr_ghost_unpack(const AmrGhostMove* m, const double* buf, void* stream) {
+  return ghost_move(m, const_cast<double*>(buf), stream, true);
 }

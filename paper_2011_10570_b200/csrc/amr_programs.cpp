@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -129,6 +130,9 @@ extern "C" AmrProg* amr_programs_build(const AmrMesh* mesh, int64_t n_tiles, con
   std::vector<std::vector<double>> w_t(nth);
   std::vector<std::vector<uint8_t>> need_all(n_tiles);
   int err = 0;
+  // AMR_MAX_BASES lowers the source-group limit (tests of the refusal path)
+  const char* mb_env = std::getenv("AMR_MAX_BASES");
+  const int max_bases = mb_env ? std::min(MAX_BASES, std::max(1, std::atoi(mb_env))) : MAX_BASES;
 #pragma omp parallel num_threads(nth) reduction(| : err)
   {
     const int tid = omp_get_thread_num();
@@ -283,7 +287,7 @@ extern "C" AmrProg* amr_programs_build(const AmrMesh* mesh, int64_t n_tiles, con
     for (auto& s : sslot) bases.push_back(s.first);
     std::sort(bases.begin(), bases.end());
     bases.erase(std::unique(bases.begin(), bases.end()), bases.end());
-    if ((int64_t)bases.size() > MAX_BASES) {
+    if ((int64_t)bases.size() > max_bases) {
       err |= 2;
       continue;
     }

@@ -178,7 +178,7 @@ __device__ __forceinline__ TileCtx tile_ctx(const AmrStageParams& P, const unsig
   c.faces = (lmeta >> 16) & 0x3F;
   c.tl = P.tail + (int64_t)c.h[14] * 8;
   c.taps_off = c.h[15];
-  const int cur = lts ? P.coef->cur[c.cad] : P.gts_cur;
+  const int cur = lts ? (int)((P.l_cur_mask >> c.cad) & 1u) : P.gts_cur;
   c.Ucur = cur ? P.U1 : P.U0;
   c.Unew = cur ? P.U0 : P.U1;
   c.V = (P.stage == 0) ? c.Ucur : P.Y + (int64_t)(P.stage & 1) * 2 * P.ld;
@@ -221,7 +221,6 @@ __device__ __forceinline__ void tile_epilogue(const AmrStageParams& P, const Til
   const int64_t n = P.ld;
   const int s = P.stage;
   const bool last = (s == P.n_stages - 1);
-  const AmrSliceCoef* C = P.coef;
   const int64_t g = c.g0 + k;
   double* Ks = P.K + (int64_t)s * 2 * n;
   if (!last || LTS) {
@@ -233,7 +232,7 @@ __device__ __forceinline__ void tile_epilogue(const AmrStageParams& P, const Til
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const int jv = P.vt_j[t];
-      const double cf = LTS ? C->cstage[c.cad][s + 1][jv] : P.g_cstage[s + 1][jv];
+      const double cf = LTS ? P.l_cnext[c.cad][jv] : P.g_cstage[s + 1][jv];
       const double kx = (jv == s) ? ks.x : __ldg(P.K + (int64_t)jv * 2 * n + g);
       const double ky = (jv == s) ? ks.y : __ldg(P.K + (int64_t)jv * 2 * n + n + g);
       yx = yx + cf * kx;
@@ -259,7 +258,7 @@ __device__ __forceinline__ void tile_epilogue(const AmrStageParams& P, const Til
 #pragma unroll
     for (int jj = 0; jj < AMR_MAXP; ++jj) {
       if (jj >= P.n_stages) break;
-      const double cf = LTS ? C->comb[c.cad][jj] : P.g_comb[jj];
+      const double cf = LTS ? P.l_comb[c.cad][jj] : P.g_comb[jj];
       if (cf == 0.0) continue;
       ux = ux + cf * kx[jj];
       uy = uy + cf * ky[jj];
@@ -425,6 +424,9 @@ __global__ void __launch_bounds__(NTH, (NTH <= 128 ? 2 * AMR_CROSS_MINB : AMR_CR
   uint16_t* own = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(slot) + CK::slot_bytes(P.max_slots));
   const int tid = threadIdx.x;
   AMR_PROBE(0);
+  // programmatic dependent launch: the next kernel on the stream may start its
+  // CTAs (and fetch its static tables) while this grid drains
+  pdl_launch_dependents();
 
   // ---- 1: the head (one bulk copy at a fixed stride), weights meanwhile
   if (tid == 0) {
@@ -439,6 +441,9 @@ __global__ void __launch_bounds__(NTH, (NTH <= 128 ? 2 * AMR_CROSS_MINB : AMR_CR
   for (int i = tid; i < P.n_wtab; i += NTH) cp_async8(s_w + i, P.wtab + i);
   __syncthreads();  // mbarrier initialised before anyone waits on it
   mbar_wait(bar, 0);
+  // everything above reads static tables only; the fields (and the interface
+  // buffer) are the previous kernels' output
+  pdl_wait();
   AMR_PROBE(1);
   const TileCtx c = tile_ctx(P, head, LTS);
   const uint32_t tail_bytes = (uint32_t)c.h[7];

@@ -24,8 +24,7 @@ int launch_cross_one(const AmrStageParams* p, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(stage_cross)");
     configured[dev] = dyn;
   }
-  stage_cross<DIM, PPO, LTS, NT, NTH><<<(unsigned)p->n_tiles, NTH, dyn, st>>>(*p);
-  return AMR_OK;
+  return pdl_launch(stage_cross<DIM, PPO, LTS, NT, NTH>, dim3((unsigned)p->n_tiles), dim3(NTH), dyn, st, *p);
 }
 
 template <int DIM, int PPO, bool LTS, int NTH>

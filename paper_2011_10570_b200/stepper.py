@@ -16,11 +16,17 @@ B200 design:
 * each stage is one launch of the fused unzip + time-interpolation + RHS +
   zip kernel (``amr_stage``); the last stage also does the RK combine;
 * per-slice LTS coefficients (transfer matrices, parities, dt products) are
-  computed once per slice phase on the host and kept on the device.
-* multi-GPU: one process per GPU, contiguous weighted-Morton leaf ranges,
-  every rank holds the full zip layout (180 GB HBM makes that cheap), and the
-  ghost leaves of the reference's exchange plan move over NCCL after every
-  stage (``GhostExchange``), exactly where the reference calls ``_ship``.
+  computed once per slice phase on the host and kept on the device;
+* ranks: a partitioned mesh (``mesh.pmap.ranks > 1``) runs as R ranks, each
+  holding only its owned leaves plus the ghost leaves its tiles read
+  (``_Rank``).  Without a process group the R ranks are simulated in this
+  process on one device (the reference's ``rank_records``, stepper.py:158-161)
+  and ghosts move by device copies; under ``torch.distributed`` each process
+  owns one rank and the same packed shipments move over NCCL.  Either way the
+  shipments happen exactly where the reference calls ``_ship``
+  (stepper.py:430,455): after every stage and after the step, for the leaves
+  that stepped.  A rank launches the tiles other ranks read first, so the
+  shipment overlaps its interior tiles.
 """
 from __future__ import annotations
 
@@ -148,15 +154,471 @@ def _pow2_exact(x: float) -> bool:
     return x > 0 and m == 0.5
 
 
+def _source_leaves(prog: dict, starts: np.ndarray, tile_leaves: np.ndarray) -> np.ndarray:
+    """Sorted leaves whose zip nodes the programs read (their own tiles included):
+    the positive source bases of every head, and the source nodes of the
+    interface pairs."""
+    heads = prog["heads"]
+    h32 = heads.view(np.int32).reshape(heads.shape[0], -1)
+    nt = len(tile_leaves)
+    out = [np.asarray(tile_leaves, dtype=np.int64)]
+    if nt:
+        W = min(63, h32.shape[1] - 16)
+        bases = h32[:nt, 16:16 + W]
+        valid = (np.arange(W)[None, :] < h32[:nt, 6][:, None]) & (bases >= 0)
+        out.append(np.searchsorted(starts, np.unique(bases[valid]).astype(np.int64), side="right") - 1)
+    if prog["n_iface"]:
+        out.append(np.searchsorted(starts, np.unique(prog["if_gid"]).astype(np.int64), side="right") - 1)
+    return np.unique(np.concatenate(out))
+
+
+class _Rank:
+    """One rank's share of the mesh on a device: its tiles' stage programs, the
+    zip rows of its owned leaves and of the ghost leaves those tiles read
+    (owned + ghosts in leaf order, so a leaf is one contiguous range), and the
+    launches of one RK stage."""
+
+    def __init__(self, mesh: Mesh, leaf_cad: np.ndarray, lts_kernel: bool, l_max: int, rank: int, owned: np.ndarray):
+        self.mesh, self.cad, self.l_max = mesh, leaf_cad, l_max
+        self.rank = rank
+        self.owned = np.asarray(owned, dtype=np.int64)
+        cad = leaf_cad
+        order = np.lexsort((self.owned, -cad[self.owned]))
+        self.tiles = self.owned[order]  # cadence order; reordered by layout()
+        from . import tileprog
+
+        if len(self.tiles):
+            self.prog = tileprog.build_programs_native(mesh, self.tiles.astype(np.int32), cad, lts_kernel)
+        else:  # an empty rank (more ranks than the weights can split)
+            self.prog = dict(heads=np.zeros((1, 64), np.uint8), tail=np.zeros(8, np.uint16), max_head=64,
+                             max_slots=0, max_tail=0, if_gid=np.zeros(0, np.int32), if_cad=np.zeros(0, np.int32),
+                             n_iface=0, wtab=np.zeros(1), n_rows=0, n_cells=0)
+        self.src_leaves = _source_leaves(self.prog, mesh.leaf_starts, self.tiles)
+        own_mask = np.zeros(len(cad) + 1, dtype=bool)
+        own_mask[self.owned] = True
+        self.ghosts = self.src_leaves[~own_mask[self.src_leaves]]
+
+    # -- layout ---------------------------------------------------------------------
+    def layout(self, boundary_leaves: np.ndarray) -> None:
+        """Host side: fix the launch order (tiles other ranks read first, each
+        part finest cadence first) and the local node layout (owned + ghost
+        leaves in leaf order), and rewrite the programs' node ids to it."""
+        mesh = self.mesh
+        cad = self.cad
+        starts = mesh.leaf_starts
+        n_leaves = len(cad)
+        prog = self.prog
+        # launch order: [boundary | interior], each finest cadence first
+        is_b = np.zeros(n_leaves, dtype=bool)
+        is_b[np.asarray(boundary_leaves, dtype=np.int64)] = True
+        tb = is_b[self.tiles]
+        perm = np.lexsort((self.tiles, -cad[self.tiles], ~tb))
+        self.tiles = self.tiles[perm]
+        heads = prog["heads"][: len(perm)][perm] if len(perm) else prog["heads"]
+        tcad = cad[self.tiles]
+        tb = tb[perm]
+        self.n_boundary = int(tb.sum())
+        levels = range(self.l_max + 2)
+        self.prefix_b = [int(np.sum(tcad[tb] >= c)) for c in levels]
+        self.prefix_i = [int(np.sum(tcad[~tb] >= c)) for c in levels]
+        n_iface = prog["n_iface"]
+        self.n_iface = n_iface
+        self.if_prefix = [int(np.sum((prog["if_cad"][:n_iface] & 0xFF) >= c)) for c in levels]
+        # local layout: owned + ghost leaves in leaf order
+        self.local_leaves = np.union1d(self.owned, self.ghosts)
+        counts = (starts[1:] - starts[:-1])[self.local_leaves]
+        lstart = np.zeros(len(self.local_leaves) + 1, dtype=np.int64)
+        np.cumsum(counts, out=lstart[1:])
+        self.n_local = int(lstart[-1])
+        if self.n_local >= 2 ** 31 - 2:
+            raise ValueError("a rank holds more than 2^31 zip nodes; partition the mesh over more ranks")
+        self.leaf_lstart = np.full(n_leaves, -1, dtype=np.int64)
+        self.leaf_lstart[self.local_leaves] = lstart[:-1]
+        self.identity = self.n_local == mesh.n_nodes and len(self.local_leaves) == n_leaves
+        if_gid = prog["if_gid"]
+        if not self.identity:
+            heads = np.ascontiguousarray(heads)
+            h32 = heads.view(np.int32).reshape(heads.shape[0], -1)
+            nt = len(self.tiles)
+            if nt:
+                h32[:nt, 0] = self.leaf_lstart[self.tiles]
+                W = min(63, h32.shape[1] - 16)
+                bases = h32[:nt, 16:16 + W]
+                valid = (np.arange(W)[None, :] < h32[:nt, 6][:, None]) & (bases >= 0)
+                old = bases[valid].astype(np.int64)
+                lf = np.searchsorted(starts, old, side="right") - 1
+                new = self.leaf_lstart[lf]
+                if np.any(starts[lf] != old) or np.any(new < 0):
+                    raise RuntimeError("stage programs read a leaf outside the rank's layout")
+                bases[valid] = new.astype(np.int32)
+            if n_iface:
+                g = if_gid[:n_iface].astype(np.int64)
+                lf = np.searchsorted(starts, g, side="right") - 1
+                if_gid = (self.leaf_lstart[lf] + (g - starts[lf])).astype(np.int32)
+            # local node -> global gid (load_zip)
+            self.l2g = np.repeat(starts[self.local_leaves] - lstart[:-1], counts) + np.arange(self.n_local)
+        else:
+            self.l2g = None
+        a, b = (int(self.owned[0]), int(self.owned[-1]) + 1) if len(self.owned) else (0, 0)
+        self.own_g0, self.own_g1 = int(starts[a]), int(starts[b])  # owned gids (global), contiguous
+        self.own_l0 = int(self.leaf_lstart[a]) if len(self.owned) else 0
+        self.host = dict(heads=heads, tail=prog["tail"], wtab=prog["wtab"], if_gid=if_gid, if_cad=prog["if_cad"])
+        self.max_head, self.max_tail, self.max_slots = prog["max_head"], prog["max_tail"], prog["max_slots"]
+        self.stats = dict(n_rows=prog["n_rows"], n_cells=prog["n_cells"])
+        self.prog = None
+        # the owned leaves as ranges of equal cadence (current_zip)
+        oc = cad[self.owned]
+        first = np.concatenate([[0], np.flatnonzero(np.diff(oc)) + 1]).astype(np.int64) if len(oc) else \
+            np.zeros(0, np.int64)
+        r_start = self.leaf_lstart[self.owned[first]] if len(oc) else np.zeros(0, np.int64)
+        r_end = np.append(r_start[1:], self.own_l0 + (self.own_g1 - self.own_g0)) if len(oc) else r_start
+        self.own_ranges_host = (r_start, r_end - r_start, oc[first] if len(oc) else np.zeros(0, np.int64))
+
+    def upload(self, eng: "Engine") -> None:
+        """Device side: programs, zip rows (u0, u1, K, Y), interface buffer."""
+        import torch
+
+        self.eng = eng
+        dev = eng.device
+        T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+        pad = lambda x: x if len(x) else np.zeros(1, x.dtype)  # noqa: E731
+        h = self.host
+        self.d = dict(heads=T(h["heads"]), tail=T(h["tail"]), wtab=T(h["wtab"]), if_gid=T(pad(h["if_gid"])),
+                      if_cad=T(pad(h["if_cad"])))
+        self.host = None
+        n_iface = self.n_iface
+        n = self.n_local
+        # rows padded to an even stride ld > n (16-byte aligned rows; the kernel
+        # bulk-prefetches 16-byte aligned supersets of a tile's owned range)
+        self.ld = ld = (n + 2) // 2 * 2
+        p = eng.p
+        self.U_store = [torch.zeros((2, ld), dtype=torch.float64, device=dev) for _ in range(2)]
+        self.K_store = torch.zeros((p, 2, ld), dtype=torch.float64, device=dev)
+        self.Y_store = torch.zeros((2, 2, ld), dtype=torch.float64, device=dev)  # by stage parity
+        self.U = [u[:, :n] for u in self.U_store]
+        self.K = self.K_store[:, :, :n]
+        self.Y = self.Y_store[:, :, :n]
+        self.ibuf = torch.zeros((2, max(n_iface, 1)), dtype=torch.float64, device=dev)
+        self.prm = self._make_params()
+        self.own_ranges = _Ranges(*self.own_ranges_host, dev)
+
+    def _make_params(self) -> _native.AmrStageParams:
+        eng = self.eng
+        m = eng.mesh
+        P = _native.AmrStageParams()
+        P.dim, P.ppo, P.pad = m.dim, m.ppo, m.pad
+        P.lts = 1 if eng._lts_kernel else 0
+        P.n_stages = eng.p
+        P.nonlinear = eng._nl
+        P.n_nodes = self.n_local
+        P.ld = self.ld
+        d = self.d
+        P.max_slots = self.max_slots
+        P.if_gid, P.if_cad, P.ibuf = d["if_gid"].data_ptr(), d["if_cad"].data_ptr(), self.ibuf.data_ptr()
+        P.n_iface_total = self.n_iface
+        P.wtab, P.n_wtab = d["wtab"].data_ptr(), int(d["wtab"].numel())
+        P.heads, P.max_head, P.tail = d["heads"].data_ptr(), self.max_head, d["tail"].data_ptr()
+        P.threads = eng._threads
+        P.max_tail = self.max_tail
+        P.U0, P.U1, P.K = self.U_store[0].data_ptr(), self.U_store[1].data_ptr(), self.K_store.data_ptr()
+        P.Y = self.Y_store.data_ptr()
+        tab = eng.tab
+        for s in range(eng.p):
+            for j in range(eng.p):
+                a = tab.a[s][j]
+                P.g_cstage[s][j] = eng.dt_fine * a if (j < s and a != 0.0) else 0.0
+            w = tab.w[s]
+            P.g_comb[s] = (1 * eng.dt_fine) * w if w != 0.0 else 0.0
+        P.max_depth = m.L
+        P.top_nodes = m.top_nodes
+        for dd in range(m.dim):
+            P.lo[dd] = m.domain.lo[dd]
+            P.extent[dd] = m.domain.extent(dd)
+        for lvl in range(_native.AMR_MAXL):
+            if lvl > m.L:
+                continue
+            h = m.level_spacing(lvl)
+            h2 = h ** 2
+            P.h[lvl], P.h2[lvl] = h, h2
+            P.h2_pow2[lvl] = 1 if _pow2_exact(h2) else 0
+            P.inv_h2[lvl] = 1.0 / h2 if P.h2_pow2[lvl] else 0.0
+        P.r_eps = eng._r_eps
+        P.r_eps2 = eng._r_eps ** 2
+        P.k_chi, P.k_phi, P.f0_chi, P.f0_phi = eng.k_chi, eng.k_phi, 0.0, 0.0
+        fill_weights(P)
+        self.heads_ptr = d["heads"].data_ptr()
+        return P
+
+    # -- launches ---------------------------------------------------------------------
+    def begin_stage(self, i: int, s: int, cmin: int) -> None:
+        """Stage parameters of (slice i, stage s) and the LTS interface pass."""
+        eng = self.eng
+        P = self.prm
+        if P.lts:
+            P.coef = eng._slice_coef(i).data_ptr()
+            R = eng.schedule.slices_per_round
+            mask, cstage, comb = eng._coef_host[(i % R, (i // R) & 1)]
+            P.l_cur_mask = mask
+            for c, rows in cstage.items():
+                for j in range(eng.p):
+                    P.l_cnext[c][j] = rows[s + 1][j] if s + 1 < eng.p else 0.0
+                    P.l_comb[c][j] = comb[c][j]
+        else:
+            P.gts_cur = i & 1
+        P.stage = s
+        vt = eng._vt[s + 1] if s + 1 < eng.p else []  # the writer forms stage s+1's sources
+        P.n_vt = len(vt)
+        for t, j in enumerate(vt):
+            P.vt_j[t] = j
+        P.n_iface = self.if_prefix[cmin]
+        if P.n_iface and (self.prefix_b[cmin] or self.prefix_i[cmin]):
+            with eng._phase("time_interp"):
+                rc = eng._lib.amr_iface(C.byref(P), eng._stream())
+            if rc:
+                _native.check(rc, "amr_iface")
+
+    def launch_tiles(self, cmin: int, boundary: bool) -> None:
+        P = self.prm
+        n = self.prefix_b[cmin] if boundary else self.prefix_i[cmin]
+        if not n:
+            return
+        P.n_tiles = n
+        P.heads = self.heads_ptr + (0 if boundary else self.n_boundary * self.max_head)
+        with self.eng._phase("rhs"):
+            rc = self.eng._lib.amr_stage(C.byref(P), self.eng._stream())
+        if rc:
+            _native.check(rc, "amr_stage")
+
+    # -- state I/O ----------------------------------------------------------------------
+    def load(self, zd) -> None:
+        """u_pre = u_curr = the rank's nodes of the global device field zd, K = 0."""
+        import torch
+
+        if self.identity:
+            self.U[0].copy_(zd, non_blocking=True)
+        else:
+            if not hasattr(self, "_l2g_d"):
+                self._l2g_d = torch.from_numpy(self.l2g).to(self.eng.device)
+            self.U[0].copy_(zd.index_select(1, self._l2g_d))
+        self.U[1].copy_(self.U[0])
+        self.K.zero_()
+
+    def shipment_rows(self, s: int, i: int):
+        """(row0, row1, parity per cadence) of the record fields that changed in
+        stage s of slice i: K_s (LTS interface readers need it), and the next
+        stage's verbatim source or, after the last stage, the new u."""
+        eng = self.eng
+        ld = self.ld
+        rows0, rows1 = [], []
+        if self.prm.lts:
+            k = self.K_store.data_ptr() + s * 2 * ld * 8
+            rows0 += [k, k + ld * 8]
+            rows1 += [k, k + ld * 8]
+        par = [0] * _native.AMR_MAXL
+        if s + 1 < eng.p:
+            y = self.Y_store.data_ptr() + ((s + 1) & 1) * 2 * ld * 8
+            rows0 += [y, y + ld * 8]
+            rows1 += [y, y + ld * 8]
+        else:
+            u0, u1 = self.U_store[0].data_ptr(), self.U_store[1].data_ptr()
+            rows0 += [u0, u0 + ld * 8]
+            rows1 += [u1, u1 + ld * 8]
+            for c in range(eng.l_max + 1):  # each cadence wrote the buffer of its new parity
+                par[c] = eng._cur_parity(i + 1, c) if self.prm.lts else (i + 1) & 1
+        return rows0, rows1, par
+
+
+class _Ranges:
+    """Whole-leaf zip ranges of one rank's layout, finest cadence first, on the
+    device, with the prefix sizes per minimum cadence."""
+
+    def __init__(self, start, length, cad, device):
+        import torch
+
+        start = np.asarray(start, dtype=np.int64)
+        length = np.asarray(length, dtype=np.int64)
+        cad = np.asarray(cad, dtype=np.int64)
+        self.n = len(start)
+        off = np.zeros(self.n + 1, dtype=np.int64)
+        np.cumsum(length, out=off[1:])
+        self.total = int(off[-1])
+        self.off_host = off
+        self.cad_host = cad
+        T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(device)  # noqa: E731
+        self.start = T(start if self.n else np.zeros(1, np.int64))
+        self.off = T(off)
+        self.cad = T((cad if self.n else np.zeros(1, np.int64)).astype(np.int32))
+
+    def prefix(self, cmin: int):
+        """(ranges, nodes) with cadence >= cmin; ranges must be sorted finest first."""
+        k = int(np.sum(self.cad_host >= cmin))
+        return k, int(self.off_host[k])
+
+    def move(self, n_ranges: int, total: int, rows0, rows1, par, buf_ld: int = 0) -> _native.AmrGhostMove:
+        M = _native.AmrGhostMove()
+        M.n_ranges, M.total, M.buf_ld = n_ranges, total, buf_ld
+        M.start, M.off, M.cad = self.start.data_ptr(), self.off.data_ptr(), self.cad.data_ptr()
+        M.n_rows = len(rows0)
+        for r, (a, b) in enumerate(zip(rows0, rows1)):
+            M.row0[r], M.row1[r] = a, b
+        for c, v in enumerate(par):
+            M.par[c] = v
+        return M
+
+
+class _Link:
+    """Shipments of one (sender, receiver) pair: the sender's leaves the
+    receiver's tiles read, finest cadence first, as ranges of each side's layout."""
+
+    def __init__(self, leaves, cad, starts, send_lstart, recv_lstart, device, rows_max):
+        import torch
+
+        leaves = np.asarray(leaves, dtype=np.int64)
+        order = np.lexsort((leaves, -cad[leaves]))
+        leaves = leaves[order]
+        self.leaves = leaves
+        length = (starts[1:] - starts[:-1])[leaves]
+        lc = cad[leaves]
+        self.send = _Ranges(send_lstart[leaves], length, lc, device) if send_lstart is not None else None
+        self.recv = _Ranges(recv_lstart[leaves], length, lc, device) if recv_lstart is not None else None
+        total = int(length.sum())
+        self.total = total
+        self.sbuf = torch.empty(max(rows_max * total, 1), dtype=torch.float64, device=device) \
+            if send_lstart is not None else None
+        self.rbuf = torch.empty(max(rows_max * total, 1), dtype=torch.float64, device=device) \
+            if recv_lstart is not None else None
+
+
+def _ship_lists(need: dict, rank_ranges) -> dict:
+    """{(sender, receiver): leaves} from each receiver's ghost-leaf list."""
+    out = {}
+    for r, ghosts in need.items():
+        ghosts = np.asarray(ghosts, dtype=np.int64)
+        for q, (a, b) in enumerate(rank_ranges):
+            if q == r:
+                continue
+            sel = ghosts[(ghosts >= a) & (ghosts < b)]
+            if len(sel):
+                out[(q, r)] = sel
+    return out
+
+
+class _LocalTransport:
+    """Simulated ranks in one process (the reference's rank_records,
+    stepper.py:158-161, 318-333): every shipment is packed from the sender's
+    rows, copied buffer to buffer, and unpacked into the receiver's ghost rows,
+    all on the engine's stream."""
+
+    def __init__(self, eng: "Engine", ranks: dict, lists: dict):
+        self.eng = eng
+        self.ranks = ranks
+        cad, starts = eng._leaf_cadence, eng.mesh.leaf_starts
+        self.links = {(q, r): _Link(lv, cad, starts, ranks[q].leaf_lstart, ranks[r].leaf_lstart, eng.device, 4)
+                      for (q, r), lv in sorted(lists.items())}
+        self.bytes_moved = 0
+
+    def ship(self, i: int, s: int, cmin: int) -> None:
+        eng = self.eng
+        lib, st = eng._lib, eng._stream()
+        with eng._phase("comm"):
+            for (q, r), lk in self.links.items():
+                k, tot = lk.send.prefix(cmin)
+                if not k:
+                    continue
+                rows0, rows1, par = self.ranks[q].shipment_rows(s, i)
+                _native.check(lib.amr_ghost_pack(C.byref(lk.send.move(k, tot, rows0, rows1, par)),
+                                                 lk.sbuf.data_ptr(), st), "amr_ghost_pack")
+                n = len(rows0) * tot
+                lk.rbuf[:n].copy_(lk.sbuf[:n])  # the wire
+                rows0, rows1, par = self.ranks[r].shipment_rows(s, i)
+                _native.check(lib.amr_ghost_unpack(C.byref(lk.recv.move(k, tot, rows0, rows1, par)),
+                                                   lk.rbuf.data_ptr(), st), "amr_ghost_unpack")
+                self.bytes_moved += 8 * n
+
+    def finish(self) -> None:
+        pass
+
+
+class _DistTransport:
+    """One rank per process over torch.distributed: NCCL point-to-point between
+    GPUs (device buffers, a side stream so the interior tiles overlap the
+    shipment), or gloo through host staging (CPU-side tests)."""
+
+    def __init__(self, eng: "Engine", rk: _Rank, lists: dict, group):
+        import torch
+        import torch.distributed as dist
+
+        self.eng, self.rk, self.group = eng, rk, group
+        cad, starts = eng._leaf_cadence, eng.mesh.leaf_starts
+        me = rk.rank
+        self.out = {r: _Link(lv, cad, starts, rk.leaf_lstart, None, eng.device, 4)
+                    for (q, r), lv in sorted(lists.items()) if q == me}
+        self.inc = {q: _Link(lv, cad, starts, None, rk.leaf_lstart, eng.device, 4)
+                    for (q, r), lv in sorted(lists.items()) if r == me}
+        self.host = dist.get_backend(group) != "nccl"
+        self.global_rank = (lambda r: dist.get_global_rank(group, r)) if group is not dist.group.WORLD else (lambda r: r)
+        self.comm = torch.cuda.Stream(eng.device)
+        self.bytes_moved = 0
+
+    def ship(self, i: int, s: int, cmin: int) -> None:
+        import torch
+        import torch.distributed as dist
+
+        eng, rk = self.eng, self.rk
+        lib = eng._lib
+        cur = torch.cuda.current_stream(eng.device)
+        self.comm.wait_stream(cur)  # the boundary tiles of this stage are queued on `cur`
+        rows0, rows1, par = rk.shipment_rows(s, i)
+        nr = len(rows0)
+        with eng._phase("comm"), torch.cuda.stream(self.comm):
+            st = self.comm.cuda_stream
+            ops, recvs = [], []
+            for r, lk in self.out.items():
+                k, tot = lk.send.prefix(cmin)
+                if not k:
+                    continue
+                _native.check(lib.amr_ghost_pack(C.byref(lk.send.move(k, tot, rows0, rows1, par)),
+                                                 lk.sbuf.data_ptr(), st), "amr_ghost_pack")
+                buf = lk.sbuf[: nr * tot]
+                if self.host:
+                    buf = buf.cpu()
+                ops.append(dist.P2POp(dist.isend, buf, self.global_rank(r), self.group))
+                self.bytes_moved += 8 * nr * tot
+            for q, lk in self.inc.items():
+                k, tot = lk.recv.prefix(cmin)
+                if not k:
+                    continue
+                buf = lk.rbuf[: nr * tot]
+                hb = torch.empty(nr * tot, dtype=torch.float64) if self.host else buf
+                ops.append(dist.P2POp(dist.irecv, hb, self.global_rank(q), self.group))
+                recvs.append((lk, k, tot, buf, hb))
+            if ops:
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()  # NCCL: orders the comm stream after the transfer (no host block)
+            for lk, k, tot, buf, hb in recvs:
+                if self.host:
+                    buf.copy_(hb)
+                _native.check(lib.amr_ghost_unpack(C.byref(lk.recv.move(k, tot, rows0, rows1, par)),
+                                                   buf.data_ptr(), st), "amr_ghost_unpack")
+
+    def finish(self) -> None:
+        """The next launches on the engine's stream see the unpacked ghosts."""
+        import torch
+
+        torch.cuda.current_stream(self.eng.device).wait_stream(self.comm)
+
+
 class Engine:
-    """Wave-system timestepper over a block mesh, global or local mode, on one GPU
-    (or one GPU per rank under torch.distributed)."""
+    """Wave-system timestepper over a block mesh, global or local mode, on one GPU:
+    all ranks of a partitioned mesh simulated in-process, or one rank per
+    process under torch.distributed (``process_group``)."""
 
     NVARS = 2
 
     def __init__(self, mesh: Mesh, tableau: str | ButcherTableau = "rk3", cfl: float = 0.25,
                  mode: str = "lts", nonlinear=False, k_chi: float = 1.0, k_phi: float = 2.0,
-                 threads: int = 1, single_stage_neighbors: bool = False, device=None, process_group=None):
+                 threads: int = 1, single_stage_neighbors: bool = False, device=None, process_group=None,
+                 profile: bool = False):
         import torch
 
         if mode not in ("lts", "gts"):
@@ -198,83 +660,104 @@ class Engine:
         self._r_eps = mesh.finest_spacing()
         self._transfer_cache: dict = {}
         self._coef_cache: dict = {}
+        self._coef_host: dict = {}
+        self._prof = [] if profile else None
+        if profile:
+            self.use_graphs = False
 
-        # -- distribution ---------------------------------------------------------
-        self._dist = None
-        self.rank = 0
-        if process_group is not None or (torch.distributed.is_available() and torch.distributed.is_initialized()
-                                         and torch.distributed.get_world_size() > 1):
-            ws = torch.distributed.get_world_size(process_group)
-            if ws != mesh.pmap.ranks:
-                raise ValueError(f"mesh is partitioned for {mesh.pmap.ranks} ranks, process group has {ws}")
-            self.rank = torch.distributed.get_rank(process_group)
-            self._dist = process_group if process_group is not None else torch.distributed.group.WORLD
-
-        # -- device state ---------------------------------------------------------------
+        # -- device -------------------------------------------------------------------
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
         self.device = torch.device(device)
         if self.device.type != "cuda":
             raise RuntimeError("the engine runs on CUDA devices only (no CPU path)")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self._lib = _native.lib()
-        td = mesh.tile_data()
+        self._threads = int(os.environ.get("AMR_THREADS", "256"))
         n_leaves = len(mesh.tree.leaves)
         leaf_cad = np.empty(n_leaves, dtype=np.int32)
         for b in mesh.blocks:
             leaf_cad[b.leaf_range[0]: b.leaf_range[1]] = cadence[b.index]
         self._leaf_cadence = leaf_cad
-        counts = np.diff(td["starts"])
-        node_cad = np.repeat(leaf_cad.astype(np.uint8), counts)
-        owners = mesh.pmap.owners(n_leaves)
-        mine = np.nonzero(owners == self.rank)[0] if self._dist is not None else np.arange(n_leaves)
-        order = np.lexsort((mine, -leaf_cad[mine]))
-        tiles = mine[order].astype(np.int32)
-        lts_kernel = mode == "lts" or any(c != self.l_max for c in cadence)
-        self._init_programs(td, tiles, leaf_cad, node_cad, lts_kernel)
-        n = mesh.n_nodes
-        # the reference's (nvars, n_nodes) zip layout, SoA: chi row then phi row.
-        # Rows are padded to an even stride ld > n (16-byte aligned rows; the
-        # kernel bulk-prefetches 16-byte aligned supersets of a tile's owned range)
-        ld = (n + 2) // 2 * 2
-        self._ld = ld
-        dev = self.device
-        self._U_store = [torch.zeros((2, ld), dtype=torch.float64, device=dev) for _ in range(2)]
-        self._K_store = torch.zeros((self.p, 2, ld), dtype=torch.float64, device=dev)
-        self._U = [u[:, :n] for u in self._U_store]
-        self._K = self._K_store[:, :, :n]
-        # verbatim stage sources, double-buffered by stage parity
-        self._Y_store = torch.zeros((2, 2, ld), dtype=torch.float64, device=dev)
-        self._Y = self._Y_store[:, :, :n]
-        self._node_cad_t = self._d["node_cad"].long()
+        self._lts_kernel = mode == "lts" or any(c != self.l_max for c in cadence)
         self._vt = [[j for j in range(s_) if self.tab.a[s_][j] != 0.0] for s_ in range(self.p)]
-        self._prm = self._make_params()
-        self._exchange = _EngineExchange(self) if self._dist is not None else None
 
-    def _init_programs(self, td, tiles, leaf_cad, node_cad, lts):
-        """The stage kernel's per-tile programs (tileprog.py) on the device."""
+        # -- ranks ----------------------------------------------------------------------
+        # distributed (one rank here) only with an explicit process group, or when
+        # the default group's size is the mesh's rank count; otherwise a
+        # partitioned mesh runs as simulated ranks in this process
+        R = mesh.pmap.ranks
+        dist = torch.distributed
+        self._dist = None
+        self.rank = 0
+        if process_group is not None:
+            if process_group is True:
+                process_group = dist.group.WORLD
+            ws = dist.get_world_size(process_group)
+            if ws != R:
+                raise ValueError(f"mesh is partitioned for {R} ranks, process group has {ws}")
+            self._dist = process_group
+            self.rank = dist.get_rank(process_group)
+        elif R > 1 and process_group is None and dist.is_available() and dist.is_initialized() \
+                and dist.get_world_size() == R:
+            self._dist = dist.group.WORLD
+            self.rank = dist.get_rank()
+        rr = mesh.pmap.rank_ranges
+        with torch.cuda.device(self.device):
+            if self._dist is not None:
+                local = {self.rank: _Rank(mesh, leaf_cad, self._lts_kernel, self.l_max, self.rank, np.arange(*rr[self.rank]))}
+                gathered = [None] * R
+                dist.all_gather_object(gathered, local[self.rank].ghosts.tolist(), group=self._dist)
+                need = {r: np.asarray(g, dtype=np.int64) for r, g in enumerate(gathered)}
+            elif R > 1:
+                local = {r: _Rank(mesh, leaf_cad, self._lts_kernel, self.l_max, r, np.arange(*rr[r])) for r in range(R)}
+                need = {r: rk.ghosts for r, rk in local.items()}
+            else:
+                local = {0: _Rank(mesh, leaf_cad, self._lts_kernel, self.l_max, 0, np.arange(n_leaves))}
+                need = {}
+            lists = _ship_lists(need, rr) if need else {}
+            for r, rk in local.items():
+                sent = [lv for (q, _), lv in lists.items() if q == r]
+                rk.layout(np.unique(np.concatenate(sent)) if sent else np.zeros(0, np.int64))
+                rk.upload(self)
+            self._ranks = local
+            self._rank_list = [local[r] for r in sorted(local)]
+            if self._dist is not None:
+                self._transport = _DistTransport(self, local[self.rank], lists, self._dist)
+            elif R > 1:
+                self._transport = _LocalTransport(self, local, lists)
+            else:
+                self._transport = None
+        self.ghost_lists = lists
+
+    # single-rank views kept for tools and tests
+    @property
+    def _prm(self):
+        return self._rank_list[0].prm
+
+    @property
+    def _d(self):
+        rk = self._rank_list[0]
+        return dict(rk.d, tiles=rk.tiles)
+
+    @property
+    def _U(self):
+        return self._rank_list[0].U
+
+    @property
+    def _K(self):
+        return self._rank_list[0].K
+
+    @property
+    def _prefix(self):
+        rk = self._rank_list[0]
+        return {c: rk.prefix_b[c] + rk.prefix_i[c] for c in range(self.l_max + 1)}
+
+    def _stream(self) -> int:
         import torch
 
-        from . import tileprog
-
-        prog = tileprog.build_programs_native(self.mesh, tiles, leaf_cad, lts)  # == tileprog.build_programs
-        tcad = leaf_cad[tiles]
-        self._prefix = {c: int(np.sum(tcad >= c)) for c in range(self.l_max + 1)}
-        n_iface = prog["n_iface"]
-        self._if_prefix = {c: int(np.sum((prog["if_cad"][:n_iface] & 0xFF) >= c)) for c in range(self.l_max + 1)}
-        self._n_iface = n_iface
-        dev = self.device
-        T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
-        pad = lambda a: a if len(a) else np.zeros(1, a.dtype)  # noqa: E731
-        self._d = dict(tiles=T(tiles.astype(np.int32)), node_cad=T(node_cad), heads=T(prog["heads"]),
-                       tail=T(prog["tail"]), wtab=T(prog["wtab"]), if_gid=T(pad(prog["if_gid"])),
-                       if_cad=T(pad(prog["if_cad"])))
-        self._max_slots = prog["max_slots"]
-        self._max_head = prog["max_head"]
-        self._max_tail = prog["max_tail"]
-        self._ibuf = torch.zeros((2, max(n_iface, 1)), dtype=torch.float64, device=dev)
-        self._threads = int(os.environ.get("AMR_THREADS", "256"))
-
-
+        return torch.cuda.current_stream(self.device).cuda_stream
 
     # -- setup -------------------------------------------------------------------------
     def _promoted_cadence(self, levels: list[int]) -> list[int]:
@@ -294,50 +777,6 @@ class Engine:
                     cadence[i] = max(cadence[i], levels[j])
         return cadence
 
-    def _make_params(self) -> _native.AmrStageParams:
-        m = self.mesh
-        P = _native.AmrStageParams()
-        P.dim, P.ppo, P.pad = m.dim, m.ppo, m.pad
-        P.lts = 1 if self.mode == "lts" or any(c != self.l_max for c in self.cadence) else 0
-        P.n_stages = self.p
-        P.nonlinear = self._nl
-        P.n_nodes = m.n_nodes
-        P.ld = self._ld
-        d = self._d
-        P.max_slots = self._max_slots
-        P.if_gid, P.if_cad, P.ibuf = d["if_gid"].data_ptr(), d["if_cad"].data_ptr(), self._ibuf.data_ptr()
-        P.n_iface_total = self._n_iface
-        P.wtab, P.n_wtab = d["wtab"].data_ptr(), int(d["wtab"].numel())
-        P.heads, P.max_head, P.tail = d["heads"].data_ptr(), self._max_head, d["tail"].data_ptr()
-        P.threads = self._threads
-        P.max_tail = self._max_tail
-        P.U0, P.U1, P.K = self._U[0].data_ptr(), self._U[1].data_ptr(), self._K.data_ptr()
-        P.Y = self._Y.data_ptr()
-        for s in range(self.p):
-            for j in range(self.p):
-                a = self.tab.a[s][j]
-                P.g_cstage[s][j] = self.dt_fine * a if (j < s and a != 0.0) else 0.0
-            w = self.tab.w[s]
-            P.g_comb[s] = (1 * self.dt_fine) * w if w != 0.0 else 0.0
-        P.max_depth = m.L
-        P.top_nodes = m.top_nodes
-        for dd in range(m.dim):
-            P.lo[dd] = m.domain.lo[dd]
-            P.extent[dd] = m.domain.extent(dd)
-        for lvl in range(_native.AMR_MAXL):
-            if lvl > m.L:
-                continue
-            h = m.level_spacing(lvl)
-            h2 = h ** 2
-            P.h[lvl], P.h2[lvl] = h, h2
-            P.h2_pow2[lvl] = 1 if _pow2_exact(h2) else 0
-            P.inv_h2[lvl] = 1.0 / h2 if P.h2_pow2[lvl] else 0.0
-        P.r_eps = self._r_eps
-        P.r_eps2 = self._r_eps ** 2
-        P.k_chi, P.k_phi, P.f0_chi, P.f0_phi = self.k_chi, self.k_phi, 0.0, 0.0
-        fill_weights(P)
-        return P
-
     # -- plans (API parity; built lazily: they need every block's gather support) --
     @property
     def full_plan(self) -> ExchangePlan:
@@ -355,6 +794,24 @@ class Engine:
             ]
         return self._partial_plans
 
+    # -- phase timing (stepper.py:72-84 buckets, on the device) ---------------------------
+    def _phase(self, name: str):
+        return _PhaseTimer(self, name) if self._prof is not None else _NO_TIMER
+
+    def phase_ms(self) -> dict:
+        """Device milliseconds per phase bucket since construction (profile=True):
+        ``time_interp`` (LTS interface pass), ``rhs`` (the fused unzip + RHS + zip
+        stage kernel, which also covers the reference's ``blk_sync``), ``comm``."""
+        import torch
+
+        if self._prof is None:
+            raise RuntimeError("construct the engine with profile=True")
+        torch.cuda.synchronize(self.device)
+        for name, a, b in self._prof:
+            self.counters.phases[name] += a.elapsed_time(b) * 1e-3
+        self._prof.clear()
+        return {k: 1e3 * v for k, v in self.counters.phases.items()}
+
     # -- state I/O -----------------------------------------------------------------------
     def initialize(self, chi0, phi0=None) -> None:
         xyz = self.mesh.node_physical()
@@ -366,18 +823,23 @@ class Engine:
         self.load_zip(z)
 
     def load_zip(self, z) -> None:
-        """Load a (2, n_nodes) zip field (host numpy or device tensor): u_pre = u_curr = z, K = 0."""
+        """Load a (2, n_nodes) zip field (host numpy, pinned host or device tensor):
+        u_pre = u_curr = z, K = 0 (stepper.py:213-230)."""
         import torch
 
         if not isinstance(z, torch.Tensor):
             z = torch.from_numpy(np.ascontiguousarray(z, dtype=np.float64))
         if tuple(z.shape) != (self.NVARS, self.mesh.n_nodes):
             raise ValueError(f"zip field must be (2, {self.mesh.n_nodes}), got {tuple(z.shape)}")
-        # straight into the live buffer (one host->device copy; pinned host
-        # memory makes it a DMA), then device-side into the other parity
-        self._U[0].copy_(z.to(dtype=torch.float64), non_blocking=True)
-        self._U[1].copy_(self._U[0])
-        self._K.zero_()
+        z = z.to(dtype=torch.float64)
+        with torch.cuda.device(self.device):
+            one = self._rank_list[0]
+            if len(self._rank_list) == 1 and one.identity:
+                one.load(z)  # straight into the live buffer: one host->device DMA
+            else:
+                zd = z.to(self.device, non_blocking=True)
+                for rk in self._rank_list:
+                    rk.load(zd)
         self.i_fine = 0
 
     @property
@@ -388,18 +850,33 @@ class Engine:
         per = 1 << (self.l_max - cad)
         return ((i + per - 1) // per) & 1
 
-    def current_zip_device(self):
-        """(2, n_nodes) float64 device tensor of every leaf's u_curr."""
+    def current_zip_device(self, out=None):
+        """(2, n_nodes) float64 device tensor of every leaf's u_curr: each rank's
+        owned ranges read from the buffer of their cadence's parity (one gather
+        launch per rank).  Under torch.distributed the ranks' parts are summed
+        into the global field (every other entry is zero)."""
         import torch
 
+        n = self.mesh.n_nodes
         i = self.i_fine
-        key = tuple(self._cur_parity(i, c) for c in range(self.l_max + 1))
-        cache = self.__dict__.setdefault("_sel_cache", {})
-        sel = cache.get(key)
-        if sel is None:  # which u buffer is live, per node: a function of the cadence parities only
-            par = torch.tensor(key, device=self.device)
-            sel = cache[key] = par[self._node_cad_t].bool().unsqueeze(0)
-        return torch.where(sel, self._U[1], self._U[0])
+        with torch.cuda.device(self.device):
+            if out is None:
+                out = torch.empty((2, n), dtype=torch.float64, device=self.device) if self._dist is None else \
+                    torch.zeros((2, n), dtype=torch.float64, device=self.device)
+            par = [(self._cur_parity(i, c) if self._lts_kernel else i & 1) if c <= self.l_max else 0
+                   for c in range(_native.AMR_MAXL)]
+            st = self._stream()
+            for rk in self._rank_list:
+                rg = rk.own_ranges
+                if not rg.total:
+                    continue
+                u0, u1, ld = rk.U_store[0].data_ptr(), rk.U_store[1].data_ptr(), rk.ld
+                M = rg.move(rg.n, rg.total, [u0, u0 + 8 * ld], [u1, u1 + 8 * ld], par, buf_ld=n)
+                _native.check(self._lib.amr_ghost_pack(C.byref(M), out.data_ptr() + 8 * rk.own_g0, st),
+                              "amr_ghost_pack")
+            if self._dist is not None:
+                torch.distributed.all_reduce(out, group=self._dist)
+        return out
 
     def current_zip(self) -> np.ndarray:
         return self.current_zip_device().cpu().numpy()
@@ -419,15 +896,15 @@ class Engine:
         # after the copy that read it two calls ago has finished
         st = self.__dict__.get("_snap")
         if st is None:
-            st = self.__dict__["_snap"] = [[torch.empty_like(self._U[0]), None] for _ in range(2)]
+            st = self.__dict__["_snap"] = [
+                [torch.empty((2, self.mesh.n_nodes), dtype=torch.float64, device=self.device), None] for _ in range(2)]
             self.__dict__["_snap_i"] = 0
         j = self.__dict__["_snap_i"]
         self.__dict__["_snap_i"] = j ^ 1
         buf, prev = st[j]
         if prev is not None:
             cur.wait_event(prev)
-        live = self.current_zip_device()
-        buf.copy_(live)
+        self.current_zip_device(out=buf)
         cs = copy_stream if copy_stream is not None else cur
         cs.wait_stream(cur)
         with torch.cuda.stream(cs):
@@ -521,6 +998,13 @@ class Engine:
         raw = np.frombuffer(bytes(cf), dtype=np.uint8).copy()
         t = torch.from_numpy(raw).to(self.device)
         self._coef_cache[key] = t
+        # the entries the stage kernel takes by value (same bits)
+        mask = 0
+        for c in cads:
+            mask |= (cf.cur[c] & 1) << c
+        self._coef_host[key] = (mask,
+                                {c: [[cf.cstage[c][s][j] for j in range(p)] for s in range(p)] for c in cads},
+                                {c: [cf.comb[c][j] for j in range(p)] for c in cads})
         return t
 
     # -- the slice ------------------------------------------------------------------------------
@@ -528,41 +1012,30 @@ class Engine:
         return [c for c in sorted(set(self.cadence)) if i % (1 << (self.l_max - c)) == 0]
 
     def advance_slice(self) -> None:
-        """Advance every block eligible at the current fine slice by one of its steps."""
+        """Advance every block eligible at the current fine slice by one of its steps.
+
+        Per stage and rank: the LTS interface pass, the tiles other ranks read,
+        the shipment of what they wrote (K_s and the next stage's verbatim
+        source, or the new u after the last stage) while the interior tiles
+        run; the next stage starts when the ghosts have landed."""
         import torch
 
         i = self.i_fine
         elig = self._eligible_cadences(i)
-        n_tiles = self._prefix[min(elig)] if elig else 0
-        P = self._prm
-        P.n_tiles = n_tiles
-        P.n_iface = self._if_prefix[min(elig)] if elig else 0
-
-        if P.lts:
-            P.coef = self._slice_coef(i).data_ptr()
-        else:
-            P.gts_cur = i & 1
-        stream = torch.cuda.current_stream(self.device).cuda_stream
-        t0 = time.perf_counter()
-        for s in range(self.p):
-            P.stage = s
-            vt = self._vt[s + 1] if s + 1 < self.p else []  # the writer forms stage s+1's sources
-            P.n_vt = len(vt)
-            for t, j in enumerate(vt):
-                P.vt_j[t] = j
-            if n_tiles:
-                if P.n_iface:
-                    rc = self._lib.amr_iface(C.byref(P), stream)
-                    if rc:
-                        _native.check(rc, "amr_iface")
-                rc = self._lib.amr_stage(C.byref(P), stream)
-                if rc:
-                    _native.check(rc, "amr_stage")
-            if self._exchange is not None:
-                self._exchange.after_stage(i, s, elig)
-        if self._exchange is not None:
-            self._exchange.after_step(i, elig)
-        self.counters.phases["rhs"] += time.perf_counter() - t0
+        if elig:
+            cmin = min(elig)
+            tr = self._transport
+            with torch.cuda.device(self.device):
+                for s in range(self.p):
+                    for rk in self._rank_list:
+                        rk.begin_stage(i, s, cmin)
+                        rk.launch_tiles(cmin, True)
+                    if tr is not None:
+                        tr.ship(i, s, cmin)
+                    for rk in self._rank_list:
+                        rk.launch_tiles(cmin, False)
+                    if tr is not None:
+                        tr.finish()
         self.counters._tally(elig)
         self.i_fine += 1
 
@@ -578,7 +1051,7 @@ class Engine:
         if self.i_fine % self.schedule.slices_per_round != 0:
             raise RuntimeError("blocks are not synchronized at a coarse time")
         R = self.schedule.slices_per_round
-        if self.use_graphs and self._dist is None:
+        if self.use_graphs and self._graphable():
             self._replay_round(R)
             return
         for _ in range(R):
@@ -586,6 +1059,14 @@ class Engine:
 
     # -- CUDA graphs ----------------------------------------------------------------------
     use_graphs = True
+
+    def _graphable(self) -> bool:
+        """Single-rank and simulated-rank rounds are pure launch sequences on one
+        stream.  NCCL shipments can be captured too (AMR_GRAPH_NCCL=1); that
+        path has not run on multi-GPU hardware, so it is opt-in."""
+        if self._dist is None:
+            return True
+        return (not self._transport.host) and os.environ.get("AMR_GRAPH_NCCL") == "1"
 
     def _replay_round(self, R: int) -> None:
         """One coarse round as a captured CUDA graph.  The launch sequence of a
@@ -602,9 +1083,10 @@ class Engine:
                 self.advance_slice()
             i_next = self.i_fine
             for i in range(i_next, i_next + 2 * R):  # coefficient blocks of both parities
-                if self._prm.lts:
+                if self._lts_kernel:
                     self._slice_coef(i)
             torch.cuda.synchronize(self.device)
+            moved = self._transport.bytes_moved if self._transport is not None else 0
             for start in (i_next, i_next + R):
                 graph = torch.cuda.CUDAGraph()
                 self.i_fine = start
@@ -613,11 +1095,16 @@ class Engine:
                         self.advance_slice()
                 self._untally_round(start, R)
                 self._graphs[(start // R) & 1] = graph
+            if self._transport is not None:
+                self._round_bytes = (self._transport.bytes_moved - moved) // 2
+                self._transport.bytes_moved = moved
             self.i_fine = i_next
             return
         i0 = self.i_fine
         self._graphs[(i0 // R) & 1].replay()
         self._tally_round(i0, R)
+        if self._transport is not None:
+            self._transport.bytes_moved += self._round_bytes
         self.i_fine = i0 + R
 
     def _tally_round(self, i0: int, R: int) -> None:
@@ -635,14 +1122,56 @@ class Engine:
             self.advance_slice()
 
     def launches_per_slice(self, i: int) -> int:
-        """Kernel launches advance_slice(i) issues (stage + LTS interface passes)."""
+        """Stage-path kernel launches advance_slice(i) issues on this process
+        (LTS interface passes and stage kernels; shipments not counted)."""
         el = self._eligible_cadences(i)
         if not el:
             return 0
-        return self.p * (2 if self._if_prefix[min(el)] else 1)
+        c = min(el)
+        n = 0
+        for rk in self._rank_list:
+            tiles = (1 if rk.prefix_b[c] else 0) + (1 if rk.prefix_i[c] else 0)
+            n += tiles + (1 if tiles and rk.if_prefix[c] else 0)
+        return self.p * n
+
+    @property
+    def comm_bytes(self) -> int:
+        """Ghost bytes shipped so far (sent by the ranks held in this process)."""
+        return self._transport.bytes_moved if self._transport is not None else 0
 
     def close(self):
-        self._exchange = None
+        self._transport = None
+
+
+class _PhaseTimer:
+    def __init__(self, eng: Engine, name: str):
+        self.eng, self.name = eng, name
+
+    def __enter__(self):
+        import torch
+
+        self.a = torch.cuda.Event(enable_timing=True)
+        self.a.record(torch.cuda.current_stream(self.eng.device))
+        return self
+
+    def __exit__(self, *exc):
+        import torch
+
+        b = torch.cuda.Event(enable_timing=True)
+        b.record(torch.cuda.current_stream(self.eng.device))
+        self.eng._prof.append((self.name, self.a, b))
+        return False
+
+
+class _NoTimer:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+_NO_TIMER = _NoTimer()
 
 
 def lts_single_stage_engine(mesh: Mesh, **kw) -> Engine:
@@ -663,104 +1192,3 @@ def compare_round(lts: Engine, gts: Engine) -> float:
     a = lts.current_zip()
     b = gts.current_zip()
     return float(np.max(np.abs(a[0] - b[0])))
-
-
-class GhostExchange:
-    """Ghost-leaf transport between ranks over torch.distributed (NCCL on GPUs,
-    gloo in the CPU tests).
-
-    The reference ships whole leaf records after every stage and step
-    (stepper.py:318-361, partition.py:182-207).  Here only the record fields
-    that changed move: K_s of the leaves that just ran stage s, and their new
-    u after the step; t0/dt_units follow from the schedule and u_pre is the
-    other parity buffer the receiver already holds.  Which leaves go to which
-    rank is the reference's exchange plan (block gather footprints); since
-    every rank keeps the global zip layout, a shipment is a set of contiguous
-    gid ranges gathered into one buffer per peer."""
-
-    def __init__(self, plan: ExchangePlan, leaf_cadence: np.ndarray, leaf_starts: np.ndarray, rank: int,
-                 group=None, device=None):
-        self.group = group
-        self.rank = rank
-        self.cad = np.asarray(leaf_cadence)
-        self.starts = np.asarray(leaf_starts)
-        self.device = device
-        self.send, self.recv = {}, {}
-        for (s, r), items in plan.entries.items():
-            leaves = np.array([e.leaf for e in items], dtype=np.int64)
-            if s == rank:
-                self.send[r] = leaves
-            if r == rank:
-                self.recv[s] = leaves
-        self.peers = sorted(set(self.send) | set(self.recv))
-        self._idx = {}
-
-    @classmethod
-    def for_engine(cls, eng: "Engine") -> "GhostExchange":
-        return cls(eng.full_plan, eng._leaf_cadence, eng.mesh.leaf_starts, eng.rank, eng._dist, eng.device)
-
-    def _index(self, kind, peer, sel_key, select):
-        import torch
-
-        key = (kind, peer, sel_key)
-        if key not in self._idx:
-            leaves = (self.send if kind == "s" else self.recv).get(peer)
-            idx = None
-            if leaves is not None:
-                sel = leaves[select(self.cad[leaves])]
-                if len(sel):
-                    idx = torch.from_numpy(np.concatenate(
-                        [np.arange(self.starts[l], self.starts[l + 1]) for l in sel])).to(self.device)
-            self._idx[key] = idx
-        return self._idx[key]
-
-    def swap(self, tensor, sel_key, select) -> None:
-        """Ship the zip nodes (last axis) of the selected leaves owned here to
-        every peer that reads them."""
-        import torch
-        import torch.distributed as dist
-
-        ax = tensor.dim() - 1
-        ops, bufs = [], []
-        for peer in self.peers:
-            si = self._index("s", peer, sel_key, select)
-            ri = self._index("r", peer, sel_key, select)
-            if si is not None:
-                ops.append(dist.P2POp(dist.isend, tensor.index_select(ax, si).contiguous(), peer, self.group))
-            if ri is not None:
-                rb = torch.empty(tuple(tensor.shape[:-1]) + (len(ri),), dtype=tensor.dtype, device=tensor.device)
-                ops.append(dist.P2POp(dist.irecv, rb, peer, self.group))
-                bufs.append((ri, rb))
-        if ops:
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
-        for ri, rb in bufs:
-            tensor.index_copy_(ax, ri, rb)
-
-    def swap_from_cadence(self, tensor, min_cad: int) -> None:
-        self.swap(tensor, ("ge", min_cad), lambda c: c >= min_cad)
-
-    def swap_cadence(self, tensor, cad: int) -> None:
-        self.swap(tensor, ("eq", cad), lambda c: c == cad)
-
-
-class _EngineExchange:
-    """Engine hooks: K_s after each stage, the new u after the step."""
-
-    def __init__(self, eng: Engine):
-        self.eng = eng
-        self.gx = GhostExchange.for_engine(eng)
-
-    def after_stage(self, i: int, s: int, elig: list[int]) -> None:
-        if elig:
-            t0 = time.perf_counter()
-            self.gx.swap_from_cadence(self.eng._K[s], min(elig))
-            if s + 1 < self.eng.p:  # the verbatim sources the owners formed for stage s+1
-                self.gx.swap_from_cadence(self.eng._Y[(s + 1) & 1], min(elig))
-            self.eng.counters.phases["comm"] += time.perf_counter() - t0
-
-    def after_step(self, i: int, elig: list[int]) -> None:
-        t0 = time.perf_counter()
-        for c in elig:  # each cadence wrote the buffer of its new parity
-            self.gx.swap_cadence(self.eng._U[self.eng._cur_parity(i + 1, c)], c)
-        self.eng.counters.phases["comm"] += time.perf_counter() - t0

@@ -129,9 +129,7 @@ def test_stage_kernel_block_shapes_match_reference(cuda, monkeypatch, cfg, tag, 
 def test_unencodable_mesh_raises(cuda, monkeypatch):
     """A mesh that does not fit the compact per-tile encoding (here: a forced
     1-source-group limit) is refused with a ValueError, never run on a fallback."""
-    from paper_2011_10570_b200 import tileprog
-
-    monkeypatch.setattr(tileprog, "MAX_BASES", 1)
+    monkeypatch.setenv("AMR_MAX_BASES", "1")  # read by the native program builder
     mesh = config_mesh("cfg1")
     with pytest.raises(ValueError, match="source groups"):
         Engine(mesh, tableau="rk4", mode="lts")

@@ -4,8 +4,8 @@ reference goldens in tests/test_oracle.py), plus size-independent properties.
 cfg2 (configs[1], 3.67 M zip nodes) is compared bit for bit after one LTS
 coarse round and after GTS steps.  Properties checked at full size:
 uniform-mesh LTS == GTS bit-exact (a reference test, test_stepper.py:150-161),
-the zero field as a fixed point, rank-split invariance, and linearity of the
-linear operator."""
+the zero field as a fixed point, and linearity of the linear operator
+(rank-count invariance at this size: tests/test_ranks_gpu.py)."""
 import numpy as np
 import pytest
 
@@ -48,23 +48,6 @@ def test_cfg2_matches_oracle_bit_exact(cuda, cfg2, mode, nl, slices):
     got, want = eng.current_zip(), ref.current_zip()
     assert rel_linf(got, want) <= 1e-12
     assert np.array_equal(got, want)
-
-
-def test_cfg2_rank_split_invariance(cuda, cfg2):
-    """Partitioned blocks (R=4) leave the single-GPU result bit-identical
-    (reference: test_stepper.py:234-245)."""
-    from paper_2011_10570_b200.partition import tree_weights, weighted_partition
-
-    c, tree, mesh, _ = cfg2
-    pm = weighted_partition(tree, tree_weights(tree, "lts"), 4)
-    mesh4 = Mesh(tree, points_per_octant=9, pad=2, pmap=pm, domain=Domain(c.domain_lo, c.domain_hi))
-    outs = []
-    for m in (mesh, mesh4):
-        eng = Engine(m, tableau="rk4", mode="lts")
-        eng.initialize(c.chi0())
-        eng.lts_coarse_step()
-        outs.append(eng.current_zip())
-    assert np.array_equal(outs[0], outs[1])
 
 
 def test_uniform_3d_lts_equals_gts_bit_exact(cuda):

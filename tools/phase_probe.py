@@ -20,7 +20,7 @@ for mode in ("gts", "lts"):
     eng.initialize(cfg.chi0())
     for _ in range(eng.schedule.slices_per_round):
         eng.advance_slice()
-    nt = len(eng._d["tiles"])
+    nt = len(eng._rank_list[0].tiles)
     buf = torch.zeros((nt, 8), dtype=torch.int64, device="cuda")
     eng._prm.probe = buf.data_ptr()
     for stage_of_interest in range(eng.p):
