@@ -1,23 +1,28 @@
 """Benchmark: RK-stage zip-node updates/s of the LTS/GTS octree wave solver on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2] [--side cfg3,cfg4]
 
-One *step* = one LTS coarse round (2^dL fine slices) of BASELINE configs[1]
-("cfg2": 3D linear wave, levels 3-7, ppo 9, RK4, CFL 0.25) — the largest
-workload the metric is quoted on for one GPU.  Unit of work = one RK stage
-applied to one zip node; LTS counts the units it executes.
-Alongside: the GTS engine over the same simulated time (the LTS-vs-GTS wall
-speedup), the stage kernel's HBM roofline (68 algorithmic bytes per unit,
-CUDA events per launch), an end-to-end number through the public API with
-host buffers, the CPU oracle ("port" of the reference; the reference itself is
-pure Python and absent on the GPU box) timed on the host cores, and the SM
-clocks sampled during the timed region.
+One *step* = one LTS coarse round (2^dL fine slices).  The headline workload is
+BASELINE configs[1] ("cfg2": 3D linear wave, levels 3-7, ppo 9, RK4, CFL 0.25),
+the configuration the metric is quoted on for a single GPU and the one both
+arms (this one and `--impl reference`, the CPU port) run.  configs[2] and
+configs[3] (cfg3: 45.8 M zip nodes, cubic; cfg4: 53.8 M zip nodes, levels 2-13)
+also fit one GPU; they are measured GPU-only in the same run and reported under
+"other_configs" (the CPU arm cannot finish them in bounded time).  Unit of work
+= one RK stage applied to one zip node; LTS counts the units it
+executes.  Alongside: the GTS engine over the same simulated time (the
+LTS-vs-GTS wall speedup next to perfmodel's estimate), the stage kernel's HBM
+roofline (68 algorithmic bytes per unit, CUDA events per launch), an
+end-to-end number through the public API with pinned host buffers, the CPU
+oracle ("port" of the reference; the reference itself is pure Python and
+absent on the GPU box) timed on the host cores, and the SM clocks sampled
+during the timed region.
 
 N > 1: launched by torch.distributed.run, one rank per GPU, weighted Morton
-partition across ranks (mesh.pmap), ghost leaves over NCCL after every stage;
-time = max over ranks, value = all ranks' units / time ("weak" in the sense
-that each rank owns a contiguous 1/N of the weighted leaves of a fixed mesh
-is strong scaling — reported as "strong").
+partition across ranks (mesh.pmap), each rank holds its owned + ghost leaves
+and ships ghost records over NCCL after every stage (boundary tiles first,
+interior tiles overlapped); time = max over ranks, value = all ranks' units /
+time.  The mesh is fixed, so this is strong scaling ("strong").
 """
 from __future__ import annotations
 
@@ -132,26 +137,18 @@ def _workload(name: str) -> str:
             f"{c.tableau.upper()}, CFL {c.cfl}; step = one LTS coarse round")
 
 
+def _config(name: str, zip_nodes: int, leaves: int) -> dict:
+    """The `config` object: identical in both arms (ours and --impl reference)."""
+    return {"workload": _workload(name), "leaves": int(leaves), "zip_nodes": int(zip_nodes),
+            "l2_policy": f"inputs larger than L2 (state u0,u1,K0..K3 = {6 * 16 * zip_nodes / 1e6:.0f} MB > 126 MB)"}
+
+
 def _speedup_model(mesh, work_ratio):
     from paper_2011_10570_b200.perfmodel import estimate, histogram_from_mesh
 
     est = estimate(histogram_from_mesh(mesh.blocks))
     return {"perfmodel_speedup": est.speedup, "perfmodel_bound": est.bound,
             "zip_node_work_ratio": work_ratio}
-
-
-def _ncu_traffic():
-    """DRAM bytes per stage launch from the committed ncu capture
-    (profiles/traffic.json, written by tools/ncu_traffic.py from one
-    `ncu --set full` run of tools/profile_stage.py on cfg2)."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            d = json.load(f)
-        return float(d["lts_bytes_per_launch"]), (
-            f"ncu dram__bytes_read+write per LTS stage launch ({d['source']}); "
-            f"algorithmic bytes of the same launches: {d['lts_algorithmic_bytes_per_launch']:.3e}")
-    except Exception:
-        return None, "no committed ncu capture"
 
 
 def build_mesh(cfg_name, ranks, mode):
@@ -185,8 +182,9 @@ def units_per_round(eng, rank_only=True):
     return total, launches
 
 
-def time_rounds(eng, steps, torch, dist, per_launch=False):
-    """Device time of `steps` rounds; optional per-launch CUDA events (profiling pass)."""
+def time_rounds(eng, steps, torch, dist, per_launch=False, n_slices=None):
+    """Device time of `steps` rounds; optional per-launch CUDA events (profiling
+    pass: eager slices, every stage launch bracketed; returns (ms, tiles, is_boundary_part))."""
     dev = eng.device
     stream = torch.cuda.current_stream(dev)
     if dist is not None:
@@ -194,9 +192,8 @@ def time_rounds(eng, steps, torch, dist, per_launch=False):
     torch.cuda.synchronize(dev)
     launches = []
     if per_launch:
-        from paper_2011_10570_b200 import _native
-
-        L, P = eng._lib, eng._prm
+        L, rk = eng._lib, eng._rank_list[0]
+        P = rk.prm
         orig = L.amr_stage
 
         def timed(prm, strm):
@@ -205,14 +202,21 @@ def time_rounds(eng, steps, torch, dist, per_launch=False):
             e0.record(stream)
             rc = orig(prm, strm)
             e1.record(stream)
-            launches.append((e0, e1, int(P.n_tiles)))
+            launches.append((e0, e1, int(P.n_tiles), int(P.heads) == rk.heads_ptr and rk.n_boundary > 0))
             return rc
 
-        eng._lib = type("L", (), {"amr_stage": staticmethod(timed), "amr_iface": staticmethod(L.amr_iface)})()
+        class _Hook:
+            amr_stage = staticmethod(timed)
+
+            def __getattr__(self, name):
+                return getattr(L, name)
+
+        eng._lib = _Hook()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     start.record(stream)
-    n_slices = eng.schedule.slices_per_round
+    if n_slices is None:
+        n_slices = eng.schedule.slices_per_round
     for _ in range(steps):
         if per_launch:  # eager slices so every launch can be bracketed by events
             for _ in range(n_slices):
@@ -226,7 +230,173 @@ def time_rounds(eng, steps, torch, dist, per_launch=False):
     if per_launch:
         eng._lib = L
     ms = start.elapsed_time(end)
-    return ms, [(a.elapsed_time(b), n) for a, b, n in launches]
+    return ms, [(a.elapsed_time(b), n, bd) for a, b, n, bd in launches]
+
+
+def time_e2e(eng, steps, torch, serial=False):
+    """Seconds for `steps` end-to-end steps through the public API with HOST
+    buffers: every step uploads its (2, n_nodes) input from pinned host memory
+    (Engine.load_zip), runs one LTS coarse round and reads the result back into
+    pinned host memory (Engine.current_zip_to).  Pipelined by default: step
+    k+1's upload (copy stream, into a second staging buffer) and step k's
+    read-back (another copy stream, from a snapshot) overlap the rounds, as a
+    driver feeding independent fields would run it; `serial` does one thing at
+    a time.  All copies of all steps are inside the timed region (wall clock,
+    device synchronised on both sides)."""
+    dev = eng.device
+    n = eng.mesh.n_nodes
+    z_in = [torch.from_numpy(eng.current_zip()).pin_memory() for _ in range(2)]
+    z_out = [torch.empty((2, n), dtype=torch.float64).pin_memory() for _ in range(2)]
+    main = torch.cuda.current_stream(dev)
+    if serial:
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for k in range(steps):
+            eng.load_zip(z_in[k & 1])
+            eng.lts_coarse_step()
+            eng.current_zip_to(z_out[k & 1]).synchronize()
+        torch.cuda.synchronize(dev)
+        return time.perf_counter() - t0, "serial"
+    up, down = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    stage = [torch.empty((2, n), dtype=torch.float64, device=dev) for _ in range(2)]
+    uploaded = [None, None]   # event: staging buffer b holds its step's input
+    consumed = [None, None]   # event: load_zip has read staging buffer b
+
+    def upload(k):
+        b = k & 1
+        with torch.cuda.stream(up):
+            if consumed[b] is not None:
+                up.wait_event(consumed[b])
+            stage[b].copy_(z_in[b], non_blocking=True)
+            uploaded[b] = torch.cuda.Event()
+            uploaded[b].record(up)
+
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    upload(0)
+    for k in range(steps):
+        b = k & 1
+        main.wait_event(uploaded[b])
+        eng.load_zip(stage[b])
+        consumed[b] = torch.cuda.Event()
+        consumed[b].record(main)
+        if k + 1 < steps:
+            upload(k + 1)
+        eng.lts_coarse_step()
+        eng.current_zip_to(z_out[b], down)
+    torch.cuda.synchronize(dev)
+    return time.perf_counter() - t0, "pipelined (upload k+1 and read-back k overlap round k)"
+
+
+def _ncu_traffic_for(name):
+    """(bytes per LTS stage launch, note) from the committed ncu capture of `name`."""
+    path = os.path.join(ROOT, "profiles", "traffic.json" if name == "cfg2" else f"traffic_{name}.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["lts_bytes_per_launch"]), (
+            f"ncu dram__bytes_read+write per LTS stage launch ({d['source']}); "
+            f"algorithmic bytes of the same launches: {d['lts_algorithmic_bytes_per_launch']:.3e}")
+    except Exception:
+        return None, f"no committed ncu capture for {name}"
+
+
+def measure(name, args, torch, dist, dev, world, clk, steps, warmup, gts_slices=None):
+    """LTS rounds, the GTS engine over the same simulated time, and the stage
+    kernel's roofline (per-launch CUDA events) on config `name`.  `gts_slices`
+    bounds the GTS sample (deep configs: a round is thousands of fine slices,
+    each the same work; the rate is scaled to the round)."""
+    from paper_2011_10570_b200.stepper import Engine
+
+    t0 = time.time()
+    cfg, mesh = build_mesh(name, world, "lts")
+    t_mesh = time.time() - t0
+    chi0 = cfg.chi0()
+    res, engines = {}, {}
+    for mode in ("lts", "gts"):
+        t0 = time.time()
+        eng = Engine(mesh, tableau=cfg.tableau, cfl=cfg.cfl, mode=mode, nonlinear=cfg.nonlinear, device=dev)
+        t_eng = time.time() - t0
+        eng.initialize(chi0)
+        engines[mode] = eng
+        units, launches = units_per_round(eng)
+        n_round = engines["lts"].schedule.slices_per_round
+        if mode == "lts":
+            for _ in range(warmup):
+                eng.lts_coarse_step()
+            with clk.window():
+                ms, _ = time_rounds(eng, steps, torch, dist)
+        else:
+            n_g = n_round * steps if gts_slices is None else min(n_round * steps, gts_slices)
+            for _ in range(min(warmup * n_round, 8 if gts_slices else warmup * n_round)):
+                eng.gts_step()
+            with clk.window():
+                if dist is not None:
+                    dist.barrier()
+                torch.cuda.synchronize(dev)
+                s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s_ev.record()
+                for _ in range(n_g):
+                    eng.gts_step()
+                e_ev.record()
+                torch.cuda.synchronize(dev)
+                if dist is not None:
+                    dist.barrier()
+            ms = s_ev.elapsed_time(e_ev) * (n_round * steps / n_g)  # scaled to `steps` rounds of simulated time
+            units, launches = units * n_round, launches * n_round
+        t = torch.tensor([ms, float(units)], dtype=torch.float64, device=dev)
+        if dist is not None:
+            tmax, tsum = t.clone(), t.clone()
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+            dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+            ms_all, units_all = float(tmax[0]), float(tsum[1])
+        else:
+            ms_all, units_all = ms, float(units)
+        res[mode] = dict(ms=ms_all, units_per_step=units_all, launches_per_step=launches, engine_build_s=t_eng)
+
+    # roofline: profiling pass (per-launch CUDA events) of both engines
+    peak, peak_src = _peaks()
+    counts = np.diff(mesh.leaf_starts)
+    roof = {}
+    for mode in ("lts", "gts"):
+        eng = engines[mode]
+        rk = eng._rank_list[0]
+        if mode == "gts" and gts_slices is not None:
+            per = []
+            _, per = time_rounds(eng, 1, torch, dist, per_launch=True, n_slices=4)
+        else:
+            _, per = time_rounds(eng, 1, torch, dist, per_launch=True)
+        # algorithmic bytes per launch = 68 B x owned nodes of the launched tiles
+        cb = np.concatenate([[0], np.cumsum(counts[rk.tiles[: rk.n_boundary]])])
+        ci = np.concatenate([[0], np.cumsum(counts[rk.tiles[rk.n_boundary:]])])
+        k_ms = sum(m for m, _, _ in per)
+        k_bytes = sum(BYTES_PER_UNIT * (cb[n] if bd else ci[n]) for _, n, bd in per)
+        roof[mode] = dict(ms=k_ms, ach=k_bytes / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0, launches=len(per))
+    traffic, traffic_note = _ncu_traffic_for(name)
+    lts, gts = res["lts"], res["gts"]
+    eng = engines["lts"]
+    out = {
+        "value": lts["units_per_step"] * steps / (lts["ms"] * 1e-3),
+        "ms_per_step": lts["ms"] / steps,
+        "config": _config(name, mesh.n_nodes, len(mesh.tree.leaves)),
+        "mesh_build_s": round(t_mesh, 2), "engine_build_s": round(lts["engine_build_s"], 2),
+        "gts": {"value": gts["units_per_step"] * steps / (gts["ms"] * 1e-3), "ms_per_step": gts["ms"] / steps,
+                "units_per_step": gts["units_per_step"],
+                "sample": "whole rounds" if gts_slices is None else f"{gts_slices} fine slices, scaled to the round"},
+        "lts_vs_gts_wall_speedup": gts["ms"] / lts["ms"],
+        # the reference's work model (perfmodel.py:52-71) and the zip-node work ratio, beside the measured speedup
+        "lts_vs_gts_model": _speedup_model(mesh, gts["units_per_step"] / lts["units_per_step"]),
+        "lts_gts_equivalent_rate": gts["units_per_step"] * steps / (lts["ms"] * 1e-3),
+        "roofline": {"bound": "hbm", "achieved": roof["lts"]["ach"], "peak": peak, "unit": "GB/s",
+                     "frac": roof["lts"]["ach"] / peak, "traffic": traffic, "traffic_note": traffic_note,
+                     "peak_source": peak_src,
+                     "kernel": f"amr_stage (stage_cross, {eng._threads} threads/CTA): fused unzip on the owned cross + RHS + zip [+ RK combine]",
+                     "bytes_per_unit": BYTES_PER_UNIT,
+                     "launches": roof["lts"]["launches"], "kernel_ms_per_round": roof["lts"]["ms"],
+                     "gts_achieved": roof["gts"]["ach"], "gts_frac": roof["gts"]["ach"] / peak},
+        "gpu_launches": int(lts["launches_per_step"] * steps),
+    }
+    return out, engines, mesh, lts
 
 
 def run_ours(args):
@@ -243,138 +413,79 @@ def run_ours(args):
         dist = None
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    from paper_2011_10570_b200.stepper import Engine
 
     clk = ClockSampler(local).start()
-    t0 = time.time()
-    cfg, mesh = build_mesh(args.config, world, "lts")
-    t_mesh = time.time() - t0
-    chi0 = cfg.chi0()
-    res = {}
-    engines = {}
-    for mode in ("lts", "gts"):
-        eng = Engine(mesh, tableau=cfg.tableau, cfl=cfg.cfl, mode=mode, nonlinear=cfg.nonlinear, device=dev)
-        eng.initialize(chi0)
-        engines[mode] = eng
-        units, launches = units_per_round(eng)
-        for _ in range(args.warmup):
-            eng.lts_coarse_step() if mode == "lts" else [eng.gts_step() for _ in range(eng.schedule.slices_per_round)]
-        with clk.window():
-            if mode == "lts":
-                ms, _ = time_rounds(eng, args.steps, torch, dist)
-            else:
-                n = engines["lts"].schedule.slices_per_round
-                if dist is not None:
-                    dist.barrier()
-                torch.cuda.synchronize(dev)
-                s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s_ev.record()
-                for _ in range(args.steps * n):
-                    eng.gts_step()
-                e_ev.record()
-                torch.cuda.synchronize(dev)
-                if dist is not None:
-                    dist.barrier()
-                ms = s_ev.elapsed_time(e_ev)
-        if mode == "gts":  # a GTS "step" covers the same simulated time: 2^dL fine slices
-            n = engines["lts"].schedule.slices_per_round
-            units, launches = units * n, launches * n
-        t = torch.tensor([ms, float(units)], dtype=torch.float64, device=dev)
-        if dist is not None:
-            tmax = t.clone()
-            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-            tsum = t.clone()
-            dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-            ms_all, units_all = float(tmax[0]), float(tsum[1])
-        else:
-            ms_all, units_all = ms, float(units)
-        res[mode] = dict(ms=ms_all, units_per_step=units_all, launches_per_step=launches)
-
-    # roofline: profiling pass (per-launch CUDA events) of the headline engine
+    m, engines, mesh, lts = measure(args.config, args, torch, dist, dev, world, clk, args.steps, args.warmup)
     eng = engines["lts"]
-    _, per = time_rounds(eng, 1, torch, None if dist is None else dist, per_launch=True)
-    counts = np.diff(mesh.leaf_starts)
-    # algorithmic bytes per launch = 68 B x owned nodes of the launched tiles
-    tiles = eng._rank_list[0].tiles
-    cum = np.concatenate([[0], np.cumsum(counts[tiles])])
-    k_ms = sum(m for m, _ in per)
-    k_bytes = sum(BYTES_PER_UNIT * cum[n] for _, n in per)
-    peak, peak_src = _peaks()
-    achieved = k_bytes / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0
-    traffic, traffic_note = _ncu_traffic()
-    # same for GTS launches (all tiles)
-    geng = engines["gts"]
-    _, gper = time_rounds(geng, 1, torch, None if dist is None else dist, per_launch=True)
-    g_ms = sum(m for m, _ in gper)
-    g_bytes = sum(BYTES_PER_UNIT * cum[n] for _, n in gper) if gper else 0.0
-    g_ach = g_bytes / (g_ms * 1e-3) / 1e9 if g_ms > 0 else 0.0
 
     # e2e through the public API with host buffers (pinned), LTS
-    z_host = torch.from_numpy(eng.current_zip()).pin_memory()
-    z_out = torch.empty_like(z_host).pin_memory()
     if dist is not None:
         dist.barrier()
-    torch.cuda.synchronize(dev)
-    te0 = time.perf_counter()
-    ew = clk.window()
-    ew.__enter__()
-    for _ in range(args.steps):
-        eng.load_zip(z_host)
-        eng.lts_coarse_step()
-        z_out.copy_(eng.current_zip_device(), non_blocking=True)
-        torch.cuda.synchronize(dev)
-    te = time.perf_counter() - te0
-    ew.__exit__(None, None, None)
-    clk.stop()
+    with clk.window():
+        te, e2e_mode = time_e2e(eng, args.steps, torch, serial=args.e2e_serial)
     tt = torch.tensor([te], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     te = float(tt[0])
+    comm = None
+    if world > 1:
+        b0 = eng.comm_bytes
+        eng.lts_coarse_step()
+        comm = {"ghost_bytes_sent_per_round_rank0": int(eng.comm_bytes - b0),
+                "ghost_leaves_rank0": int(len(eng._rank_list[0].ghosts)),
+                "local_zip_nodes_rank0": int(eng._rank_list[0].n_local)}
+    remesh = _remesh_criterion(eng) if rank == 0 and world == 1 else None
 
-    lts, gts = res["lts"], res["gts"]
-    value = lts["units_per_step"] * args.steps / (lts["ms"] * 1e-3)
-    gts_value = gts["units_per_step"] * args.steps / (gts["ms"] * 1e-3)
+    # the other single-GPU BASELINE configs, GPU only
+    side = {}
+    del engines, eng
+    torch.cuda.empty_cache()
+    for name in [x for x in args.side.split(",") if x and x != "none"]:
+        if world > 1:
+            break
+        try:
+            sm, se, _, _ = measure(name, args, torch, None, dev, 1, clk, steps=3, warmup=3,
+                                   gts_slices=64 if name in ("cfg4", "cfg5") else None)
+            side[name] = sm
+            del se
+            torch.cuda.empty_cache()
+        except Exception as exc:  # report, never hide the headline
+            side[name] = {"error": f"{type(exc).__name__}: {exc}"}
+    clk.stop()
+
     out = {
         "metric": "RK-stage zip-node updates/s (LTS, executed)",
-        "value": value,
+        "value": m["value"],
         "unit": "updates/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": lts["ms"] / args.steps,
+        "ms_per_step": m["ms_per_step"],
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": f"synthetic ({args.config} mesh and Gaussian initial data, seeded; no dataset exists for this path)",
-        "config": {
-            "workload": _workload(args.config),
-            "leaves": len(mesh.tree.leaves), "zip_nodes": mesh.n_nodes,
-            "l2_policy": "inputs larger than L2 (state u0,u1,K0..K3 = "
-                         f"{6 * 16 * mesh.n_nodes / 1e6:.0f} MB > 126 MB)",
-            "parallelism": f"weighted Morton partition x{world}" if world > 1 else "1 GPU",
-            "mesh_build_s": round(t_mesh, 2),
-        },
-        "gts": {"value": gts_value, "ms_per_step": gts["ms"] / args.steps,
-                "units_per_step": gts["units_per_step"]},
-        "lts_vs_gts_wall_speedup": gts["ms"] / lts["ms"],
-        # the reference's work model (perfmodel.py:52-71) and the zip-node work ratio, beside the measured speedup
-        "lts_vs_gts_model": _speedup_model(mesh, gts["units_per_step"] / lts["units_per_step"]),
-        "lts_gts_equivalent_rate": gts["units_per_step"] * args.steps / (lts["ms"] * 1e-3),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "traffic_note": traffic_note,
-                     "peak_source": peak_src,
-                     "kernel": f"amr_stage (stage_cross, {eng._threads} threads/CTA): fused unzip on the owned cross + RHS + zip [+ RK combine]",
-                     "bytes_per_unit": BYTES_PER_UNIT,
-                     "launches": len(per), "kernel_ms_per_round": k_ms,
-                     "gts_achieved": g_ach, "gts_frac": g_ach / peak},
+        "config": m["config"],
+        "parallelism": f"weighted Morton partition x{world}, ghost records over NCCL" if world > 1 else "1 GPU",
+        "mesh_build_s": m["mesh_build_s"], "engine_build_s": m["engine_build_s"],
+        "gts": m["gts"],
+        "lts_vs_gts_wall_speedup": m["lts_vs_gts_wall_speedup"],
+        "lts_vs_gts_model": m["lts_vs_gts_model"],
+        "lts_gts_equivalent_rate": m["lts_gts_equivalent_rate"],
+        "roofline": m["roofline"],
         "e2e": {"value": lts["units_per_step"] * args.steps / te, "unit": "updates/s",
-                "h2d_bytes_per_step": int(2 * 8 * mesh.n_nodes), "d2h_bytes_per_step": int(2 * 8 * mesh.n_nodes)},
-        "gpu_launches": int(lts["launches_per_step"] * args.steps),
+                "h2d_bytes_per_step": int(2 * 8 * mesh.n_nodes), "d2h_bytes_per_step": int(2 * 8 * mesh.n_nodes),
+                "mode": e2e_mode},
+        "gpu_launches": m["gpu_launches"],
         "clocks": clk.summary(),
     }
-    if rank == 0:
-        out["remesh_criterion"] = _remesh_criterion(eng)
+    if comm is not None:
+        out["comm"] = comm
+    if side:
+        out["other_configs"] = side
+    if remesh is not None:
+        out["remesh_criterion"] = remesh
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(args, rounds=1)
     if rank == 0:
@@ -474,7 +585,7 @@ def run_reference(args):
         "unit": "updates/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (BASELINE configs[1])",
-        "config": {"workload": _workload(args.config), "zip_nodes": m.n_nodes},
+        "config": _config(args.config, m.n_nodes, len(m.leaf_starts) - 1),
         "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": "port",
                          "sample": f"{args.steps} LTS rounds of {args.config} on the oracle port "
                                    "(the reference amrlts is pure Python and not present on the GPU box)"},
@@ -490,6 +601,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--side", default="cfg3,cfg4", help="other single-GPU configs measured GPU-only (or 'none')")
+    ap.add_argument("--e2e-serial", action="store_true", help="e2e loop without copy/compute overlap")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

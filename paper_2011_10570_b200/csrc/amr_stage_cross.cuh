@@ -27,12 +27,13 @@
 template <int DIM, int PPO>
 struct CrossK {
   using T = Tile<DIM, PPO>;
-  static constexpr int HEAD = 16 + 64 * 8;                 // 2 mbarriers, interpolation weights
+  static constexpr int BARS = 64;                          // mbarriers: one per head and per tail of the CTA's tiles
+  static constexpr int HEAD = BARS + 64 * 8;               // + interpolation weights
   static constexpr int BOXB = (T::BOX * 8 + 15) / 16 * 16;  // the stencil box (chi; phi in step 5)
   static constexpr int OWNB = (T::NI * 2 + 15) / 16 * 16;  // owned node -> box cell (uint16)
   __host__ __device__ static int slot_bytes(int max_slots) { return ((max_slots + 1) * 8 + 15) / 16 * 16; }
-  __host__ __device__ static size_t smem_bytes(int max_slots, int max_head, int max_tail) {
-    return HEAD + (size_t)max_head + (size_t)max_tail + BOXB + slot_bytes(max_slots) + OWNB;
+  __host__ __device__ static size_t smem_bytes(int max_slots, int max_head, int max_tail, int tiles_per_cta) {
+    return HEAD + (size_t)tiles_per_cta * max_head + (size_t)max_tail + BOXB + slot_bytes(max_slots) + OWNB;
   }
 };
 
@@ -402,90 +403,109 @@ __device__ __forceinline__ long long gtimer() {
   return t;
 }
 #define AMR_PROBE(i) \
-  if (P.probe && threadIdx.x == 0) P.probe[(int64_t)blockIdx.x * 8 + (i)] = gtimer()
+  if (P.probe && threadIdx.x == 0) P.probe[tile * 8 + (i)] = gtimer()
 #else
 #define AMR_PROBE(i)
 #endif
 
-// One CTA per tile.
+#ifndef AMR_TPC
+#define AMR_TPC 1  // consecutive tiles per CTA (2 and 3 measured slower: the unrolled tile bodies thrash the instruction cache)
+#endif
+
+// One CTA runs AMR_TPC consecutive tiles, one after the other.  All their
+// heads are requested up front (one bulk copy each, own mbarrier), so only the
+// first head fetch is exposed; many CTAs stay resident per SM, so tiles in
+// different phases interleave.
 template <int DIM, int PPO, bool LTS, int NT, int NTH>
 __global__ void __launch_bounds__(NTH, (NTH <= 128 ? 2 * AMR_CROSS_MINB : AMR_CROSS_MINB))
     stage_cross(const __grid_constant__ AmrStageParams P) {
   using T = Tile<DIM, PPO>;
   using CK = CrossK<DIM, PPO>;
   constexpr int OPT = (T::NI + NTH - 1) / NTH;
+  constexpr int TPC = AMR_TPC;
   extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-  double* s_w = reinterpret_cast<double*>(smem + 16);
-  unsigned char* head = smem + CK::HEAD;
-  uint16_t* s_tail = reinterpret_cast<uint16_t*>(head + P.max_head);
-  double* box = reinterpret_cast<double*>(head + P.max_head + P.max_tail);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem);  // [0, TPC): heads; [TPC, 2 TPC): tails
+  double* s_w = reinterpret_cast<double*>(smem + CK::BARS);
+  unsigned char* head0 = smem + CK::HEAD;
+  const uint32_t hb = (uint32_t)P.max_head;
+  uint16_t* s_tail = reinterpret_cast<uint16_t*>(head0 + (size_t)TPC * hb);
+  double* box = reinterpret_cast<double*>(head0 + (size_t)TPC * hb + P.max_tail);
   double* slot = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(box) + CK::BOXB);
   uint16_t* own = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(slot) + CK::slot_bytes(P.max_slots));
   const int tid = threadIdx.x;
-  AMR_PROBE(0);
+  const int64_t tile0 = (int64_t)blockIdx.x * TPC;
   // programmatic dependent launch: the next kernel on the stream may start its
   // CTAs (and fetch its static tables) while this grid drains
   pdl_launch_dependents();
 
-  // ---- 1: the head (one bulk copy at a fixed stride), weights meanwhile
+  // ---- 1: the heads (one bulk copy each at a fixed stride), weights meanwhile
   if (tid == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
+#pragma unroll
+    for (int j = 0; j < 2 * TPC; ++j) mbar_init(bar + j, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    const uint32_t hb = (uint32_t)P.max_head;
-    mbar_expect_tx(bar, hb);
-    bulk_g2s(head, P.heads + (int64_t)blockIdx.x * hb, hb, bar);
+#pragma unroll
+    for (int j = 0; j < TPC; ++j) {
+      if (tile0 + j < P.n_tiles) {
+        mbar_expect_tx(bar + j, hb);
+        bulk_g2s(head0 + (size_t)j * hb, P.heads + (tile0 + j) * hb, hb, bar + j);
+      }
+    }
   }
   // interpolation weights: in flight with the gathers (waited for with them)
   for (int i = tid; i < P.n_wtab; i += NTH) cp_async8(s_w + i, P.wtab + i);
-  __syncthreads();  // mbarrier initialised before anyone waits on it
-  mbar_wait(bar, 0);
-  // everything above reads static tables only; the fields (and the interface
-  // buffer) are the previous kernels' output
-  pdl_wait();
-  AMR_PROBE(1);
-  const TileCtx c = tile_ctx(P, head, LTS);
-  const uint32_t tail_bytes = (uint32_t)c.h[7];
-  if (tid == 0) {
-    // the tail (hanging rows, taps): one bulk copy, lands during the gathers
-    if (tail_bytes) {
-      mbar_expect_tx(bar + 1, tail_bytes);
-      bulk_g2s(s_tail, c.tl, tail_bytes, bar + 1);
+  __syncthreads();  // mbarriers initialised before anyone waits on them
+
+#pragma unroll
+  for (int j = 0; j < TPC; ++j) {
+    const int64_t tile = tile0 + j;
+    if (tile >= P.n_tiles) break;
+    AMR_PROBE(0);
+    const unsigned char* head = head0 + (size_t)j * hb;
+    mbar_wait(bar + j, 0);
+    // everything above reads static tables only; the fields (and the interface
+    // buffer) are the previous kernels' output
+    if (j == 0) pdl_wait();
+    AMR_PROBE(1);
+    const TileCtx c = tile_ctx(P, head, LTS);
+    const uint32_t tail_bytes = (uint32_t)c.h[7];
+    if (tid == 0) {
+      // the tail (hanging rows, taps): one bulk copy, lands during the gathers
+      if (tail_bytes) {
+        mbar_expect_tx(bar + TPC + j, tail_bytes);
+        bulk_g2s(s_tail, c.tl, tail_bytes, bar + TPC + j);
+      }
+      tile_prefetch(P, c);
     }
-    tile_prefetch(P, c);
+
+    // ---- 2, 3: chi on the owned cross; owned-node loads in flight meanwhile
+    cross_gather<LTS, NTH>(c.h, box, slot, own, c.V, P.ibuf, 0, 0, c.g0, true);
+    cp_async_commit();
+    AMR_PROBE(2);
+    double pc[OPT], u0[OPT], u1[OPT];
+    owned_loads<OPT, NTH>(P, c, pc, u0, u1);
+    cp_async_wait<0>();
+    __syncthreads();
+    AMR_PROBE(3);
+    if (tail_bytes) mbar_wait(bar + TPC + j, 0);
+    cross_rows<NTH>(s_tail, c.nrow, c.taps_off, s_w, slot, box);
+    __syncthreads();
+    AMR_PROBE(4);
+
+    // ---- 4: RHS at the owned nodes
+    rhs_pass1<DIM, PPO, LTS, NT, NTH, OPT>(P, c, box, own, pc, u0, u1);
+    AMR_PROBE(5);
+    if (c.faces != 0) {
+      // ---- 5: physical-face tiles: phi on the owned cross, radiative phi rows
+      __syncthreads();  // everyone is done reading chi from the box
+      cross_gather<LTS, NTH>(c.h, box, slot, own, c.V, P.ibuf, P.ld, P.n_iface_total, c.g0, false);
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+      cross_rows<NTH>(s_tail, c.nrow, c.taps_off, s_w, slot, box);
+      __syncthreads();
+      rhs_pass2<DIM, PPO, LTS, NT, NTH, OPT>(P, c, box, own, u0, u1);
+    }
+    if (j + 1 < TPC) __syncthreads();  // box, slots, own map and tail are free for the next tile
+    AMR_PROBE(6);
   }
-
-  // ---- 2, 3: chi on the owned cross; owned-node loads in flight meanwhile
-  cross_gather<LTS, NTH>(c.h, box, slot, own, c.V, P.ibuf, 0, 0, c.g0, true);
-  cp_async_commit();
-  AMR_PROBE(2);
-  double pc[OPT], u0[OPT], u1[OPT];
-  owned_loads<OPT, NTH>(P, c, pc, u0, u1);
-  cp_async_wait<0>();
-  __syncthreads();
-  AMR_PROBE(3);
-  if (tail_bytes) mbar_wait(bar + 1, 0);
-  cross_rows<NTH>(s_tail, c.nrow, c.taps_off, s_w, slot, box);
-  __syncthreads();
-  AMR_PROBE(4);
-
-  // ---- 4: RHS at the owned nodes
-  rhs_pass1<DIM, PPO, LTS, NT, NTH, OPT>(P, c, box, own, pc, u0, u1);
-  AMR_PROBE(5);
-#ifdef AMR_PHASE_PROBE
-  __syncthreads();
-  AMR_PROBE(6);
-#endif
-  if (c.faces == 0) return;
-
-  // ---- 5: physical-face tiles: phi on the owned cross, radiative phi rows
-  __syncthreads();  // everyone is done reading chi from the box
-  cross_gather<LTS, NTH>(c.h, box, slot, own, c.V, P.ibuf, P.ld, P.n_iface_total, c.g0, false);
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  cross_rows<NTH>(s_tail, c.nrow, c.taps_off, s_w, slot, box);
-  __syncthreads();
-  rhs_pass2<DIM, PPO, LTS, NT, NTH, OPT>(P, c, box, own, u0, u1);
 }

@@ -16,7 +16,7 @@ int launch_cross_one(const AmrStageParams* p, cudaStream_t st) {
   cudaGetDevice(&dev);
   if (dev >= kMaxDev) return AMR_EINVAL;
   using CK = CrossK<DIM, PPO>;
-  const size_t dyn = CK::smem_bytes(p->max_slots, p->max_head, p->max_tail);
+  const size_t dyn = CK::smem_bytes(p->max_slots, p->max_head, p->max_tail, AMR_TPC);
   static size_t configured[kMaxDev] = {0};
   if (dyn > configured[dev]) {
     cudaError_t e = cudaFuncSetAttribute(stage_cross<DIM, PPO, LTS, NT, NTH>,
@@ -24,7 +24,7 @@ int launch_cross_one(const AmrStageParams* p, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(stage_cross)");
     configured[dev] = dyn;
   }
-  return pdl_launch(stage_cross<DIM, PPO, LTS, NT, NTH>, dim3((unsigned)p->n_tiles), dim3(NTH), dyn, st, *p);
+  return pdl_launch(stage_cross<DIM, PPO, LTS, NT, NTH>, dim3((unsigned)((p->n_tiles + AMR_TPC - 1) / AMR_TPC)), dim3(NTH), dyn, st, *p);
 }
 
 template <int DIM, int PPO, bool LTS, int NTH>

@@ -861,8 +861,9 @@ class Engine:
         i = self.i_fine
         with torch.cuda.device(self.device):
             if out is None:
-                out = torch.empty((2, n), dtype=torch.float64, device=self.device) if self._dist is None else \
-                    torch.zeros((2, n), dtype=torch.float64, device=self.device)
+                out = torch.empty((2, n), dtype=torch.float64, device=self.device)
+            if self._dist is not None:
+                out.zero_()  # the other ranks' entries: summed in below
             par = [(self._cur_parity(i, c) if self._lts_kernel else i & 1) if c <= self.l_max else 0
                    for c in range(_native.AMR_MAXL)]
             st = self._stream()

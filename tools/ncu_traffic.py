@@ -16,7 +16,7 @@ def _is_lts(name: str) -> bool:
 import numpy as np
 
 
-def main(rep, out="profiles/traffic.json"):
+def main(rep, out="profiles/traffic.json", cfg="cfg2"):
     q = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
                         "dram__bytes_read.sum,dram__bytes_write.sum,launch__grid_size"],
                        capture_output=True, text=True).stdout
@@ -29,17 +29,17 @@ def main(rep, out="profiles/traffic.json"):
     for r in rows[2:]:
         if _is_lts(r[i_n]):
             lts.append((float(r[i_r]) * scale[units[i_r]] + float(r[i_w]) * scale[units[i_w]], int(float(r[i_g]))))
-    # algorithmic bytes: 68 B x owned nodes of the launched tiles (cfg2 mesh)
+    # algorithmic bytes: 68 B x owned nodes of the launched tiles
     sys.path.insert(0, ".")
     from bench import build_mesh
 
-    _, mesh = build_mesh("cfg2", 1, "lts")
+    _, mesh = build_mesh(cfg, 1, "lts")
     lv = mesh.tree.arrays()[1]
     counts = np.diff(mesh.leaf_starts)
     order = np.lexsort((np.arange(len(lv)), -lv))
     cum = np.concatenate([[0], np.cumsum(counts[order])])
     alg = [68.0 * cum[g] for _, g in lts]
-    d = {"source": rep.split("/")[-1], "lts_launches": len(lts),
+    d = {"source": rep.split("/")[-1], "config": cfg, "lts_launches": len(lts),
          "lts_bytes_per_launch": float(np.mean([b for b, _ in lts])),
          "lts_algorithmic_bytes_per_launch": float(np.mean(alg)),
          "ratio": float(np.sum([b for b, _ in lts]) / np.sum(alg))}
@@ -48,4 +48,4 @@ def main(rep, out="profiles/traffic.json"):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], *sys.argv[2:3])
+    main(sys.argv[1], *sys.argv[2:4])

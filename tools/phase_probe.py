@@ -40,13 +40,17 @@ for mode in ("gts", "lts"):
         eng._lib = lib
         torch.cuda.synchronize()
         t = buf.cpu().numpy().astype(np.float64)
-        t = t[t[:, 0] > 0]
-        t0 = t[:, 0].min()
-        life = (t[:, 6] - t[:, 0]) / 1e3
-        d = np.diff(t[:, :7], axis=1) / 1e3
+        tpc = int(os.environ.get("TPC", "1"))
+        idx = np.arange(len(t))
+        ok = t[:, 0] > 0
+        t0 = t[ok, 0].min()
+        span = (t[ok, 6].max() - t0) / 1e3
         names = ["head", "gather-issue", "gather-wait", "rows", "rhs(own)", "rhs(all)"]
-        span = (t[:, 6].max() - t0) / 1e3
-        print(f"{mode} stage {stage_of_interest}: {len(t)} tiles, span {span:.1f} us, "
-              f"mean CTA life {life.mean():.2f} us; " +
-              ", ".join(f"{n} {v:.2f}" for n, v in zip(names, d.mean(axis=0))))
+        for j in range(tpc):  # j-th tile of its CTA
+            tj = t[ok & (idx % tpc == j)]
+            life = (tj[:, 6] - tj[:, 0]) / 1e3
+            d = np.diff(tj[:, :7], axis=1) / 1e3
+            print(f"{mode} stage {stage_of_interest} tile {j}/{tpc}: {len(tj)} tiles, span {span:.1f} us, "
+                  f"mean tile life {life.mean():.2f} us; " +
+                  ", ".join(f"{n} {v:.2f}" for n, v in zip(names, d.mean(axis=0))))
     eng._prm.probe = None
