@@ -378,7 +378,7 @@ def measure(name, args, torch, dist, dev, world, clk, steps, warmup, gts_slices=
     out = {
         "value": lts["units_per_step"] * steps / (lts["ms"] * 1e-3),
         "ms_per_step": lts["ms"] / steps,
-        "config": _config(name, mesh.n_nodes, len(mesh.tree.leaves)),
+        "config": _config(name, mesh.n_nodes, len(mesh.tree)),
         "mesh_build_s": round(t_mesh, 2), "engine_build_s": round(lts["engine_build_s"], 2),
         "gts": {"value": gts["units_per_step"] * steps / (gts["ms"] * 1e-3), "ms_per_step": gts["ms"] / steps,
                 "units_per_step": gts["units_per_step"],

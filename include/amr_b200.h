@@ -52,6 +52,25 @@ AmrTree* amr_balance(int dim, int max_depth, int64_t n, const int32_t* anchors,
 int amr_tree_fetch(const AmrTree* t, int32_t* anchors_out, int32_t* levels_out);
 void amr_tree_free(AmrTree* t);
 
+/* Device octree (octree.py:249-330 on the GPU; csrc/amr_octree.cu).  An
+ * octant is the 64-bit key morton(anchor) << 6 | level; a linear octree is a
+ * sorted key array in device memory.  Refinement (construct, octree.py:249-271)
+ * and the 2:1 balance ripple (octree.py:289-330) are rounds of
+ * mark -> exclusive prefix sum of the output counts (1, or 2^dim when marked;
+ * the caller's) -> amr_oct_split, which keeps the array sorted.
+ * amr_oct_balance_mark marks every leaf that is more than one level coarser
+ * than a leaf probing it (the reference's diagonal probe cells); mark must be
+ * zero on entry; balance is reached when it stays zero.  All pointers are
+ * device pointers. */
+int amr_oct_keys(int dim, int max_depth, int64_t n, const int32_t* anchors, const int32_t* levels,
+                 uint64_t* keys, void* stream);
+int amr_oct_octants(int dim, int max_depth, int64_t n, const uint64_t* keys, int32_t* anchors,
+                    int32_t* levels, void* stream);
+int amr_oct_split(int dim, int max_depth, int64_t n, const uint64_t* keys, const int32_t* mark,
+                  const int64_t* offsets, uint64_t* out, void* stream);
+int amr_oct_balance_mark(int dim, int max_depth, int64_t n, const uint64_t* keys, int32_t* mark,
+                         void* stream);
+
 /* ------------------------------------------------------------------ mesh -- */
 
 /* Node registry + leaf-tile gather tables (mesh.py:214-398).  `owners` (may be

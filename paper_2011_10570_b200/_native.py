@@ -83,6 +83,10 @@ SIGNATURES = {
     "amr_abi_version": ([], C.c_int),
     "amr_morton_sort": ([C.c_int, C.c_int, C.c_int64, _i32p, _i32p, _i64p], C.c_int),
     "amr_balance": ([C.c_int, C.c_int, C.c_int64, _i32p, _i32p, _i64p], _vp),
+    "amr_oct_keys": ([C.c_int, C.c_int, C.c_int64, _vp, _vp, _vp, _vp], C.c_int),
+    "amr_oct_octants": ([C.c_int, C.c_int, C.c_int64, _vp, _vp, _vp, _vp], C.c_int),
+    "amr_oct_split": ([C.c_int, C.c_int, C.c_int64, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "amr_oct_balance_mark": ([C.c_int, C.c_int, C.c_int64, _vp, _vp, _vp], C.c_int),
     "amr_tree_fetch": ([_vp, _i32p, _i32p], C.c_int),
     "amr_tree_free": ([_vp], None),
     "amr_mesh_build": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, _i32p, _i32p, _i32p, C.c_int], _vp),

@@ -1,7 +1,7 @@
 """Build the native library in-tree: paper_2011_10570_b200/_lib/libamr_b200.so.
 
 One nvcc per source (in parallel) compiles the sm_100a kernels (amr_kernels.cu,
-amr_wavelet.cu) and the host C++ mesh builder (amr_mesh.cpp); one link makes
+amr_wavelet.cu, amr_octree.cu) and the host C++ mesh builder (amr_mesh.cpp); one link makes
 the C-ABI shared library that Python loads with ctypes.  Flags that matter for parity:
   -fmad=false            no FMA contraction in device code (numpy rounds every op)
   -ffp-contract=off      same for the host C++ (interpolation weights)
@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libamr_b200.so")
 INCLUDE = os.path.abspath(os.path.join(HERE, "..", "include"))
-SOURCES = ["amr_kernels.cu", "amr_wavelet.cu", "amr_mesh.cpp", "amr_programs.cpp"]
+SOURCES = ["amr_kernels.cu", "amr_wavelet.cu", "amr_octree.cu", "amr_mesh.cpp", "amr_programs.cpp"]
 # the stage-kernel launcher, compiled once per (dim, ppo, lts) in parallel
 INSTANCES = [(d, p, l) for d in (2, 3) for p in (5, 7, 9) for l in (0, 1)]
 INST_SRC = "amr_stage_inst.cu"

@@ -34,6 +34,25 @@ def box_dist2_batch(anchors: np.ndarray, level: int, max_depth: int, center, lo=
     return d2
 
 
+def box_dist2_device(anchors, level: int, max_depth: int, center, lo=-1.0, hi=1.0):
+    """box_dist2_batch on a CUDA int32 (n, dim) anchor tensor: the same float64
+    operations in the same order (torch elementwise ops are correctly rounded
+    like numpy's), so the decisions are identical."""
+    import torch
+
+    scale = (hi - lo) / (1 << max_depth)
+    side = 1 << (max_depth - level)
+    d2 = torch.zeros(anchors.shape[0], dtype=torch.float64, device=anchors.device)
+    zero = torch.zeros((), dtype=torch.float64, device=anchors.device)
+    for d, c in enumerate(center[: anchors.shape[1]]):
+        a = anchors[:, d].to(torch.float64)
+        m = lo + a * scale - c
+        M = lo + (anchors[:, d].to(torch.int64) + side).to(torch.float64) * scale - c
+        inside = (m <= 0.0) & (0.0 <= M)
+        d2 = d2 + torch.where(inside, zero, torch.minimum(m * m, M * M))
+    return d2
+
+
 def box_dist2(key, center, lo: float = -1.0, hi: float = 1.0) -> float:
     """Squared distance from ``center`` to the octant's closed box (same
     arithmetic as the reference test predicate, test_stepper.py:22-25)."""
@@ -85,6 +104,20 @@ class BandRefine:
             tgt = np.where((d2 < rad * rad) & (lvl > tgt), lvl, tgt)
         return level < tgt
 
+    def batch_device(self, anchors, level: int, max_depth: int):
+        import torch
+
+        if level < self.base:
+            return torch.ones(anchors.shape[0], dtype=torch.bool, device=anchors.device)
+        d2 = None
+        for c in self.centers:
+            e = box_dist2_device(anchors, level, max_depth, c, self.lo, self.hi)
+            d2 = e if d2 is None else torch.minimum(d2, e)
+        tgt = torch.full((anchors.shape[0],), self.base, dtype=torch.int64, device=anchors.device)
+        for rad, lvl in self.bands:
+            tgt = torch.where((d2 < rad * rad) & (lvl > tgt), torch.full_like(tgt, lvl), tgt)
+        return level < tgt
+
 
 @dataclass(frozen=True)
 class SphereSeeds:
@@ -111,6 +144,17 @@ class SphereSeeds:
         for c, r, lvl in self.spheres:
             if level < lvl:
                 out |= box_dist2_batch(anchors, level, max_depth, c, self.lo, self.hi) < r * r
+        return out
+
+    def batch_device(self, anchors, level: int, max_depth: int):
+        import torch
+
+        if level < self.base:
+            return torch.ones(anchors.shape[0], dtype=torch.bool, device=anchors.device)
+        out = torch.zeros(anchors.shape[0], dtype=torch.bool, device=anchors.device)
+        for c, r, lvl in self.spheres:
+            if level < lvl:
+                out |= box_dist2_device(anchors, level, max_depth, c, self.lo, self.hi) < r * r
         return out
 
 
@@ -147,6 +191,21 @@ class GradedSpheres:
         out = np.zeros(len(anchors), dtype=bool)
         for c, r, lt in self._targets():
             d2 = box_dist2_batch(anchors, level, max_depth, c, self.lo, self.hi)
+            for k in range(8):
+                if level < lt - k:
+                    out |= d2 < (r * 2 ** k) ** 2
+        return out
+
+    def batch_device(self, anchors, level: int, max_depth: int):
+        import torch
+
+        if level < self.base:
+            return torch.ones(anchors.shape[0], dtype=torch.bool, device=anchors.device)
+        out = torch.zeros(anchors.shape[0], dtype=torch.bool, device=anchors.device)
+        for c, r, lt in self._targets():
+            if level >= lt:
+                continue
+            d2 = box_dist2_device(anchors, level, max_depth, c, self.lo, self.hi)
             for k in range(8):
                 if level < lt - k:
                     out |= d2 < (r * 2 ** k) ** 2

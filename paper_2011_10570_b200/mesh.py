@@ -76,7 +76,7 @@ class Block:
 def decompose_blocks(tree: LinearOctree, points_per_octant: int = 7, pad: int = 2,
                      pmap: PartitionMap | None = None) -> list[Block]:
     """Maximal uniform blocks split at rank cuts (mesh.py:87-135), native recursion."""
-    owners = pmap.owners(len(tree.leaves)) if pmap is not None else np.zeros(len(tree.leaves), dtype=int)
+    owners = pmap.owners(len(tree)) if pmap is not None else np.zeros(len(tree), dtype=int)
     return _blocks_from_native(_NativeMesh(tree, points_per_octant, 2, owners, registry=False), tree,
                                points_per_octant, pad)
 
@@ -144,14 +144,14 @@ class Mesh:
             domain = Domain((0.0,) * self.dim, (float(1 << self.L),) * self.dim)
         self.domain = domain
         if pmap is None:
-            w = np.ones(len(tree.leaves))
-            pmap = PartitionMap([(0, len(tree.leaves))], w, np.array([float(len(tree.leaves))]))
+            w = np.ones(len(tree))
+            pmap = PartitionMap([(0, len(tree))], w, np.array([float(len(tree))]))
         self.pmap = pmap
-        owners = pmap.owners(len(tree.leaves))
+        owners = pmap.owners(len(tree))
         self._nm = _NativeMesh(tree, points_per_octant, pad, owners)
         L = self._nm.lib
         self.blocks = _blocks_from_native(self._nm, tree, points_per_octant, pad)
-        n_leaves = len(tree.leaves)
+        n_leaves = len(tree)
         self.leaf_block = np.empty(n_leaves, dtype=int)
         for b in self.blocks:
             self.leaf_block[b.leaf_range[0]: b.leaf_range[1]] = b.index
@@ -173,7 +173,7 @@ class Mesh:
     @property
     def leaf_gids(self) -> np.ndarray:
         if self._leaf_gids is None:
-            g = np.empty((len(self.tree.leaves), self.ppo ** self.dim), dtype=np.int32)
+            g = np.empty((len(self.tree), self.ppo ** self.dim), dtype=np.int32)
             _native.check(self._nm.lib.amr_mesh_leaf_gids(self._nm.h, _native.ptr(g, C.c_int32)), "leaf_gids")
             self._leaf_gids = g.astype(np.int64)
         return self._leaf_gids
@@ -316,7 +316,7 @@ class Mesh:
         nvars = block_arrays[0].shape[0]
         out = np.empty((nvars, self.n_nodes))
         zp = self.zip_positions
-        for i in range(len(self.tree.leaves)):
+        for i in range(len(self.tree)):
             a, b = self.leaf_slices[i]
             if b == a:
                 continue
@@ -371,7 +371,7 @@ class Mesh:
         """Leaf-tile unzip tables for the stage kernel (see include/amr_b200.h)."""
         if self._tile is None:
             L = self._nm.lib
-            n = len(self.tree.leaves)
+            n = len(self.tree)
             E = int(L.amr_tile_entries(self.dim, self.ppo))
             table = np.empty((n, E), dtype=np.int32)
             _native.check(L.amr_mesh_tile_table(self._nm.h, _native.ptr(table, C.c_int32)), "tile_table")

@@ -675,7 +675,7 @@ class Engine:
             self.device = torch.device("cuda", torch.cuda.current_device())
         self._lib = _native.lib()
         self._threads = int(os.environ.get("AMR_THREADS", "256"))
-        n_leaves = len(mesh.tree.leaves)
+        n_leaves = len(mesh.tree)
         leaf_cad = np.empty(n_leaves, dtype=np.int32)
         for b in mesh.blocks:
             leaf_cad[b.leaf_range[0]: b.leaf_range[1]] = cadence[b.index]
