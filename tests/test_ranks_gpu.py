@@ -106,6 +106,15 @@ def test_profile_phase_buckets(cuda):
     eng.lts_coarse_step()
     ms = eng.phase_ms()
     assert ms["rhs"] > 0 and ms["time_interp"] > 0 and ms["comm"] > 0
+    from paper_2011_10570_b200 import report
+
+    row = report.phase_row(eng)
+    assert row[0] == 2 and row[1] == 0.0 and row[3] == ms["rhs"]
+    work = report.work_rows(eng)
+    nb = {lvl: sum(1 for b in eng.mesh.blocks if b.leaf_level == lvl) for lvl in (3, 4, 5, 6)}
+    assert [w[0] for w in work] == [3, 4, 5, 6]
+    assert [w[2] for w in work] == [nb[lvl] * (1 << (lvl - 3)) for lvl in (3, 4, 5, 6)]  # block-steps of one round
+    assert report.parse_csv(report.to_csv(report.PHASES, [row]))[0] == list(report.PHASES)
 
 
 WORKER = r"""
