@@ -81,6 +81,40 @@ typedef struct AmrMesh AmrMesh;
 AmrMesh* amr_mesh_build(int dim, int max_depth, int ppo, int pad, int64_t n_leaves,
                         const int32_t* anchors, const int32_t* levels, const int32_t* owners,
                         int n_threads);
+/* The same tables built on the device (csrc/amr_devmesh.cu; all pointers are
+ * device pointers; keys = the tree's sorted 64-bit keys, amr_oct_keys).  The
+ * passes of amr_mesh_build, one launch each:
+ *   amr_dm_ownership  status[n][ppo^dim] (1 owned, 0 shared, -1 hanging), owner leaf, owned count per leaf;
+ *   amr_dm_gids       leaf_gids from the exclusive prefix sum `starts` of the counts (the caller's);
+ *   amr_dm_table      tile table with -2 at hanging points, and their number per leaf;
+ *   amr_dm_hang_list  (table position, lattice code) of every hanging entry, at the exclusive prefix sum hang_off;
+ *   amr_dm_table_rows table[pos] = -2 - row, row = index of the code among the sorted unique codes (the caller's);
+ *   amr_dm_rows       interpolation rows of those codes: with row_ptr == NULL the tap counts, else the
+ *                     gid-sorted taps at row_ptr (exclusive prefix sum of the counts).
+ * err (device int, zero on entry) collects: 1 point outside every leaf, 2 row longer than 128 taps,
+ * 4 hanging taps nested deeper than 6.  amr_mesh_from_tables wraps host copies of the results in a
+ * mesh handle (blocks, views and the program builder work as after amr_mesh_build). */
+int amr_dm_ownership(int dim, int max_depth, int ppo, int pad, int64_t n, const uint64_t* keys,
+                     const int32_t* anchors, const int32_t* levels, int8_t* status, int32_t* owner,
+                     int64_t* counts, int* err, void* stream);
+int amr_dm_gids(int dim, int max_depth, int ppo, int pad, int64_t n, const uint64_t* keys, const int32_t* anchors,
+                const int32_t* levels, const int8_t* status, const int32_t* owner, const int64_t* starts,
+                int32_t* leaf_gids, void* stream);
+int amr_dm_table(int dim, int max_depth, int ppo, int pad, int64_t n, const uint64_t* keys, const int32_t* anchors,
+                 const int32_t* levels, const int32_t* leaf_gids, int32_t* table, int32_t* n_hang, void* stream);
+int amr_dm_hang_list(int dim, int max_depth, int ppo, int pad, int64_t n, const uint64_t* keys,
+                     const int32_t* anchors, const int32_t* levels, const int32_t* table, const int64_t* hang_off,
+                     int64_t* pos, int64_t* code, void* stream);
+int amr_dm_table_rows(int64_t n_hang, const int64_t* pos, const int64_t* code, int64_t n_rows, const int64_t* rows,
+                      int32_t* table, void* stream);
+int amr_dm_rows(int dim, int max_depth, int ppo, int pad, int64_t n, const uint64_t* keys, const int32_t* anchors,
+                const int32_t* levels, const int32_t* leaf_gids, int64_t n_rows, const int64_t* codes,
+                const int64_t* row_ptr, int32_t* counts, int32_t* gid_out, double* w_out, int* err, void* stream);
+AmrMesh* amr_mesh_from_tables(int dim, int max_depth, int ppo, int pad, int64_t n_leaves, const int32_t* anchors,
+                              const int32_t* levels, const int32_t* owners, const int64_t* starts,
+                              const int32_t* leaf_gids, const int32_t* table, int64_t n_rows,
+                              const int64_t* hang_codes, const int64_t* row_ptr, const int32_t* gid,
+                              const double* w);
 void amr_mesh_free(AmrMesh* m);
 
 int64_t amr_mesh_n_nodes(const AmrMesh* m);

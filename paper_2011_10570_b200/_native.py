@@ -90,6 +90,15 @@ SIGNATURES = {
     "amr_tree_fetch": ([_vp, _i32p, _i32p], C.c_int),
     "amr_tree_free": ([_vp], None),
     "amr_mesh_build": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, _i32p, _i32p, _i32p, C.c_int], _vp),
+    "amr_dm_ownership": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64] + [_vp] * 8, C.c_int),
+    "amr_dm_gids": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64] + [_vp] * 8, C.c_int),
+    "amr_dm_table": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64] + [_vp] * 7, C.c_int),
+    "amr_dm_hang_list": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64] + [_vp] * 8, C.c_int),
+    "amr_dm_table_rows": ([C.c_int64, _vp, _vp, C.c_int64, _vp, _vp, _vp], C.c_int),
+    "amr_dm_rows": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, _vp, _vp, _vp, _vp, C.c_int64] + [_vp] * 7,
+                    C.c_int),
+    "amr_mesh_from_tables": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int64, _i32p, _i32p, _i32p, _i64p, _i32p,
+                              _i32p, C.c_int64, _i64p, _i64p, _i32p, _f64p], _vp),
     "amr_mesh_free": ([_vp], None),
     "amr_mesh_n_nodes": ([_vp], C.c_int64),
     "amr_mesh_leaf_starts": ([_vp, _i64p], C.c_int),

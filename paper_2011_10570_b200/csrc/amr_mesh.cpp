@@ -720,6 +720,59 @@ extern "C" AmrMesh* amr_mesh_build(int dim, int L, int ppo, int pad, int64_t n_l
   return m;
 }
 
+// A mesh handle around tables built elsewhere (the device builder,
+// amr_devmesh.cu): the registry, tile table and interpolation rows are taken
+// as given; the Morton index, blocks and the lazy API gathers work as after
+// amr_mesh_build.
+extern "C" AmrMesh* amr_mesh_from_tables(int dim, int L, int ppo, int pad, int64_t n_leaves,
+                                         const int32_t* anchors, const int32_t* levels, const int32_t* owners,
+                                         const int64_t* starts, const int32_t* leaf_gids, const int32_t* table,
+                                         int64_t n_rows, const int64_t* hang_codes, const int64_t* iptr,
+                                         const int32_t* igid, const double* iw) {
+  if ((dim != 2 && dim != 3) || ppo < 5 || ppo % 2 == 0 || pad != 2) {
+    fail(AMR_EINVAL, "amr_mesh_from_tables: dim 2/3, odd ppo >= 5, pad 2");
+    return nullptr;
+  }
+  AmrMesh* m = new AmrMesh();
+  m->dim = dim;
+  m->L = L;
+  m->ppo = ppo;
+  m->pad = pad;
+  m->scale = ppo - 1;
+  m->top_nodes = (int64_t)m->scale << L;
+  m->n_leaves = n_leaves;
+  m->per_leaf = ipow(ppo, dim);
+  m->nthreads = omp_get_max_threads();
+  m->anchor.assign(n_leaves * 3, 0);
+  m->level.assign(levels, levels + n_leaves);
+  m->owner.assign(n_leaves, 0);
+  for (int64_t i = 0; i < n_leaves; ++i) {
+    for (int d = 0; d < dim; ++d) m->anchor[i * 3 + d] = anchors[i * dim + d];
+    if (owners) m->owner[i] = owners[i];
+  }
+  std::vector<std::pair<uint64_t, int32_t>> kv(n_leaves);
+  for (int64_t i = 0; i < n_leaves; ++i) kv[i] = {morton_code(&m->anchor[i * 3], dim, L), (int32_t)i};
+  std::sort(kv.begin(), kv.end());
+  m->mcodes.resize(n_leaves);
+  m->mperm.resize(n_leaves);
+  for (int64_t i = 0; i < n_leaves; ++i) {
+    m->mcodes[i] = kv[i].first;
+    m->mperm[i] = kv[i].second;
+  }
+  m->starts.assign(starts, starts + n_leaves + 1);
+  m->n_nodes = m->starts[n_leaves];
+  m->leaf_gids.assign(leaf_gids, leaf_gids + (size_t)n_leaves * m->per_leaf);
+  m->E = amr_tile_entries(dim, ppo);
+  m->table.assign(table, table + (size_t)n_leaves * m->E);
+  m->hang_codes.assign(hang_codes, hang_codes + n_rows);
+  m->iptr.assign(iptr, iptr + n_rows + 1);
+  m->igid.assign(igid, igid + m->iptr.back());
+  m->iw.assign(iw, iw + m->iptr.back());
+  int32_t root[3] = {0, 0, 0};
+  if (n_leaves > 0) decompose(m, root, 0, 0, n_leaves);
+  return m;
+}
+
 extern "C" void amr_mesh_free(AmrMesh* m) { delete m; }
 
 // read-only views for the program builder (amr_programs.cpp)

@@ -81,16 +81,102 @@ def decompose_blocks(tree: LinearOctree, points_per_octant: int = 7, pad: int = 
                                points_per_octant, pad)
 
 
-class _NativeMesh:
-    """Owning handle around AmrMesh*."""
+def device_tables(tree: LinearOctree, ppo: int, pad: int, device) -> dict:
+    """Node registry, leaf-tile table and interpolation rows of a Morton-ordered
+    balanced tree, built on the device (csrc/amr_devmesh.cu; the passes of
+    mesh.py:214-398).  Returns device tensors: ``starts`` (leaf_slices),
+    ``leaf_gids`` [n, ppo^dim], ``table`` [n, E], the sorted lattice ``codes`` of
+    the hanging points and their rows as CSR (``row_ptr``, ``gid``, ``w``).
+    Prefix sums and the sort/unique of the codes are torch's (cub)."""
+    import torch
 
-    def __init__(self, tree: LinearOctree, ppo: int, pad: int, owners, registry: bool = True):
+    L = _native.lib()
+    dim, depth = tree.dim, tree.max_depth
+    an, lv = tree.arrays()
+    n = len(lv)
+    P = ppo ** dim
+    E = int(L.amr_tile_entries(dim, ppo))
+    with torch.cuda.device(device):
+        st = torch.cuda.current_stream(device).cuda_stream
+        a_d = torch.from_numpy(np.ascontiguousarray(an, dtype=np.int32)).to(device)
+        l_d = torch.from_numpy(np.ascontiguousarray(lv, dtype=np.int32)).to(device)
+        keys = torch.empty(n, dtype=torch.int64, device=device)
+        _native.check(L.amr_oct_keys(dim, depth, n, a_d.data_ptr(), l_d.data_ptr(), keys.data_ptr(), st), "amr_oct_keys")
+        if n > 1 and not bool(torch.all(keys[1:] > keys[:-1])):
+            raise ValueError("leaves are not in Morton order: not a valid linear octree for the device builder")
+        geo = (dim, depth, ppo, pad, n, keys.data_ptr(), a_d.data_ptr(), l_d.data_ptr())
+        err = torch.zeros(1, dtype=torch.int32, device=device)
+        status = torch.empty((n, P), dtype=torch.int8, device=device)
+        owner = torch.empty((n, P), dtype=torch.int32, device=device)
+        counts = torch.empty(n, dtype=torch.int64, device=device)
+        _native.check(L.amr_dm_ownership(*geo, status.data_ptr(), owner.data_ptr(), counts.data_ptr(),
+                                         err.data_ptr(), st), "amr_dm_ownership")
+        if int(err[0]):
+            raise ValueError("leaf point outside every leaf: tree is not complete")
+        starts = torch.zeros(n + 1, dtype=torch.int64, device=device)
+        torch.cumsum(counts, 0, out=starts[1:])
+        if int(starts[-1]) >= 2 ** 31:
+            raise ValueError("more than 2^31 zip nodes: int32 gids overflow")
+        leaf_gids = torch.empty((n, P), dtype=torch.int32, device=device)
+        _native.check(L.amr_dm_gids(*geo, status.data_ptr(), owner.data_ptr(), starts.data_ptr(),
+                                    leaf_gids.data_ptr(), st), "amr_dm_gids")
+        del status, owner
+        table = torch.empty((n, E), dtype=torch.int32, device=device)
+        n_hang = torch.empty(n, dtype=torch.int32, device=device)
+        _native.check(L.amr_dm_table(*geo, leaf_gids.data_ptr(), table.data_ptr(), n_hang.data_ptr(), st),
+                      "amr_dm_table")
+        hang_end = torch.cumsum(n_hang.to(torch.int64), 0)
+        total_h = int(hang_end[-1]) if n else 0
+        hang_off = hang_end - n_hang
+        pos = torch.empty(max(total_h, 1), dtype=torch.int64, device=device)
+        code = torch.empty(max(total_h, 1), dtype=torch.int64, device=device)
+        _native.check(L.amr_dm_hang_list(*geo, table.data_ptr(), hang_off.data_ptr(), pos.data_ptr(),
+                                         code.data_ptr(), st), "amr_dm_hang_list")
+        codes = torch.unique(code[:total_h])  # sorted
+        nr = codes.numel()
+        _native.check(L.amr_dm_table_rows(total_h, pos.data_ptr(), code.data_ptr(), nr, codes.data_ptr(),
+                                          table.data_ptr(), st), "amr_dm_table_rows")
+        del pos, code
+        cnt = torch.empty(max(nr, 1), dtype=torch.int32, device=device)
+        _native.check(L.amr_dm_rows(*geo, leaf_gids.data_ptr(), nr, codes.data_ptr(), None, cnt.data_ptr(), None, None,
+                                    err.data_ptr(), st), "amr_dm_rows")
+        row_ptr = torch.zeros(nr + 1, dtype=torch.int64, device=device)
+        if nr:
+            torch.cumsum(cnt[:nr].to(torch.int64), 0, out=row_ptr[1:])
+        nnz = int(row_ptr[-1])
+        gid = torch.empty(max(nnz, 1), dtype=torch.int32, device=device)
+        w = torch.empty(max(nnz, 1), dtype=torch.float64, device=device)
+        _native.check(L.amr_dm_rows(*geo, leaf_gids.data_ptr(), nr, codes.data_ptr(), row_ptr.data_ptr(), cnt.data_ptr(),
+                                    gid.data_ptr(), w.data_ptr(), err.data_ptr(), st), "amr_dm_rows")
+        e = int(err[0])
+        if e:
+            raise ValueError("device mesh builder: " + ("lattice point outside the domain during interpolation"
+                                                        if e & 1 else "interpolation row exceeds the builder's limits"))
+    return dict(starts=starts, leaf_gids=leaf_gids, table=table, codes=codes, row_ptr=row_ptr, gid=gid[:nnz], w=w[:nnz])
+
+
+class _NativeMesh:
+    """Owning handle around AmrMesh*: built by the host passes (amr_mesh_build),
+    or around tables built on the device (``device=...``, Morton order)."""
+
+    def __init__(self, tree: LinearOctree, ppo: int, pad: int, owners, registry: bool = True, device=None):
         anchors, levels = tree.arrays()
         self.lib = _native.lib()
         own = np.ascontiguousarray(owners, dtype=np.int32)
-        self.h = self.lib.amr_mesh_build(tree.dim, tree.max_depth, ppo, pad, len(levels),
-                                         _native.ptr(anchors, C.c_int32), _native.ptr(levels, C.c_int32),
-                                         _native.ptr(own, C.c_int32), 0)
+        self.on_device = device is not None
+        if device is not None:
+            t = device_tables(tree, ppo, pad, device)
+            h = {k: np.ascontiguousarray(v.cpu().numpy()) for k, v in t.items()}
+            p32, p64 = (lambda a: _native.ptr(a, C.c_int32)), (lambda a: _native.ptr(a, C.c_int64))
+            self.h = self.lib.amr_mesh_from_tables(
+                tree.dim, tree.max_depth, ppo, pad, len(levels), p32(anchors), p32(levels), p32(own),
+                p64(h["starts"]), p32(h["leaf_gids"]), p32(h["table"]), len(h["codes"]), p64(h["codes"]),
+                p64(h["row_ptr"]), p32(h["gid"] if len(h["gid"]) else np.zeros(1, np.int32)),
+                _native.ptr(h["w"] if len(h["w"]) else np.zeros(1), C.c_double))
+        else:
+            self.h = self.lib.amr_mesh_build(tree.dim, tree.max_depth, ppo, pad, len(levels),
+                                             _native.ptr(anchors, C.c_int32), _native.ptr(levels, C.c_int32),
+                                             _native.ptr(own, C.c_int32), 0)
         if not self.h:
             raise ValueError(_native.last_error())
 
@@ -148,7 +234,17 @@ class Mesh:
             pmap = PartitionMap([(0, len(tree))], w, np.array([float(len(tree))]))
         self.pmap = pmap
         owners = pmap.owners(len(tree))
-        self._nm = _NativeMesh(tree, points_per_octant, pad, owners)
+        # registry, tile tables and interpolation rows: on the device when there is one
+        # (Morton order), else the host passes; both give the same tables
+        # (tests/test_devmesh_gpu.py).  AMR_HOST_MESH=1 forces the host builder.
+        import os
+
+        from .octree import _device
+
+        dev = None if os.environ.get("AMR_HOST_MESH") == "1" else _device()
+        if dev is not None and (tree.ordering.kind != "morton" or tree.dim * tree.max_depth > 57):
+            dev = None
+        self._nm = _NativeMesh(tree, points_per_octant, pad, owners, device=dev)
         L = self._nm.lib
         self.blocks = _blocks_from_native(self._nm, tree, points_per_octant, pad)
         n_leaves = len(tree)

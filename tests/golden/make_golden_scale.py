@@ -125,7 +125,9 @@ def make_fields(names):
                 data[key + "__max"] = np.max(np.abs(z), axis=1)
                 print(name, key, "max", data[key + "__max"], round(time.time() - t1, 1), "s", flush=True)
             del e
-        np.savez_compressed(os.path.join(HERE, f"scale_{name}.npz"), **data)
+        # AMR_GOLDEN_OUT: write elsewhere (cfg4 needs more host memory than this container has: it is
+        # generated on the GPU box, whose copy of the repo is scratch, and brought back in gpurun_out/)
+        np.savez_compressed(os.path.join(os.environ.get("AMR_GOLDEN_OUT", HERE), f"scale_{name}.npz"), **data)
         del m
 
 
