@@ -154,6 +154,47 @@ int amr_programs_fetch(const AmrProg* p, uint8_t* heads, uint16_t* tail, int32_t
                        double* wtab);
 void amr_programs_free(AmrProg* p);
 
+/* The same programs built on the device (csrc/amr_devprog.cu), byte-identical
+ * to amr_programs_build.  All pointers are device pointers.  cell / cell2e /
+ * pos are the cross-entry lookup tables of tileprog.cross_cells (box cell of an
+ * entry, its inverse, interior positions [NI][3]); ukeys / grp_start / wtab
+ * are filled in by the caller between the passes (sort/unique of the candidate
+ * keys and of the used rows' weights):
+ *   amr_dp_need    need[n_tiles][E], row_used[n_rows], n_keys[n_tiles];
+ *   amr_dp_keys    candidate keys at the exclusive prefix offsets key_off;
+ *   amr_dp_encode  heads == NULL: sizes[n_tiles][5] = head bytes, tail bytes, slots, rows, cells;
+ *                  else heads at stride max_head and tails at tail_off (bytes, 16-aligned).
+ * Kernels run `blocks` x `threads` threads over the tiles; scratch holds
+ * amr_dp_scratch_bytes(blocks * threads).  err bits: 1 > 1022 slots, 2 > 63
+ * source groups, 4 offset >= 1024, 8 > 1023 rows, 16 row word overflow. */
+typedef struct {
+  int dim, max_depth, ppo, lts, row_stride, n_wtab, max_bases;
+  int64_t n_leaves, n_tiles, n_iface;
+  const int32_t* table;
+  const int64_t* starts;
+  const int32_t* anchors;   /* [n_leaves][dim] */
+  const int32_t* levels;
+  const int32_t* leaf_cad;
+  const int32_t* tiles;
+  const int64_t* row_ptr;
+  const int32_t* gid;
+  const double* w;
+  const int32_t* cell;
+  const int32_t* cell2e;
+  const int16_t* pos;
+  const int64_t* ukeys;
+  const int64_t* grp_start;
+  const double* wtab;
+} AmrDevProg;
+int amr_dp_scratch_bytes(int threads_total, int64_t* bytes);
+int amr_dp_need(const AmrDevProg* a, uint8_t* need, uint8_t* row_used, int64_t* n_keys, int blocks, int threads,
+                void* stream);
+int amr_dp_keys(const AmrDevProg* a, const uint8_t* need, const int64_t* key_off, int64_t* keys, int blocks,
+                int threads, void* stream);
+int amr_dp_encode(const AmrDevProg* a, const uint8_t* need, void* scratch, int64_t* sizes, uint8_t* heads,
+                  int64_t max_head, const int64_t* tail_off, uint16_t* tail, int* err, int blocks, int threads,
+                  void* stream);
+
 /* Public maximal blocks (decompose_blocks, mesh.py:87-135) */
 int64_t amr_mesh_n_blocks(const AmrMesh* m);
 int amr_mesh_blocks(const AmrMesh* m, int32_t* root_anchor, int32_t* root_level,
@@ -208,7 +249,10 @@ typedef struct {
   int64_t n_iface_total;
   const int32_t* if_gid;
   const int32_t* if_cad;       /* reader cadence | source cadence << 8 */
-  double* ibuf;                /* [2][n_iface_total] */
+  double* ibuf;                /* [2][n_iface_total]: the slab of this stage, read by amr_stage */
+  double* ibuf0;               /* [n_stages][2][n_iface_total]: all slabs, written by amr_iface */
+  int if_phase;                /* amr_iface: 0 every pair for this stage; 1 (stage 0) also all stages of the
+                                  pairs whose source is not stepping now; 2 (later stages) skip those pairs */
   int n_vt;                    /* verbatim stage-source terms of stage s+1 (a[s+1][j] != 0) */
   int vt_j[AMR_MAXP];          /* their j */
   double* Y;                   /* [2 buffers][2][ld]: verbatim sources; stage s reads buffer s&1 and its

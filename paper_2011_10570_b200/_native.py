@@ -42,7 +42,7 @@ class AmrStageParams(C.Structure):
         ("n_tiles", C.c_int64), ("n_nodes", C.c_int64), ("ld", C.c_int64),
         ("heads", _vp), ("tail", _vp), ("max_head", C.c_int), ("max_tail", C.c_int), ("max_slots", C.c_int), ("threads", C.c_int), ("probe", _vp),
         ("wtab", _vp), ("n_wtab", C.c_int),
-        ("n_iface", C.c_int64), ("n_iface_total", C.c_int64), ("if_gid", _vp), ("if_cad", _vp), ("ibuf", _vp),
+        ("n_iface", C.c_int64), ("n_iface_total", C.c_int64), ("if_gid", _vp), ("if_cad", _vp), ("ibuf", _vp), ("ibuf0", _vp), ("if_phase", C.c_int),
         ("n_vt", C.c_int), ("vt_j", C.c_int * AMR_MAXP), ("Y", _vp),
         ("U0", _vp), ("U1", _vp), ("K", _vp),
         ("coef", _vp),
@@ -65,6 +65,17 @@ class AmrStageParams(C.Structure):
 
 
 AMR_GHOST_ROWS = 8
+
+
+class AmrDevProg(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int), ("max_depth", C.c_int), ("ppo", C.c_int), ("lts", C.c_int), ("row_stride", C.c_int),
+        ("n_wtab", C.c_int), ("max_bases", C.c_int),
+        ("n_leaves", C.c_int64), ("n_tiles", C.c_int64), ("n_iface", C.c_int64),
+        ("table", _vp), ("starts", _vp), ("anchors", _vp), ("levels", _vp), ("leaf_cad", _vp), ("tiles", _vp),
+        ("row_ptr", _vp), ("gid", _vp), ("w", _vp), ("cell", _vp), ("cell2e", _vp), ("pos", _vp),
+        ("ukeys", _vp), ("grp_start", _vp), ("wtab", _vp),
+    ]
 
 
 class AmrGhostMove(C.Structure):
@@ -114,6 +125,11 @@ SIGNATURES = {
     "amr_programs_info": ([_vp, _i64p], C.c_int),
     "amr_programs_fetch": ([_vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "amr_programs_free": ([_vp], None),
+    "amr_dp_scratch_bytes": ([C.c_int, _i64p], C.c_int),
+    "amr_dp_need": ([C.POINTER(AmrDevProg), _vp, _vp, _vp, C.c_int, C.c_int, _vp], C.c_int),
+    "amr_dp_keys": ([C.POINTER(AmrDevProg), _vp, _vp, _vp, C.c_int, C.c_int, _vp], C.c_int),
+    "amr_dp_encode": ([C.POINTER(AmrDevProg), _vp, _vp, _vp, _vp, C.c_int64, _vp, _vp, _vp, C.c_int, C.c_int, _vp],
+                      C.c_int),
     "amr_mesh_blocks": ([_vp, _i32p, _i32p, _i32p, _i64p, _i32p], C.c_int),
     "amr_mesh_block_gather": ([_vp, C.c_int64, _i64p, _i64p, _i64p, _i64p, _f64p], C.c_int),
     "amr_stage": ([C.POINTER(AmrStageParams), _vp], C.c_int),

@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libamr_b200.so")
 INCLUDE = os.path.abspath(os.path.join(HERE, "..", "include"))
-SOURCES = ["amr_kernels.cu", "amr_wavelet.cu", "amr_octree.cu", "amr_devmesh.cu", "amr_mesh.cpp", "amr_programs.cpp"]
+SOURCES = ["amr_kernels.cu", "amr_wavelet.cu", "amr_octree.cu", "amr_devmesh.cu", "amr_devprog.cu", "amr_mesh.cpp", "amr_programs.cpp"]
 # the stage-kernel launcher, compiled once per (dim, ppo, lts) in parallel
 INSTANCES = [(d, p, l) for d in (2, 3) for p in (5, 7, 9) for l in (0, 1)]
 INST_SRC = "amr_stage_inst.cu"

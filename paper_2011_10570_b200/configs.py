@@ -250,7 +250,8 @@ class WaveConfig:
             tot = None
             for c, a in zip(cs, amps):
                 r2 = sum((x - cc) ** 2 for x, cc in zip(xs, c))
-                term = a * np.exp(-r2 / w**2)
+                q = -r2 / w**2
+                term = a * (q.exp() if hasattr(q, "exp") else np.exp(q))  # torch tensors: device evaluation
                 tot = term if tot is None else tot + term
             return tot
 

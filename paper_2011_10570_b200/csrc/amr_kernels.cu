@@ -29,7 +29,13 @@ namespace {
 // pair whose step size or time differs from the reader's (delta=0 transfer or
 // virtual substep + transfer, stepper.py:256-314), once per stage, so the
 // stage kernel reads it like a copy.  Pairs are sorted finest reader first:
-// the eligible readers of a slice are a prefix.
+// the eligible readers of a slice are a prefix.  The buffer holds one slab per
+// stage, [stage][var][pair].  A pair whose source is not stepping at this slice
+// (virtual substep, mode 2) depends on nothing the slice computes, so the
+// stage-0 launch (if_phase 1) fills all its stages at once — the source's u_pre
+// and K are read once instead of once per stage — and the later launches
+// (if_phase 2) skip it; a slice where only one cadence steps needs no later
+// launch at all.
 __global__ void __launch_bounds__(256) iface_kernel(const AmrStageParams P) {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");  // the stage kernel may fetch its tile heads meanwhile
   const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
@@ -37,9 +43,69 @@ __global__ void __launch_bounds__(256) iface_kernel(const AmrStageParams P) {
   const int g = __ldg(P.if_gid + i);
   const int cc = __ldg(P.if_cad + i);  // reader cadence | source cadence << 8 (no dependent lookup)
   asm volatile("griddepcontrol.wait;\n" ::: "memory");              // the fields are the previous stage kernel's output
-  const double2 v = lts_source(P.U0, P.U1, P.K, P.ld, P.n_stages, g, P.stage, cc & 0xFF, cc >> 8, P.coef);
-  P.ibuf[i] = v.x;
-  P.ibuf[P.n_iface_total + i] = v.y;
+  const int lr = cc & 0xFF, ls = cc >> 8;
+  const AmrSliceCoef* C = P.coef;
+  const int64_t N = P.n_iface_total;
+  const int mode = C->mode[lr][ls];
+  if (P.if_phase != 0 && mode == 2) {
+    if (P.if_phase == 2) return;  // filled by the stage-0 launch
+    const int p = P.n_stages;
+    const int64_t n = P.ld;
+    double2 kk[AMR_MAXP];
+#pragma unroll
+    for (int k = 0; k < AMR_MAXP; ++k)
+      kk[k] = (k < p) ? ld_pair(P.K + (int64_t)k * 2 * n, n, g) : make_double2(0.0, 0.0);
+    double2 y0 = ld_pair(C->cur[ls] ? P.U0 : P.U1, n, g);  // u_pre: the virtual substep starts there
+    const double(*Mv)[AMR_MAXP] = C->Mv[lr][ls];
+#pragma unroll
+    for (int a = 0; a < AMR_MAXP; ++a) {
+      if (a >= p) break;
+      const double c = C->dtw[lr][ls][a];
+      if (c == 0.0) continue;
+      double ax = 0.0, ay = 0.0;
+#pragma unroll
+      for (int k = 0; k <= a; ++k) {
+        ax = fma(Mv[a][k], kk[k].x, ax);
+        ay = fma(Mv[a][k], kk[k].y, ay);
+      }
+      y0.x = y0.x + c * ax;
+      y0.y = y0.y + c * ay;
+    }
+    const double(*M)[AMR_MAXP] = C->M[lr][ls];
+    double2 mk[AMR_MAXP];  // (M K)_j, shared by the stages
+#pragma unroll
+    for (int j = 0; j < AMR_MAXP; ++j) {
+      double ax = 0.0, ay = 0.0;
+      if (j < p - 1) {
+#pragma unroll
+        for (int k = 0; k < AMR_MAXP; ++k) {
+          if (k > p - 1) break;
+          ax = fma(M[j][k], kk[k].x, ax);
+          ay = fma(M[j][k], kk[k].y, ay);
+        }
+      }
+      mk[j] = make_double2(ax, ay);
+    }
+#pragma unroll
+    for (int s = 0; s < AMR_MAXP; ++s) {
+      if (s >= p) break;
+      double2 y = y0;
+#pragma unroll
+      for (int j = 0; j < AMR_MAXP; ++j) {
+        if (j >= s) break;
+        const double c = C->cstage[lr][s][j];
+        if (c == 0.0) continue;
+        y.x = y.x + c * mk[j].x;
+        y.y = y.y + c * mk[j].y;
+      }
+      P.ibuf0[(int64_t)(2 * s) * N + i] = y.x;
+      P.ibuf0[(int64_t)(2 * s + 1) * N + i] = y.y;
+    }
+    return;
+  }
+  const double2 v = lts_source(P.U0, P.U1, P.K, P.ld, P.n_stages, g, P.stage, lr, ls, C);
+  P.ibuf0[(int64_t)(2 * P.stage) * N + i] = v.x;
+  P.ibuf0[(int64_t)(2 * P.stage + 1) * N + i] = v.y;
 }
 
 

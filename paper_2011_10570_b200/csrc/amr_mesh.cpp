@@ -98,6 +98,10 @@ extern "C" AmrTree* amr_balance(int dim, int L, int64_t n, const int32_t* anchor
     fail(AMR_EINVAL, "dimension must be 2 or 3");
     return nullptr;
   }
+  if (L < 0 || L > 30 || dim * L > 58) {  // pack_key keeps dim*L code bits above 5 level bits
+    fail(AMR_EINVAL, "max_depth too large for 64-bit Morton keys");
+    return nullptr;
+  }
   const int32_t top = 1 << L;
   std::unordered_set<uint64_t> leafset;
   leafset.reserve((size_t)(n * 4 + 16));

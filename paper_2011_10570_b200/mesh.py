@@ -81,6 +81,10 @@ def decompose_blocks(tree: LinearOctree, points_per_octant: int = 7, pad: int = 
                                points_per_octant, pad)
 
 
+class _NotMortonOrder(ValueError):
+    """The leaf order is another curve's: the device builder (leaf index = key position) does not apply."""
+
+
 def device_tables(tree: LinearOctree, ppo: int, pad: int, device) -> dict:
     """Node registry, leaf-tile table and interpolation rows of a Morton-ordered
     balanced tree, built on the device (csrc/amr_devmesh.cu; the passes of
@@ -103,7 +107,7 @@ def device_tables(tree: LinearOctree, ppo: int, pad: int, device) -> dict:
         keys = torch.empty(n, dtype=torch.int64, device=device)
         _native.check(L.amr_oct_keys(dim, depth, n, a_d.data_ptr(), l_d.data_ptr(), keys.data_ptr(), st), "amr_oct_keys")
         if n > 1 and not bool(torch.all(keys[1:] > keys[:-1])):
-            raise ValueError("leaves are not in Morton order: not a valid linear octree for the device builder")
+            raise _NotMortonOrder("leaves are not in Morton order")
         geo = (dim, depth, ppo, pad, n, keys.data_ptr(), a_d.data_ptr(), l_d.data_ptr())
         err = torch.zeros(1, dtype=torch.int32, device=device)
         status = torch.empty((n, P), dtype=torch.int8, device=device)
@@ -152,7 +156,8 @@ def device_tables(tree: LinearOctree, ppo: int, pad: int, device) -> dict:
         if e:
             raise ValueError("device mesh builder: " + ("lattice point outside the domain during interpolation"
                                                         if e & 1 else "interpolation row exceeds the builder's limits"))
-    return dict(starts=starts, leaf_gids=leaf_gids, table=table, codes=codes, row_ptr=row_ptr, gid=gid[:nnz], w=w[:nnz])
+    return dict(starts=starts, leaf_gids=leaf_gids, table=table, codes=codes, row_ptr=row_ptr, gid=gid[:nnz], w=w[:nnz],
+                anchors=a_d, levels=l_d)
 
 
 class _NativeMesh:
@@ -164,9 +169,15 @@ class _NativeMesh:
         self.lib = _native.lib()
         own = np.ascontiguousarray(owners, dtype=np.int32)
         self.on_device = device is not None
+        self.tables = None  # device tensors of the tables when they were built there
         if device is not None:
-            t = device_tables(tree, ppo, pad, device)
-            h = {k: np.ascontiguousarray(v.cpu().numpy()) for k, v in t.items()}
+            try:
+                t = self.tables = device_tables(tree, ppo, pad, device)
+            except _NotMortonOrder:  # leaves along another curve: the host passes index them themselves
+                device = None
+                self.on_device = False
+        if device is not None:
+            h = {k: np.ascontiguousarray(v.cpu().numpy()) for k, v in t.items() if k not in ("anchors", "levels")}
             p32, p64 = (lambda a: _native.ptr(a, C.c_int32)), (lambda a: _native.ptr(a, C.c_int64))
             self.h = self.lib.amr_mesh_from_tables(
                 tree.dim, tree.max_depth, ppo, pad, len(levels), p32(anchors), p32(levels), p32(own),
@@ -463,6 +474,22 @@ class Mesh:
         return out
 
     # -- engine view ---------------------------------------------------------------
+    def device_tables(self):
+        """The registry and tile tables as device tensors (built there, or
+        uploaded from the host builder's arrays), for the device program builder."""
+        if self._nm.tables is None:
+            import torch
+
+            dev = torch.device("cuda", torch.cuda.current_device())
+            td = self.tile_data()
+            an, lv = self.tree.arrays()
+            T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+            nnz = int(td["interp_ptr"][-1])
+            self._nm.tables = dict(starts=T(self.leaf_starts), table=T(td["table"]), row_ptr=T(td["interp_ptr"]),
+                                   gid=T(td["interp_gid"][:max(nnz, 1)]), w=T(td["interp_w"][:max(nnz, 1)]),
+                                   anchors=T(an.astype(np.int32)), levels=T(lv.astype(np.int32)))
+        return self._nm.tables
+
     def tile_data(self) -> dict:
         """Leaf-tile unzip tables for the stage kernel (see include/amr_b200.h)."""
         if self._tile is None:
@@ -508,6 +535,36 @@ class Mesh:
         nc = self.node_coords
         for d in range(self.dim):
             out[:, d] = self.domain.lo[d] + (nc[:, d] / self.top_nodes) * self.domain.extent(d)
+        return out
+
+    def node_physical_device(self):
+        """node_physical as per-axis float64 CUDA tensors, from the device
+        registry (each leaf's owned lattice points scattered to their gids):
+        the same ``lo + (coord / top_nodes) * extent`` operations, no host pass
+        over the nodes (cfg5: 6e8 nodes)."""
+        import torch
+
+        t = self.device_tables()
+        if "leaf_gids" not in t:
+            dev = t["table"].device
+            t["leaf_gids"] = torch.from_numpy(self.leaf_gids.astype(np.int32)).to(dev)
+        lg, st = t["leaf_gids"], t["starts"]
+        dev = lg.device
+        n, P = lg.shape
+        own = (lg >= st[:-1, None]) & (lg < st[1:, None])
+        idx = lg[own].to(torch.int64)
+        leaf = torch.arange(n, device=dev)[:, None].expand(n, P)[own]
+        k = torch.arange(P, device=dev)[None, :].expand(n, P)[own]
+        del own
+        s = (torch.ones((), dtype=torch.int64, device=dev) << (self.L - t["levels"].to(torch.int64)))[leaf]
+        out = []
+        for d in range(self.dim):
+            loc = (k // self.ppo ** (self.dim - 1 - d)) % self.ppo
+            coord = torch.empty(self.n_nodes, dtype=torch.float64, device=dev)
+            coord[idx] = (t["anchors"][:, d].to(torch.int64)[leaf] * self.scale + s * loc).to(torch.float64)
+            top = torch.full((), float(self.top_nodes), dtype=torch.float64, device=dev)
+            ext = torch.full((), self.domain.extent(d), dtype=torch.float64, device=dev)
+            out.append(self.domain.lo[d] + (coord / top) * ext)
         return out
 
     def block_axes(self, block: Block) -> list[np.ndarray]:

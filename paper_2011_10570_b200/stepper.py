@@ -154,21 +154,57 @@ def _pow2_exact(x: float) -> bool:
     return x > 0 and m == 0.5
 
 
+def _as_tensors(prog: dict) -> dict:
+    """The program arrays as torch tensors (CPU for the host builder's numpy
+    arrays, CUDA for the device builder's), so one code path lays them out."""
+    import torch
+
+    out = dict(prog)
+    for k in ("heads", "tail", "if_gid", "if_cad", "wtab"):
+        v = prog[k]
+        if not isinstance(v, torch.Tensor):
+            v = np.ascontiguousarray(v)
+            if v.dtype == np.uint16:
+                v = v.view(np.int16)
+            v = torch.from_numpy(v)
+        out[k] = v
+    return out
+
+
+def _head_words(heads):
+    """(n, max_head / 4) int32 view of the heads."""
+    import torch
+
+    return heads.view(torch.int32).reshape(heads.shape[0], -1)
+
+
+def _base_mask(h32, nt: int):
+    """The source-group base words of the first nt heads and the mask of the real (>= 0) ones."""
+    import torch
+
+    W = min(63, h32.shape[1] - 16)
+    bases = h32[:nt, 16:16 + W]
+    valid = (torch.arange(W, device=h32.device)[None, :] < h32[:nt, 6][:, None]) & (bases >= 0)
+    return bases, valid
+
+
 def _source_leaves(prog: dict, starts: np.ndarray, tile_leaves: np.ndarray) -> np.ndarray:
     """Sorted leaves whose zip nodes the programs read (their own tiles included):
     the positive source bases of every head, and the source nodes of the
     interface pairs."""
+    import torch
+
     heads = prog["heads"]
-    h32 = heads.view(np.int32).reshape(heads.shape[0], -1)
     nt = len(tile_leaves)
     out = [np.asarray(tile_leaves, dtype=np.int64)]
+    st = torch.from_numpy(np.ascontiguousarray(starts)).to(heads.device)
     if nt:
-        W = min(63, h32.shape[1] - 16)
-        bases = h32[:nt, 16:16 + W]
-        valid = (np.arange(W)[None, :] < h32[:nt, 6][:, None]) & (bases >= 0)
-        out.append(np.searchsorted(starts, np.unique(bases[valid]).astype(np.int64), side="right") - 1)
+        bases, valid = _base_mask(_head_words(heads), nt)
+        vals = torch.unique(bases[valid]).to(torch.int64)
+        out.append((torch.searchsorted(st, vals, right=True) - 1).cpu().numpy())
     if prog["n_iface"]:
-        out.append(np.searchsorted(starts, np.unique(prog["if_gid"]).astype(np.int64), side="right") - 1)
+        g = torch.unique(prog["if_gid"][: prog["n_iface"]]).to(torch.int64)
+        out.append((torch.searchsorted(st, g, right=True) - 1).cpu().numpy())
     return np.unique(np.concatenate(out))
 
 
@@ -187,12 +223,16 @@ class _Rank:
         self.tiles = self.owned[order]  # cadence order; reordered by layout()
         from . import tileprog
 
-        if len(self.tiles):
-            self.prog = tileprog.build_programs_native(mesh, self.tiles.astype(np.int32), cad, lts_kernel)
-        else:  # an empty rank (more ranks than the weights can split)
-            self.prog = dict(heads=np.zeros((1, 64), np.uint8), tail=np.zeros(8, np.uint16), max_head=64,
-                             max_slots=0, max_tail=0, if_gid=np.zeros(0, np.int32), if_cad=np.zeros(0, np.int32),
-                             n_iface=0, wtab=np.zeros(1), n_rows=0, n_cells=0)
+        if not len(self.tiles):  # an empty rank (more ranks than the weights can split)
+            prog = dict(heads=np.zeros((1, 64), np.uint8), tail=np.zeros(8, np.uint16), max_head=64,
+                        max_slots=0, max_tail=0, if_gid=np.zeros(0, np.int32), if_cad=np.zeros(0, np.int32),
+                        n_iface=0, wtab=np.zeros(1), n_rows=0, n_cells=0)
+        elif mesh._nm.on_device and os.environ.get("AMR_HOST_PROGRAMS") != "1":
+            # tables were built on the device: so are the programs (byte-identical to the host builder)
+            prog = tileprog.build_programs_device(mesh, self.tiles.astype(np.int32), cad, lts_kernel)
+        else:
+            prog = tileprog.build_programs_native(mesh, self.tiles.astype(np.int32), cad, lts_kernel)
+        self.prog = _as_tensors(prog)
         self.src_leaves = _source_leaves(self.prog, mesh.leaf_starts, self.tiles)
         own_mask = np.zeros(len(cad) + 1, dtype=bool)
         own_mask[self.owned] = True
@@ -212,9 +252,12 @@ class _Rank:
         is_b = np.zeros(n_leaves, dtype=bool)
         is_b[np.asarray(boundary_leaves, dtype=np.int64)] = True
         tb = is_b[self.tiles]
+        import torch
+
         perm = np.lexsort((self.tiles, -cad[self.tiles], ~tb))
         self.tiles = self.tiles[perm]
-        heads = prog["heads"][: len(perm)][perm] if len(perm) else prog["heads"]
+        pdev = prog["heads"].device
+        heads = prog["heads"][torch.from_numpy(perm).to(pdev)] if len(perm) else prog["heads"]
         tcad = cad[self.tiles]
         tb = tb[perm]
         self.n_boundary = int(tb.sum())
@@ -223,7 +266,8 @@ class _Rank:
         self.prefix_i = [int(np.sum(tcad[~tb] >= c)) for c in levels]
         n_iface = prog["n_iface"]
         self.n_iface = n_iface
-        self.if_prefix = [int(np.sum((prog["if_cad"][:n_iface] & 0xFF) >= c)) for c in levels]
+        rcad = (prog["if_cad"][:n_iface] & 0xFF).cpu().numpy() if n_iface else np.zeros(0, np.int64)
+        self.if_prefix = [int(np.sum(rcad >= c)) for c in levels]
         # local layout: owned + ghost leaves in leaf order
         self.local_leaves = np.union1d(self.owned, self.ghosts)
         counts = (starts[1:] - starts[:-1])[self.local_leaves]
@@ -237,24 +281,23 @@ class _Rank:
         self.identity = self.n_local == mesh.n_nodes and len(self.local_leaves) == n_leaves
         if_gid = prog["if_gid"]
         if not self.identity:
-            heads = np.ascontiguousarray(heads)
-            h32 = heads.view(np.int32).reshape(heads.shape[0], -1)
+            st = torch.from_numpy(np.ascontiguousarray(starts)).to(pdev)
+            ls = torch.from_numpy(self.leaf_lstart).to(pdev)
+            h32 = _head_words(heads)
             nt = len(self.tiles)
             if nt:
-                h32[:nt, 0] = self.leaf_lstart[self.tiles]
-                W = min(63, h32.shape[1] - 16)
-                bases = h32[:nt, 16:16 + W]
-                valid = (np.arange(W)[None, :] < h32[:nt, 6][:, None]) & (bases >= 0)
-                old = bases[valid].astype(np.int64)
-                lf = np.searchsorted(starts, old, side="right") - 1
-                new = self.leaf_lstart[lf]
-                if np.any(starts[lf] != old) or np.any(new < 0):
+                h32[:nt, 0] = ls[torch.from_numpy(self.tiles).to(pdev)].to(torch.int32)
+                bases, valid = _base_mask(h32, nt)
+                old = bases[valid].to(torch.int64)
+                lf = torch.searchsorted(st, old, right=True) - 1
+                new = ls[lf]
+                if bool(torch.any(st[lf] != old)) or bool(torch.any(new < 0)):
                     raise RuntimeError("stage programs read a leaf outside the rank's layout")
-                bases[valid] = new.astype(np.int32)
+                bases[valid] = new.to(torch.int32)
             if n_iface:
-                g = if_gid[:n_iface].astype(np.int64)
-                lf = np.searchsorted(starts, g, side="right") - 1
-                if_gid = (self.leaf_lstart[lf] + (g - starts[lf])).astype(np.int32)
+                g = if_gid[:n_iface].to(torch.int64)
+                lf = torch.searchsorted(st, g, right=True) - 1
+                if_gid = (ls[lf] + (g - st[lf])).to(torch.int32)
             # local node -> global gid (load_zip)
             self.l2g = np.repeat(starts[self.local_leaves] - lstart[:-1], counts) + np.arange(self.n_local)
         else:
@@ -262,7 +305,7 @@ class _Rank:
         a, b = (int(self.owned[0]), int(self.owned[-1]) + 1) if len(self.owned) else (0, 0)
         self.own_g0, self.own_g1 = int(starts[a]), int(starts[b])  # owned gids (global), contiguous
         self.own_l0 = int(self.leaf_lstart[a]) if len(self.owned) else 0
-        self.host = dict(heads=heads, tail=prog["tail"], wtab=prog["wtab"], if_gid=if_gid, if_cad=prog["if_cad"])
+        self.progt = dict(heads=heads, tail=prog["tail"], wtab=prog["wtab"], if_gid=if_gid, if_cad=prog["if_cad"])
         self.max_head, self.max_tail, self.max_slots = prog["max_head"], prog["max_tail"], prog["max_slots"]
         self.stats = dict(n_rows=prog["n_rows"], n_cells=prog["n_cells"])
         self.prog = None
@@ -274,18 +317,24 @@ class _Rank:
         r_end = np.append(r_start[1:], self.own_l0 + (self.own_g1 - self.own_g0)) if len(oc) else r_start
         self.own_ranges_host = (r_start, r_end - r_start, oc[first] if len(oc) else np.zeros(0, np.int64))
 
+    @property
+    def host(self) -> dict:
+        """The laid-out programs as numpy arrays (tests, tileprog.decode)."""
+        h = self.progt
+        out = {k: h[k].cpu().numpy() for k in ("heads", "wtab", "if_gid", "if_cad")}
+        out["tail"] = h["tail"].cpu().numpy().view(np.uint16)
+        return out
+
     def upload(self, eng: "Engine") -> None:
         """Device side: programs, zip rows (u0, u1, K, Y), interface buffer."""
         import torch
 
         self.eng = eng
         dev = eng.device
-        T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
-        pad = lambda x: x if len(x) else np.zeros(1, x.dtype)  # noqa: E731
-        h = self.host
-        self.d = dict(heads=T(h["heads"]), tail=T(h["tail"]), wtab=T(h["wtab"]), if_gid=T(pad(h["if_gid"])),
-                      if_cad=T(pad(h["if_cad"])))
-        self.host = None
+        pad = lambda x: x if x.numel() else torch.zeros(1, dtype=x.dtype)  # noqa: E731
+        h = self.progt
+        self.d = {k: pad(h[k]).contiguous().to(dev) for k in ("heads", "tail", "wtab", "if_gid", "if_cad")}
+        self.progt = None
         n_iface = self.n_iface
         n = self.n_local
         # rows padded to an even stride ld > n (16-byte aligned rows; the kernel
@@ -298,7 +347,7 @@ class _Rank:
         self.U = [u[:, :n] for u in self.U_store]
         self.K = self.K_store[:, :, :n]
         self.Y = self.Y_store[:, :, :n]
-        self.ibuf = torch.zeros((2, max(n_iface, 1)), dtype=torch.float64, device=dev)
+        self.ibuf = torch.zeros((p, 2, max(n_iface, 1)), dtype=torch.float64, device=dev)  # one slab per stage
         self.prm = self._make_params()
         self.own_ranges = _Ranges(*self.own_ranges_host, dev)
 
@@ -314,7 +363,8 @@ class _Rank:
         P.ld = self.ld
         d = self.d
         P.max_slots = self.max_slots
-        P.if_gid, P.if_cad, P.ibuf = d["if_gid"].data_ptr(), d["if_cad"].data_ptr(), self.ibuf.data_ptr()
+        P.if_gid, P.if_cad = d["if_gid"].data_ptr(), d["if_cad"].data_ptr()
+        P.ibuf = P.ibuf0 = self.ibuf.data_ptr()
         P.n_iface_total = self.n_iface
         P.wtab, P.n_wtab = d["wtab"].data_ptr(), int(d["wtab"].numel())
         P.heads, P.max_head, P.tail = d["heads"].data_ptr(), self.max_head, d["tail"].data_ptr()
@@ -371,7 +421,11 @@ class _Rank:
         for t, j in enumerate(vt):
             P.vt_j[t] = j
         P.n_iface = self.if_prefix[cmin]
-        if P.n_iface and (self.prefix_b[cmin] or self.prefix_i[cmin]):
+        P.ibuf = self.ibuf.data_ptr() + s * 2 * max(self.n_iface, 1) * 8
+        # stage 0 also fills every stage of the pairs whose source is not stepping at this slice;
+        # later stages redo only the pairs whose source steps too — none when one cadence steps alone
+        P.if_phase = 1 if s == 0 else 2
+        if P.n_iface and (self.prefix_b[cmin] or self.prefix_i[cmin]) and (s == 0 or eng._n_eligible(i) > 1):
             with eng._phase("time_interp"):
                 rc = eng._lib.amr_iface(C.byref(P), eng._stream())
             if rc:
@@ -813,7 +867,25 @@ class Engine:
         return {k: 1e3 * v for k, v in self.counters.phases.items()}
 
     # -- state I/O -----------------------------------------------------------------------
-    def initialize(self, chi0, phi0=None) -> None:
+    def initialize(self, chi0, phi0=None, device_eval: bool = False) -> None:
+        """Evaluate initial data on the zip nodes and load all state
+        (stepper.py:198-211).  ``device_eval``: evaluate ``chi0`` / ``phi0``
+        (written with array methods or torch ops) on device coordinates
+        instead of numpy on the host — for meshes where a host pass over every
+        node is the slow part (cfg5); transcendentals then round as CUDA's, not
+        libm's, so the data is not bit-identical to the host evaluation."""
+        if device_eval:
+            import torch
+
+            with torch.cuda.device(self.device):
+                xs = self.mesh.node_physical_device()
+                z = torch.zeros((self.NVARS, self.mesh.n_nodes), dtype=torch.float64, device=self.device)
+                z[0] = chi0(*xs)
+                if phi0 is not None:
+                    z[1] = phi0(*xs)
+                del xs
+            self.load_zip(z)
+            return
         xyz = self.mesh.node_physical()
         coords = [xyz[:, d] for d in range(self.mesh.dim)]
         z = np.zeros((self.NVARS, self.mesh.n_nodes))
@@ -1012,6 +1084,9 @@ class Engine:
     def _eligible_cadences(self, i: int) -> list[int]:
         return [c for c in sorted(set(self.cadence)) if i % (1 << (self.l_max - c)) == 0]
 
+    def _n_eligible(self, i: int) -> int:
+        return len(self._eligible_cadences(i))
+
     def advance_slice(self) -> None:
         """Advance every block eligible at the current fine slice by one of its steps.
 
@@ -1132,8 +1207,9 @@ class Engine:
         n = 0
         for rk in self._rank_list:
             tiles = (1 if rk.prefix_b[c] else 0) + (1 if rk.prefix_i[c] else 0)
-            n += tiles + (1 if tiles and rk.if_prefix[c] else 0)
-        return self.p * n
+            iface = (1 if len(el) == 1 else self.p) if tiles and rk.if_prefix[c] else 0
+            n += self.p * tiles + iface
+        return n
 
     @property
     def comm_bytes(self) -> int:

@@ -432,3 +432,119 @@ def build_programs_native(mesh, tiles: np.ndarray, leaf_cad: np.ndarray, lts: bo
     return dict(heads=heads, tail=tail, max_head=max_head, max_slots=max_slots, max_tail=max_tail,
                 if_gid=if_gid[:n_iface], if_cad=if_cad[:n_iface], n_iface=n_iface, wtab=wtab, n_rows=n_rows,
                 n_cells=n_cells)
+
+
+def build_programs_device(mesh, tiles: np.ndarray, leaf_cad: np.ndarray, lts: bool, device=None) -> dict:
+    """build_programs on the device (csrc/amr_devprog.cu) from the mesh's
+    device tables (``Mesh.device_tables``): the same dict, byte for byte
+    (tests/test_devprog_gpu.py), with ``heads``, ``tail``, ``if_gid``,
+    ``if_cad`` and ``wtab`` as CUDA tensors.  One thread per tile; the
+    sort/unique of the interface-pair keys and of the used weights are torch's."""
+    import ctypes as C
+
+    import torch
+
+    from . import _native
+
+    L = _native.lib()
+    tabs = mesh.device_tables()
+    device = tabs["table"].device if device is None else device
+    dim, ppo = mesh.dim, mesh.ppo
+    nt = len(tiles)
+    n_leaves = len(leaf_cad)
+    E = tabs["table"].shape[1]
+    NI = ppo ** dim
+    cells = cross_cells(dim, ppo)
+    bs = box_strides(dim, ppo)
+    cell2e = np.full(box_cells(dim, ppo), -1, dtype=np.int32)
+    cell2e[cells] = np.arange(len(cells), dtype=np.int32)
+    pos = np.zeros((NI, 3), dtype=np.int16)
+    k = np.arange(NI)
+    for d in range(dim):
+        pos[:, d] = (k // ppo ** (dim - 1 - d)) % ppo
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(device)  # noqa: E731
+    with torch.cuda.device(device):
+        st = torch.cuda.current_stream(device).cuda_stream
+        d_cell, d_c2e, d_pos = T(cells.astype(np.int32)), T(cell2e), T(pos)
+        d_tiles, d_cad = T(np.asarray(tiles, dtype=np.int32)), T(np.asarray(leaf_cad, dtype=np.int32))
+        A = _native.AmrDevProg()
+        A.dim, A.max_depth, A.ppo, A.lts, A.row_stride = dim, mesh.L, ppo, 1 if lts else 0, bs[-2]
+        A.max_bases = int(os.environ.get("AMR_MAX_BASES", "0"))
+        A.n_leaves, A.n_tiles = n_leaves, nt
+        A.table, A.starts = tabs["table"].data_ptr(), tabs["starts"].data_ptr()
+        A.anchors, A.levels = tabs["anchors"].data_ptr(), tabs["levels"].data_ptr()
+        A.leaf_cad, A.tiles = d_cad.data_ptr(), d_tiles.data_ptr()
+        A.row_ptr, A.gid, A.w = tabs["row_ptr"].data_ptr(), tabs["gid"].data_ptr(), tabs["w"].data_ptr()
+        A.cell, A.cell2e, A.pos = d_cell.data_ptr(), d_c2e.data_ptr(), d_pos.data_ptr()
+        threads = 128
+        blocks = max(1, min((nt + threads - 1) // threads, 148 * 4))
+        n_rows_mesh = tabs["row_ptr"].numel() - 1
+        need = torch.empty((max(nt, 1), E), dtype=torch.uint8, device=device)
+        row_used = torch.zeros(max(n_rows_mesh, 1), dtype=torch.uint8, device=device)
+        n_keys = torch.zeros(max(nt, 1), dtype=torch.int64, device=device)
+        _native.check(L.amr_dp_need(C.byref(A), need.data_ptr(), row_used.data_ptr(), n_keys.data_ptr(), blocks,
+                                    threads, st), "amr_dp_need")
+        # interface pairs: unique (reader cadence, gid) keys, finest reader first
+        ukeys = torch.zeros(0, dtype=torch.int64, device=device)
+        if lts and nt:
+            ends = torch.cumsum(n_keys[:nt], 0)
+            total = int(ends[-1])
+            if total:
+                keys = torch.empty(total, dtype=torch.int64, device=device)
+                off = ends - n_keys[:nt]
+                _native.check(L.amr_dp_keys(C.byref(A), need.data_ptr(), off.data_ptr(), keys.data_ptr(), blocks,
+                                            threads, st), "amr_dp_keys")
+                ukeys = torch.unique(keys)
+        n_iface = ukeys.numel()
+        if n_iface:
+            if_gid = ukeys & 0xFFFFFFFF
+            hi = ukeys >> 32
+            leaf = torch.searchsorted(tabs["starts"], if_gid, right=True) - 1
+            if_cad = (31 - hi) | (d_cad[leaf].to(torch.int64) << 8)
+            new = torch.ones(n_iface, dtype=torch.bool, device=device)
+            new[1:] = (hi[1:] != hi[:-1]) | (leaf[1:] != leaf[:-1])
+            idx = torch.arange(n_iface, dtype=torch.int64, device=device)
+            grp_start = torch.cummax(torch.where(new, idx, torch.zeros_like(idx)), 0).values
+        else:
+            if_gid = if_cad = grp_start = torch.zeros(0, dtype=torch.int64, device=device)
+        # weights of the used rows
+        counts = tabs["row_ptr"][1:] - tabs["row_ptr"][:-1]
+        used_w = tabs["w"][torch.repeat_interleave(row_used[:n_rows_mesh].bool(), counts)] if n_rows_mesh else \
+            torch.zeros(0, dtype=torch.float64, device=device)
+        wtab = torch.unique(torch.cat([torch.zeros(1, dtype=torch.float64, device=device), used_w]))
+        if wtab.numel() > 64:
+            raise ProgramError(f"{wtab.numel()} distinct interpolation weights (> 64)")
+        gs = grp_start if n_iface else torch.zeros(1, dtype=torch.int64, device=device)
+        uk = ukeys if n_iface else torch.zeros(1, dtype=torch.int64, device=device)
+        A.n_iface, A.ukeys, A.grp_start = n_iface, uk.data_ptr(), gs.data_ptr()
+        A.n_wtab, A.wtab = wtab.numel(), wtab.data_ptr()
+        nb = C.c_int64(0)
+        L.amr_dp_scratch_bytes(blocks * threads, C.byref(nb))
+        scratch = torch.empty(nb.value, dtype=torch.uint8, device=device)
+        sizes = torch.zeros((max(nt, 1), 5), dtype=torch.int64, device=device)
+        err = torch.zeros(1, dtype=torch.int32, device=device)
+        _native.check(L.amr_dp_encode(C.byref(A), need.data_ptr(), scratch.data_ptr(), sizes.data_ptr(), None, 0,
+                                      None, None, err.data_ptr(), blocks, threads, st), "amr_dp_encode")
+        e = int(err[0])
+        if e:
+            raise ProgramError("programs: a tile reads more source groups than the encoding holds (> 63)" if e & 2
+                               else "programs: a tile reads too many interpolation sources (> 1022)" if e & 1
+                               else "programs: tile does not fit the compact encoding")
+        max_head = max(64, int(sizes[:nt, 0].max())) if nt else 64
+        tail_end = torch.cumsum(sizes[:, 1], 0)
+        tail_total = int(tail_end[nt - 1]) if nt else 0
+        if tail_total // 16 >= (1 << 31):
+            raise ProgramError("tile tails exceed 32 GB")
+        tail_off = tail_end - sizes[:, 1]
+        heads = torch.zeros((max(nt, 1), max_head), dtype=torch.uint8, device=device)
+        tail = torch.zeros(max(tail_total // 2, 8), dtype=torch.int16, device=device)
+        _native.check(L.amr_dp_encode(C.byref(A), need.data_ptr(), scratch.data_ptr(), sizes.data_ptr(),
+                                      heads.data_ptr(), max_head, tail_off.data_ptr(), tail.data_ptr(), err.data_ptr(),
+                                      blocks, threads, st), "amr_dp_encode")
+        if int(err[0]):
+            raise ProgramError("hanging row does not fit the packed row word")
+        tot = sizes[:nt].sum(0) if nt else torch.zeros(5, dtype=torch.int64)
+        return dict(heads=heads, tail=tail, max_head=max_head, max_slots=int(sizes[:nt, 2].max()) if nt else 0,
+                    max_tail=int(sizes[:nt, 1].max()) if nt else 0, if_gid=if_gid.to(torch.int32),
+                    if_cad=if_cad.to(torch.int32), n_iface=n_iface, wtab=wtab, n_rows=int(tot[3]),
+                    n_cells=int(tot[4]))

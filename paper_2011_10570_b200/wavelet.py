@@ -22,6 +22,7 @@ np.tensordot (OpenBLAS dgemm) arithmetic, see tests/test_wavelet*.py.
 from __future__ import annotations
 
 from dataclasses import dataclass
+import os
 from enum import Enum
 from typing import Callable
 
@@ -31,7 +32,13 @@ from . import _native
 from .octree import LinearOctree, OctKey
 
 _CHUNK_VALUES = 1 << 22  # samples per host->device chunk (32 MiB of fp64)
-_HOST_WORKERS = 8  # threads evaluating f on host chunks
+# Threads evaluating f on host chunks.  f is called on chunked (n, npd, ...) coordinate
+# arrays; the reference calls it once per octant on (npd,)*dim grids, in order.  For an
+# elementwise f (every reference test and BASELINE predicate) the samples are the same
+# bits either way.  An f that is not elementwise or not thread-safe must not be batched:
+# AMR_WAVELET_WORKERS=1 evaluates chunks one at a time, and `_probe_elementwise` refuses
+# an f whose values on an octant change with the rest of the batch.
+_HOST_WORKERS = max(1, int(os.environ.get("AMR_WAVELET_WORKERS", "8")))
 _PINNED: list = []
 
 
@@ -150,7 +157,19 @@ def _sample_values(f: Callable, axes: list[np.ndarray], npd: int) -> np.ndarray:
     vals = np.asarray(f(*grids), dtype=float)
     if vals.shape != shape:  # f returned a broadcastable array (e.g. a constant)
         vals = np.array(np.broadcast_to(vals, shape))
+    if n > 1:
+        _probe_elementwise(f, grids, vals, shape)
     return vals.reshape(n, -1)
+
+
+def _probe_elementwise(f: Callable, grids, vals: np.ndarray, shape) -> None:
+    """The reference evaluates f octant by octant; batching is only the same
+    function for an elementwise f.  Check it on the first octant of the batch."""
+    one = np.asarray(f(*[g[:1] for g in grids]), dtype=float)
+    one = np.broadcast_to(one, (1,) + tuple(shape[1:]))
+    if not np.array_equal(one, vals[:1], equal_nan=True):
+        raise ValueError("the field function is not elementwise: its values on one octant change when octants "
+                         "are batched; evaluate it per octant (wavelet_coefficient) instead")
 
 
 _LAUNCHERS: dict = {}

@@ -74,3 +74,25 @@ def test_hilbert_trees_use_the_host_builder(cuda):
     tree = random_tree(np.random.default_rng(1), 2, 4)  # default ordering: Hilbert
     mesh = Mesh(tree, points_per_octant=5, pad=2)
     assert not mesh._nm.on_device
+
+
+@pytest.mark.parametrize("name", ["cfg1", "mini3d"])
+def test_device_node_coordinates_and_initial_data(cuda, name):
+    """node_physical_device == node_physical bit for bit; Engine.initialize(device_eval=True)
+    differs from the host evaluation only by the rounding of exp (CUDA vs libm)."""
+    from helpers import config_mesh
+
+    from paper_2011_10570_b200.stepper import Engine
+
+    c = CONFIGS[name]
+    mesh = config_mesh(name)
+    xs = mesh.node_physical_device()
+    want = mesh.node_physical()
+    for d in range(mesh.dim):
+        assert np.array_equal(xs[d].cpu().numpy(), want[:, d])
+    a = Engine(mesh, tableau="rk4", mode="lts")
+    b = Engine(mesh, tableau="rk4", mode="lts")
+    a.initialize(c.chi0())
+    b.initialize(c.chi0(), device_eval=True)
+    za, zb = a.current_zip(), b.current_zip()
+    assert np.max(np.abs(za - zb)) <= 4e-16 * max(1.0, np.max(np.abs(za)))
