@@ -406,9 +406,15 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("AMR_DIST_BACKEND", "nccl")  # gloo: the multi-rank path on one GPU (host-staged ghosts)
+    if backend != "nccl":
+        local = local % max(torch.cuda.device_count(), 1)
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         dist = None
     dev = torch.device("cuda", local)
@@ -467,7 +473,8 @@ def run_ours(args):
         "dtype": "f64",
         "data": f"synthetic ({args.config} mesh and Gaussian initial data, seeded; no dataset exists for this path)",
         "config": m["config"],
-        "parallelism": f"weighted Morton partition x{world}, ghost records over NCCL" if world > 1 else "1 GPU",
+        "parallelism": (f"weighted Morton partition x{world}, ghost records over "
+                        f"{os.environ.get('AMR_DIST_BACKEND', 'nccl')}") if world > 1 else "1 GPU",
         "mesh_build_s": m["mesh_build_s"], "engine_build_s": m["engine_build_s"],
         "gts": m["gts"],
         "lts_vs_gts_wall_speedup": m["lts_vs_gts_wall_speedup"],

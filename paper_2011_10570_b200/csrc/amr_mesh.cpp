@@ -765,13 +765,15 @@ extern "C" AmrMesh* amr_mesh_from_tables(int dim, int L, int ppo, int pad, int64
   }
   m->starts.assign(starts, starts + n_leaves + 1);
   m->n_nodes = m->starts[n_leaves];
-  m->leaf_gids.assign(leaf_gids, leaf_gids + (size_t)n_leaves * m->per_leaf);
   m->E = amr_tile_entries(dim, ppo);
-  m->table.assign(table, table + (size_t)n_leaves * m->E);
-  m->hang_codes.assign(hang_codes, hang_codes + n_rows);
-  m->iptr.assign(iptr, iptr + n_rows + 1);
-  m->igid.assign(igid, igid + m->iptr.back());
-  m->iw.assign(iw, iw + m->iptr.back());
+  if (leaf_gids && table) {  // NULL: a light handle (blocks and leaf slices only)
+    m->leaf_gids.assign(leaf_gids, leaf_gids + (size_t)n_leaves * m->per_leaf);
+    m->table.assign(table, table + (size_t)n_leaves * m->E);
+    m->hang_codes.assign(hang_codes, hang_codes + n_rows);
+    m->iptr.assign(iptr, iptr + n_rows + 1);
+    m->igid.assign(igid, igid + m->iptr.back());
+    m->iw.assign(iw, iw + m->iptr.back());
+  }
   int32_t root[3] = {0, 0, 0};
   if (n_leaves > 0) decompose(m, root, 0, 0, n_leaves);
   return m;

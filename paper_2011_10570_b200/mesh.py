@@ -170,26 +170,51 @@ class _NativeMesh:
         own = np.ascontiguousarray(owners, dtype=np.int32)
         self.on_device = device is not None
         self.tables = None  # device tensors of the tables when they were built there
+        self._full = True
         if device is not None:
             try:
-                t = self.tables = device_tables(tree, ppo, pad, device)
+                self.tables = device_tables(tree, ppo, pad, device)
             except _NotMortonOrder:  # leaves along another curve: the host passes index them themselves
                 device = None
                 self.on_device = False
         if device is not None:
-            h = {k: np.ascontiguousarray(v.cpu().numpy()) for k, v in t.items() if k not in ("anchors", "levels")}
-            p32, p64 = (lambda a: _native.ptr(a, C.c_int32)), (lambda a: _native.ptr(a, C.c_int64))
-            self.h = self.lib.amr_mesh_from_tables(
-                tree.dim, tree.max_depth, ppo, pad, len(levels), p32(anchors), p32(levels), p32(own),
-                p64(h["starts"]), p32(h["leaf_gids"]), p32(h["table"]), len(h["codes"]), p64(h["codes"]),
-                p64(h["row_ptr"]), p32(h["gid"] if len(h["gid"]) else np.zeros(1, np.int32)),
-                _native.ptr(h["w"] if len(h["w"]) else np.zeros(1), C.c_double))
+            # a light handle (blocks, leaf slices); host copies of the big tables only when an
+            # API view asks for them (full()) — the engine works on the device tensors
+            self._args = (tree.dim, tree.max_depth, ppo, pad, len(levels), anchors, levels, own)
+            self._full = False
+            self.h = self._from_tables(full=False)
         else:
             self.h = self.lib.amr_mesh_build(tree.dim, tree.max_depth, ppo, pad, len(levels),
                                              _native.ptr(anchors, C.c_int32), _native.ptr(levels, C.c_int32),
                                              _native.ptr(own, C.c_int32), 0)
         if not self.h:
             raise ValueError(_native.last_error())
+
+    def _from_tables(self, full: bool):
+        dim, depth, ppo, pad, n, anchors, levels, own = self._args
+        p32, p64 = (lambda a: _native.ptr(a, C.c_int32)), (lambda a: _native.ptr(a, C.c_int64))
+        t = self.tables
+        starts = np.ascontiguousarray(t["starts"].cpu().numpy())
+        if not full:
+            return self.lib.amr_mesh_from_tables(dim, depth, ppo, pad, n, p32(anchors), p32(levels), p32(own),
+                                                 p64(starts), None, None, 0, None, None, None, None)
+        h = {k: np.ascontiguousarray(t[k].cpu().numpy()) for k in ("leaf_gids", "table", "codes", "row_ptr", "gid", "w")}
+        return self.lib.amr_mesh_from_tables(
+            dim, depth, ppo, pad, n, p32(anchors), p32(levels), p32(own), p64(starts), p32(h["leaf_gids"]),
+            p32(h["table"]), len(h["codes"]), p64(h["codes"]), p64(h["row_ptr"]),
+            p32(h["gid"] if len(h["gid"]) else np.zeros(1, np.int32)),
+            _native.ptr(h["w"] if len(h["w"]) else np.zeros(1), C.c_double))
+
+    def full(self):
+        """The handle with host copies of every table (API views, the host program builder)."""
+        if not self._full:
+            h = self._from_tables(full=True)
+            if not h:
+                raise ValueError(_native.last_error())
+            old, self.h = self.h, h
+            self.lib.amr_mesh_free(old)
+            self._full = True
+        return self.h
 
     def __del__(self):
         h, self.h = getattr(self, "h", None), None
@@ -281,7 +306,7 @@ class Mesh:
     def leaf_gids(self) -> np.ndarray:
         if self._leaf_gids is None:
             g = np.empty((len(self.tree), self.ppo ** self.dim), dtype=np.int32)
-            _native.check(self._nm.lib.amr_mesh_leaf_gids(self._nm.h, _native.ptr(g, C.c_int32)), "leaf_gids")
+            _native.check(self._nm.lib.amr_mesh_leaf_gids(self._nm.full(), _native.ptr(g, C.c_int32)), "leaf_gids")
             self._leaf_gids = g.astype(np.int64)
         return self._leaf_gids
 
@@ -289,7 +314,7 @@ class Mesh:
     def node_coords(self) -> np.ndarray:
         if self._node_coords is None:
             c = np.empty((self.n_nodes, self.dim), dtype=np.int32)
-            _native.check(self._nm.lib.amr_mesh_node_coords(self._nm.h, _native.ptr(c, C.c_int32)), "node_coords")
+            _native.check(self._nm.lib.amr_mesh_node_coords(self._nm.full(), _native.ptr(c, C.c_int32)), "node_coords")
             self._node_coords = c.astype(np.int64)
         return self._node_coords
 
@@ -338,6 +363,7 @@ class Mesh:
     # -- gathers ------------------------------------------------------------------
     def _block_csr(self, b: int):
         L = self._nm.lib
+        self._nm.full()
         rows, nnz = C.c_int64(0), C.c_int64(0)
         _native.check(L.amr_mesh_block_gather(self._nm.h, b, C.byref(rows), C.byref(nnz), None, None, None),
                       "block_gather")
@@ -494,6 +520,7 @@ class Mesh:
         """Leaf-tile unzip tables for the stage kernel (see include/amr_b200.h)."""
         if self._tile is None:
             L = self._nm.lib
+            self._nm.full()
             n = len(self.tree)
             E = int(L.amr_tile_entries(self.dim, self.ppo))
             table = np.empty((n, E), dtype=np.int32)
@@ -551,20 +578,26 @@ class Mesh:
         lg, st = t["leaf_gids"], t["starts"]
         dev = lg.device
         n, P = lg.shape
-        own = (lg >= st[:-1, None]) & (lg < st[1:, None])
-        idx = lg[own].to(torch.int64)
-        leaf = torch.arange(n, device=dev)[:, None].expand(n, P)[own]
-        k = torch.arange(P, device=dev)[None, :].expand(n, P)[own]
-        del own
-        s = (torch.ones((), dtype=torch.int64, device=dev) << (self.L - t["levels"].to(torch.int64)))[leaf]
+        coords = [torch.empty(self.n_nodes, dtype=torch.float64, device=dev) for _ in range(self.dim)]
+        kk = torch.arange(P, device=dev)
+        locs = [((kk // self.ppo ** (self.dim - 1 - d)) % self.ppo)[None, :] for d in range(self.dim)]
+        chunk = 1 << 15  # leaves per pass: temporaries stay small next to an engine's state
+        for a in range(0, n, chunk):
+            b = min(n, a + chunk)
+            g = lg[a:b]
+            own = (g >= st[a:b, None]) & (g < st[a + 1:b + 1, None])
+            idx = g[own].to(torch.int64)
+            s = (torch.ones((), dtype=torch.int64, device=dev) << (self.L - t["levels"][a:b].to(torch.int64)))[:, None]
+            for d in range(self.dim):
+                c = t["anchors"][a:b, d].to(torch.int64)[:, None] * self.scale + s * locs[d]
+                coords[d][idx] = c[own].to(torch.float64)
         out = []
+        top = torch.full((), float(self.top_nodes), dtype=torch.float64, device=dev)
         for d in range(self.dim):
-            loc = (k // self.ppo ** (self.dim - 1 - d)) % self.ppo
-            coord = torch.empty(self.n_nodes, dtype=torch.float64, device=dev)
-            coord[idx] = (t["anchors"][:, d].to(torch.int64)[leaf] * self.scale + s * loc).to(torch.float64)
-            top = torch.full((), float(self.top_nodes), dtype=torch.float64, device=dev)
             ext = torch.full((), self.domain.extent(d), dtype=torch.float64, device=dev)
-            out.append(self.domain.lo[d] + (coord / top) * ext)
+            x = coords[d]
+            x.div_(top).mul_(ext).add_(self.domain.lo[d])  # lo + (coord / top) * extent, in place
+            out.append(x)
         return out
 
     def block_axes(self, block: Block) -> list[np.ndarray]:

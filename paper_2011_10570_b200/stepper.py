@@ -870,7 +870,7 @@ class Engine:
     def initialize(self, chi0, phi0=None, device_eval: bool = False) -> None:
         """Evaluate initial data on the zip nodes and load all state
         (stepper.py:198-211).  ``device_eval``: evaluate ``chi0`` / ``phi0``
-        (written with array methods or torch ops) on device coordinates
+        (elementwise, written with array methods or torch ops) on device coordinates
         instead of numpy on the host — for meshes where a host pass over every
         node is the slow part (cfg5); transcendentals then round as CUDA's, not
         libm's, so the data is not bit-identical to the host evaluation."""
@@ -879,10 +879,14 @@ class Engine:
 
             with torch.cuda.device(self.device):
                 xs = self.mesh.node_physical_device()
-                z = torch.zeros((self.NVARS, self.mesh.n_nodes), dtype=torch.float64, device=self.device)
-                z[0] = chi0(*xs)
-                if phi0 is not None:
-                    z[1] = phi0(*xs)
+                n = self.mesh.n_nodes
+                z = torch.zeros((self.NVARS, n), dtype=torch.float64, device=self.device)
+                step = 1 << 26  # nodes per evaluation (elementwise functions): bounded temporaries
+                for a in range(0, n, step):
+                    part = [x[a:a + step] for x in xs]
+                    z[0, a:a + step] = chi0(*part)
+                    if phi0 is not None:
+                        z[1, a:a + step] = phi0(*part)
                 del xs
             self.load_zip(z)
             return

@@ -412,7 +412,7 @@ def build_programs_native(mesh, tiles: np.ndarray, leaf_cad: np.ndarray, lts: bo
     L = _native.lib()
     tiles = np.ascontiguousarray(tiles, dtype=np.int32)
     cad = np.ascontiguousarray(leaf_cad, dtype=np.int32)
-    h = L.amr_programs_build(mesh._nm.h, len(tiles), _native.ptr(tiles, C.c_int32), _native.ptr(cad, C.c_int32),
+    h = L.amr_programs_build(mesh._nm.full(), len(tiles), _native.ptr(tiles, C.c_int32), _native.ptr(cad, C.c_int32),
                              1 if lts else 0, box_strides(mesh.dim, mesh.ppo)[-2], n_threads)
     if not h:
         raise ProgramError(_native.last_error())

@@ -83,29 +83,3 @@ def test_linearity_full_size(cuda, cfg2):
         eng.lts_coarse_step()
         outs.append(eng.current_zip())
     assert rel_linf(outs[2], 2.0 * outs[0] - 0.5 * outs[1]) <= 1e-12
-
-
-@pytest.mark.slow
-def test_cfg3_cubic_matches_oracle(cuda):
-    """configs[2] (45.8 M zip nodes, cubic): GTS step and the first LTS slices,
-    bit for bit.  Slow (oracle mesh build ~2 min): run with AMR_SLOW=1."""
-    import os
-
-    from oracle import oracle as O
-
-    if not os.environ.get("AMR_SLOW"):
-        pytest.skip("set AMR_SLOW=1")
-    c = CONFIGS["cfg3"]
-    tree = config_tree("cfg3")
-    mesh = config_mesh("cfg3", tree=tree)
-    a, lv = tree.arrays()
-    om = O.OracleMesh(c.dim, c.max_depth, a, lv, c.ppo, c.pad, c.domain_lo, c.domain_hi)
-    assert np.array_equal(mesh.leaf_slices, om.leaf_slices)
-    for mode, slices in (("gts", 1), ("lts", 2)):
-        eng = Engine(mesh, tableau="rk4", mode=mode, nonlinear="cubic")
-        eng.initialize(c.chi0())
-        ref = O.OracleEngine(om, "rk4", 0.25, mode, "cubic")
-        ref.initialize(c.chi0())
-        eng.run_to(slices)
-        ref.run_to(slices)
-        assert np.array_equal(eng.current_zip(), ref.current_zip()), mode

@@ -80,12 +80,13 @@ SNAP = {
     "cfg2": [("gts", False, [1, 1024, 2048]), ("lts", False, [16, 1024, 2048]), ("lts-cubic", "cubic", [16])],
     "cfg3": [("gts", None, [1]), ("lts", None, [32, 256])],
     "cfg4": [("gts", None, [1]), ("lts", None, [1024])],
-    "cfg5": [("gts", None, [1]), ("lts", None, [4])],
 }
 
 
+# cfg5 (6.1e8 zip nodes) has no field golden: the oracle would need ~330 GB and hours for its mesh
+# (DESIGN.md section 2); its tree, balance and partitions are pinned above and in test_octree_gpu.py
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4", "cfg5"])
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4"])
 def test_fields_match_oracle_at_scale(cuda, name):
     from paper_2011_10570_b200.stepper import Engine
 
