@@ -49,6 +49,18 @@ __device__ __forceinline__ void cross_gather(const int* __restrict__ h, double* 
   const uint32_t* runs = reinterpret_cast<const uint32_t*>(bases + ((nbase + 3) & ~3));
   const uint16_t* sl = reinterpret_cast<const uint16_t*>(runs + ((nrun + 3) & ~3));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // the interpolation sources first, as their own cp.async group: the hanging
+  // rows start when these have landed, while the copy runs are still in flight
+  for (int k = threadIdx.x; k < nslot; k += NTH) {
+    const int code = sl[k];
+    const int base = bases[code >> 10], off = code & 1023;
+    if (!LTS || base >= 0)
+      cp_async8(slot + k, V + vo + base + off);
+    else
+      cp_async8(slot + k, IB + ibo + (-base - 1 + off));
+  }
+  if (threadIdx.x == 0) slot[nslot] = 0.0;  // zero slot of the padding taps
+  cp_async_commit();
   const int cnt4[4] = {h[11] & 0xFFFF, h[11] >> 16, h[12] & 0xFFFF, h[12] >> 16};
   int r0 = 0;
 #pragma unroll
@@ -73,15 +85,7 @@ __device__ __forceinline__ void cross_gather(const int* __restrict__ h, double* 
     }
     r0 += cnt;
   }
-  for (int k = threadIdx.x; k < nslot; k += NTH) {
-    const int code = sl[k];
-    const int base = bases[code >> 10], off = code & 1023;
-    if (!LTS || base >= 0)
-      cp_async8(slot + k, V + vo + base + off);
-    else
-      cp_async8(slot + k, IB + ibo + (-base - 1 + off));
-  }
-  if (threadIdx.x == 0) slot[nslot] = 0.0;  // zero slot of the padding taps
+  cp_async_commit();
 }
 
 // step 3: hanging rows into the box, from the tile's tail in shared memory.
@@ -479,15 +483,17 @@ __global__ void __launch_bounds__(NTH, (NTH <= 128 ? 2 * AMR_CROSS_MINB : AMR_CR
 
     // ---- 2, 3: chi on the owned cross; owned-node loads in flight meanwhile
     cross_gather<LTS, NTH>(c.h, box, slot, own, c.V, P.ibuf, 0, 0, c.g0, true);
-    cp_async_commit();
     AMR_PROBE(2);
     double pc[OPT], u0[OPT], u1[OPT];
     owned_loads<OPT, NTH>(P, c, pc, u0, u1);
+    if (c.nrow) {  // tile-uniform: the rows overlap the copy runs still in flight
+      cp_async_wait<1>();  // slots (and weights) landed
+      __syncthreads();
+      AMR_PROBE(3);
+      if (tail_bytes) mbar_wait(bar + TPC + j, 0);
+      cross_rows<NTH>(s_tail, c.nrow, c.taps_off, s_w, slot, box);
+    }
     cp_async_wait<0>();
-    __syncthreads();
-    AMR_PROBE(3);
-    if (tail_bytes) mbar_wait(bar + TPC + j, 0);
-    cross_rows<NTH>(s_tail, c.nrow, c.taps_off, s_w, slot, box);
     __syncthreads();
     AMR_PROBE(4);
 
@@ -498,7 +504,6 @@ __global__ void __launch_bounds__(NTH, (NTH <= 128 ? 2 * AMR_CROSS_MINB : AMR_CR
       // ---- 5: physical-face tiles: phi on the owned cross, radiative phi rows
       __syncthreads();  // everyone is done reading chi from the box
       cross_gather<LTS, NTH>(c.h, box, slot, own, c.V, P.ibuf, P.ld, P.n_iface_total, c.g0, false);
-      cp_async_commit();
       cp_async_wait<0>();
       __syncthreads();
       cross_rows<NTH>(s_tail, c.nrow, c.taps_off, s_w, slot, box);
