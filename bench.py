@@ -427,8 +427,14 @@ def run_ours(args):
     # e2e through the public API with host buffers (pinned), LTS
     if dist is not None:
         dist.barrier()
+    # K steps take ~30 ms of wall clock on cfg2, so one host hiccup can double a sample: the K-step loop
+    # is repeated and the median reported (every sample is in the line)
+    e2e_samples = []
     with clk.window():
-        te, e2e_mode = time_e2e(eng, args.steps, torch, serial=args.e2e_serial)
+        for _ in range(5):
+            te, e2e_mode = time_e2e(eng, args.steps, torch, serial=args.e2e_serial)
+            e2e_samples.append(te)
+    te = float(np.median(e2e_samples))
     tt = torch.tensor([te], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -483,7 +489,9 @@ def run_ours(args):
         "roofline": m["roofline"],
         "e2e": {"value": lts["units_per_step"] * args.steps / te, "unit": "updates/s",
                 "h2d_bytes_per_step": int(2 * 8 * mesh.n_nodes), "d2h_bytes_per_step": int(2 * 8 * mesh.n_nodes),
-                "mode": e2e_mode},
+                "mode": e2e_mode,
+                "samples": [lts["units_per_step"] * args.steps / t for t in e2e_samples],
+                "statistic": f"median of {len(e2e_samples)} runs of {args.steps} steps"},
         "gpu_launches": m["gpu_launches"],
         "clocks": clk.summary(),
     }
