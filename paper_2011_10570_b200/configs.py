@@ -14,7 +14,7 @@ All numbers here are frozen: goldens, tests and ``bench.py`` depend on them.
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 

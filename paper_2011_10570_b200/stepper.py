@@ -31,9 +31,8 @@ B200 design:
 from __future__ import annotations
 
 import os
-import time
 from collections import defaultdict
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 
