@@ -160,3 +160,24 @@ def test_two_processes_gloo_on_one_device(cuda, tmp_path):
     c = CONFIGS["cfg1"]
     _, want = _run(config_mesh("cfg1"), c, "lts", False, 2)
     assert np.array_equal(np.load(out), want[-1])
+
+
+def test_more_ranks_than_leaves(cuda):
+    """Empty ranks (weighted_partition with more ranks than the weights can split) run and change nothing."""
+    from paper_2011_10570_b200.mesh import Domain, Mesh
+    from paper_2011_10570_b200.octree import SfcOrdering, uniform_tree
+    from paper_2011_10570_b200.partition import tree_weights, weighted_partition
+    from paper_2011_10570_b200.wave import gaussian_pulse
+
+    tree = uniform_tree(2, 2, 1, SfcOrdering("morton", 2, 2))
+    dom = Domain((-1.0, -1.0), (1.0, 1.0))
+    pm = weighted_partition(tree, tree_weights(tree, "lts"), 8)
+    assert pm.has_empty_ranks
+    outs = []
+    for pmap in (None, pm):
+        eng = Engine(Mesh(tree, points_per_octant=5, pad=2, pmap=pmap, domain=dom), tableau="rk4", mode="lts")
+        eng.initialize(gaussian_pulse((0.1, -0.2), 0.3, 1.0))
+        for _ in range(3):
+            eng.lts_coarse_step()
+        outs.append(eng.current_zip())
+    assert np.array_equal(outs[0], outs[1])
