@@ -444,7 +444,11 @@ class _Rank:
 
     # -- state I/O ----------------------------------------------------------------------
     def load(self, zd) -> None:
-        """u_pre = u_curr = the rank's nodes of the global device field zd, K = 0."""
+        """u_pre = u_curr = the rank's nodes of the global device field zd.  K is left as it
+        is: at slice 0 every leaf steps, so each K_j is written before anything reads it
+        (same-step stage sources read K_j only for j below the running stage; virtual
+        substeps read the K of a source's last completed step, and the first of those is
+        slice 0's), and the reference's ``K = 0`` (stepper.py:224) is never observable."""
         import torch
 
         if self.identity:
@@ -454,7 +458,6 @@ class _Rank:
                 self._l2g_d = torch.from_numpy(self.l2g).to(self.eng.device)
             self.U[0].copy_(zd.index_select(1, self._l2g_d))
         self.U[1].copy_(self.U[0])
-        self.K.zero_()
 
     def shipment_rows(self, s: int, i: int):
         """(row0, row1, parity per cadence) of the record fields that changed in
@@ -899,7 +902,7 @@ class Engine:
 
     def load_zip(self, z) -> None:
         """Load a (2, n_nodes) zip field (host numpy, pinned host or device tensor):
-        u_pre = u_curr = z, K = 0 (stepper.py:213-230)."""
+        u_pre = u_curr = z, time 0 (stepper.py:213-230)."""
         import torch
 
         if not isinstance(z, torch.Tensor):
