@@ -597,7 +597,7 @@ def run_reference(args):
     cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
     print(json.dumps({
         "impl": "reference", "metric": "RK-stage zip-node updates/s (LTS, executed)", "value": value,
-        "unit": "updates/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (BASELINE configs[1])",
         "config": _config(args.config, m.n_nodes, len(m.leaf_starts) - 1),
