@@ -443,9 +443,15 @@ def run_ours(args):
     if world > 1:
         b0 = eng.comm_bytes
         eng.lts_coarse_step()
-        comm = {"ghost_bytes_sent_per_round_rank0": int(eng.comm_bytes - b0),
-                "ghost_leaves_rank0": int(len(eng._rank_list[0].ghosts)),
-                "local_zip_nodes_rank0": int(eng._rank_list[0].n_local)}
+        rk = eng._rank_list[0]
+        mine = [int(eng.comm_bytes - b0), int(len(rk.ghosts)), int(rk.n_local), int(len(rk.tiles)), int(rk.n_boundary)]
+        allr = [None] * world
+        dist.all_gather_object(allr, mine)
+        comm = {"per_rank": [dict(zip(("ghost_bytes_sent_per_round", "ghost_leaves", "local_zip_nodes", "tiles",
+                                       "boundary_tiles"), v)) for v in allr],
+                "backend": backend}
+        print(f"[rank {rank}] ghost bytes sent per round {mine[0]}, ghost leaves {mine[1]}, local zip nodes {mine[2]}, "
+              f"tiles {mine[3]} ({mine[4]} read by other ranks)", file=sys.stderr, flush=True)
     remesh = _remesh_criterion(eng) if rank == 0 and world == 1 else None
 
     # the other single-GPU BASELINE configs, GPU only
