@@ -184,7 +184,7 @@ def units_per_round(eng, rank_only=True):
 
 def time_rounds(eng, steps, torch, dist, per_launch=False, n_slices=None):
     """Device time of `steps` rounds; optional per-launch CUDA events (profiling
-    pass: eager slices, every stage launch bracketed; returns (ms, tiles, is_boundary_part))."""
+    pass: eager slices, every stage launch bracketed; returns (ms, tiles, first tile in the launch order))."""
     dev = eng.device
     stream = torch.cuda.current_stream(dev)
     if dist is not None:
@@ -202,7 +202,7 @@ def time_rounds(eng, steps, torch, dist, per_launch=False, n_slices=None):
             e0.record(stream)
             rc = orig(prm, strm)
             e1.record(stream)
-            launches.append((e0, e1, int(P.n_tiles), int(P.heads) == rk.heads_ptr and rk.n_boundary > 0))
+            launches.append((e0, e1, int(P.n_tiles), (int(P.heads) - rk.heads_ptr) // rk.max_head))
             return rc
 
         class _Hook:
@@ -367,10 +367,9 @@ def measure(name, args, torch, dist, dev, world, clk, steps, warmup, gts_slices=
         else:
             _, per = time_rounds(eng, 1, torch, dist, per_launch=True)
         # algorithmic bytes per launch = 68 B x owned nodes of the launched tiles
-        cb = np.concatenate([[0], np.cumsum(counts[rk.tiles[: rk.n_boundary]])])
-        ci = np.concatenate([[0], np.cumsum(counts[rk.tiles[rk.n_boundary:]])])
+        cum = np.concatenate([[0], np.cumsum(counts[rk.tiles])])
         k_ms = sum(m for m, _, _ in per)
-        k_bytes = sum(BYTES_PER_UNIT * (cb[n] if bd else ci[n]) for _, n, bd in per)
+        k_bytes = sum(BYTES_PER_UNIT * (cum[off + n] - cum[off]) for _, n, off in per)
         roof[mode] = dict(ms=k_ms, ach=k_bytes / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0, launches=len(per))
     traffic, traffic_note = _ncu_traffic_for(name)
     lts, gts = res["lts"], res["gts"]

@@ -240,6 +240,8 @@ typedef struct {
   int max_tail;                /* largest tail in bytes (bulk-copied into shared memory) */
   int max_slots;               /* largest interpolation-source set of any tile (shared memory) */
   int threads;                 /* threads per CTA: 128 or 256 */
+  int lean;                    /* 1: every tile of this launch is off the physical faces (and the source is not
+                                  sin): run the lean kernel instance (no face / coordinate paths) */
   long long* probe;            /* NULL, or [n_tiles][8] phase timestamps (builds with -DAMR_PHASE_PROBE) */
   const double* wtab;          /* distinct interpolation weights (<= 64, device) */
   int n_wtab;

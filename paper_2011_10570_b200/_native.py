@@ -40,7 +40,7 @@ class AmrStageParams(C.Structure):
         ("lts", C.c_int), ("stage", C.c_int), ("n_stages", C.c_int),
         ("nonlinear", C.c_int), ("gts_cur", C.c_int),
         ("n_tiles", C.c_int64), ("n_nodes", C.c_int64), ("ld", C.c_int64),
-        ("heads", _vp), ("tail", _vp), ("max_head", C.c_int), ("max_tail", C.c_int), ("max_slots", C.c_int), ("threads", C.c_int), ("probe", _vp),
+        ("heads", _vp), ("tail", _vp), ("max_head", C.c_int), ("max_tail", C.c_int), ("max_slots", C.c_int), ("threads", C.c_int), ("lean", C.c_int), ("probe", _vp),
         ("wtab", _vp), ("n_wtab", C.c_int),
         ("n_iface", C.c_int64), ("n_iface_total", C.c_int64), ("if_gid", _vp), ("if_cad", _vp), ("ibuf", _vp), ("ibuf0", _vp), ("if_phase", C.c_int),
         ("n_vt", C.c_int), ("vt_j", C.c_int * AMR_MAXP), ("Y", _vp),

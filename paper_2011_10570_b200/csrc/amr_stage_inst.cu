@@ -10,7 +10,7 @@ namespace {
 // per-device launch state (a process may drive several GPUs)
 constexpr int kMaxDev = 64;
 
-template <int DIM, int PPO, bool LTS, int NT, int NTH>
+template <int DIM, int PPO, bool LTS, int NT, int NTH, bool FULL>
 int launch_cross_one(const AmrStageParams* p, cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -19,29 +19,34 @@ int launch_cross_one(const AmrStageParams* p, cudaStream_t st) {
   const size_t dyn = CK::smem_bytes(p->max_slots, p->max_head, p->max_tail, AMR_TPC);
   static size_t configured[kMaxDev] = {0};
   if (dyn > configured[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(stage_cross<DIM, PPO, LTS, NT, NTH>,
+    cudaError_t e = cudaFuncSetAttribute(stage_cross<DIM, PPO, LTS, NT, NTH, FULL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(stage_cross)");
     configured[dev] = dyn;
   }
-  return pdl_launch(stage_cross<DIM, PPO, LTS, NT, NTH>, dim3((unsigned)((p->n_tiles + AMR_TPC - 1) / AMR_TPC)), dim3(NTH), dyn, st, *p);
+  return pdl_launch(stage_cross<DIM, PPO, LTS, NT, NTH, FULL>, dim3((unsigned)((p->n_tiles + AMR_TPC - 1) / AMR_TPC)), dim3(NTH), dyn, st, *p);
 }
 
-template <int DIM, int PPO, bool LTS, int NTH>
+template <int DIM, int PPO, bool LTS, int NTH, bool FULL>
 int launch_cross_nt(const AmrStageParams* p, cudaStream_t st) {
   switch (p->n_vt) {
-    case 0: return launch_cross_one<DIM, PPO, LTS, 0, NTH>(p, st);
-    case 1: return launch_cross_one<DIM, PPO, LTS, 1, NTH>(p, st);
-    case 2: return launch_cross_one<DIM, PPO, LTS, 2, NTH>(p, st);
-    case 3: return launch_cross_one<DIM, PPO, LTS, 3, NTH>(p, st);
+    case 0: return launch_cross_one<DIM, PPO, LTS, 0, NTH, FULL>(p, st);
+    case 1: return launch_cross_one<DIM, PPO, LTS, 1, NTH, FULL>(p, st);
+    case 2: return launch_cross_one<DIM, PPO, LTS, 2, NTH, FULL>(p, st);
+    case 3: return launch_cross_one<DIM, PPO, LTS, 3, NTH, FULL>(p, st);
     default: return AMR_EINVAL;
   }
 }
 
 template <int DIM, int PPO, bool LTS>
 int launch_stage_nt(const AmrStageParams* p, cudaStream_t st) {
-  if (p->threads == 256) return launch_cross_nt<DIM, PPO, LTS, 256>(p, st);
-  return launch_cross_nt<DIM, PPO, LTS, 128>(p, st);
+  if (p->lean) {  // the caller vouches: no physical face, no coordinate-dependent source
+    if (p->nonlinear == 1) return AMR_EINVAL;
+    if (p->threads == 256) return launch_cross_nt<DIM, PPO, LTS, 256, false>(p, st);
+    return launch_cross_nt<DIM, PPO, LTS, 128, false>(p, st);
+  }
+  if (p->threads == 256) return launch_cross_nt<DIM, PPO, LTS, 256, true>(p, st);
+  return launch_cross_nt<DIM, PPO, LTS, 128, true>(p, st);
 }
 
 }  // namespace

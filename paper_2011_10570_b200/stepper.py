@@ -217,6 +217,7 @@ class _Rank:
         self.mesh, self.cad, self.l_max = mesh, leaf_cad, l_max
         self.rank = rank
         self.owned = np.asarray(owned, dtype=np.int64)
+        self.split = False  # set by the engine: launch the lean kernel instance on tiles off the physical faces
         cad = leaf_cad
         order = np.lexsort((self.owned, -cad[self.owned]))
         self.tiles = self.owned[order]  # cadence order; reordered by layout()
@@ -253,16 +254,31 @@ class _Rank:
         tb = is_b[self.tiles]
         import torch
 
-        perm = np.lexsort((self.tiles, -cad[self.tiles], ~tb))
+        # tiles on a physical face need the full kernel instance (biased and radiative rows); with
+        # `split` they form a second group after the lean tiles of each part
+        an, lv = mesh.tree.arrays()
+        side = (1 << (mesh.L - lv[self.tiles].astype(np.int64)))[:, None]
+        a = an[self.tiles].astype(np.int64)
+        on_face = np.any((a == 0) | (a + side == (1 << mesh.L)), axis=1) if len(self.tiles) else np.zeros(0, bool)
+        tf = on_face if self.split else np.zeros(len(self.tiles), dtype=bool)
+        perm = np.lexsort((self.tiles, -cad[self.tiles], tf, ~tb))
         self.tiles = self.tiles[perm]
         pdev = prog["heads"].device
         heads = prog["heads"][torch.from_numpy(perm).to(pdev)] if len(perm) else prog["heads"]
         tcad = cad[self.tiles]
-        tb = tb[perm]
+        tb, tf = tb[perm], tf[perm]
         self.n_boundary = int(tb.sum())
         levels = range(self.l_max + 2)
         self.prefix_b = [int(np.sum(tcad[tb] >= c)) for c in levels]
         self.prefix_i = [int(np.sum(tcad[~tb] >= c)) for c in levels]
+        # launch groups: (boundary | interior) x (lean | full), each finest cadence first
+        self.groups = {}
+        off = 0
+        for part, pm in ((True, tb), (False, ~tb)):
+            for full, fm in ((False, ~tf), (True, tf)):
+                sel = pm & fm
+                self.groups[(part, full)] = (off, [int(np.sum(tcad[sel] >= c)) for c in levels])
+                off += int(sel.sum())
         n_iface = prog["n_iface"]
         self.n_iface = n_iface
         rcad = (prog["if_cad"][:n_iface] & 0xFF).cpu().numpy() if n_iface else np.zeros(0, np.int64)
@@ -432,15 +448,18 @@ class _Rank:
 
     def launch_tiles(self, cmin: int, boundary: bool) -> None:
         P = self.prm
-        n = self.prefix_b[cmin] if boundary else self.prefix_i[cmin]
-        if not n:
-            return
-        P.n_tiles = n
-        P.heads = self.heads_ptr + (0 if boundary else self.n_boundary * self.max_head)
-        with self.eng._phase("rhs"):
-            rc = self.eng._lib.amr_stage(C.byref(P), self.eng._stream())
-        if rc:
-            _native.check(rc, "amr_stage")
+        for full in (False, True):
+            off, prefix = self.groups[(boundary, full)]
+            n = prefix[cmin]
+            if not n:
+                continue
+            P.n_tiles = n
+            P.heads = self.heads_ptr + off * self.max_head
+            P.lean = 1 if (self.split and not full) else 0
+            with self.eng._phase("rhs"):
+                rc = self.eng._lib.amr_stage(C.byref(P), self.eng._stream())
+            if rc:
+                _native.check(rc, "amr_stage")
 
     # -- state I/O ----------------------------------------------------------------------
     def load(self, zd) -> None:
@@ -773,7 +792,9 @@ class Engine:
                 local = {0: _Rank(mesh, leaf_cad, self._lts_kernel, self.l_max, 0, np.arange(n_leaves))}
                 need = {}
             lists = _ship_lists(need, rr) if need else {}
+            split = self._lts_kernel and self._nl != 1 and os.environ.get("AMR_SPLIT", "1") == "1"
             for r, rk in local.items():
+                rk.split = split
                 sent = [lv for (q, _), lv in lists.items() if q == r]
                 rk.layout(np.unique(np.concatenate(sent)) if sent else np.zeros(0, np.int64))
                 rk.upload(self)
@@ -1212,7 +1233,7 @@ class Engine:
         c = min(el)
         n = 0
         for rk in self._rank_list:
-            tiles = (1 if rk.prefix_b[c] else 0) + (1 if rk.prefix_i[c] else 0)
+            tiles = sum(1 for (_, prefix) in rk.groups.values() if prefix[c])
             iface = (1 if len(el) == 1 else self.p) if tiles and rk.if_prefix[c] else 0
             n += self.p * tiles + iface
         return n

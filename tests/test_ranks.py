@@ -24,13 +24,14 @@ from paper_2011_10570_b200 import tileprog
 from paper_2011_10570_b200.stepper import _Link, _Rank, _ship_lists
 
 
-def _ranks(mesh, lts=True):
+def _ranks(mesh, lts=True, split=False):
     lv = mesh.tree.arrays()[1].astype(np.int32)
     cad = lv if lts else np.full_like(lv, lv.max())
     rr = mesh.pmap.rank_ranges
     ranks = {r: _Rank(mesh, cad, lts, int(lv.max()), r, np.arange(*rr[r])) for r in range(len(rr))}
     lists = _ship_lists({r: rk.ghosts for r, rk in ranks.items()}, rr)
     for r, rk in ranks.items():
+        rk.split = split
         sent = [v for (q, _), v in lists.items() if q == r]
         rk.layout(np.unique(np.concatenate(sent)) if sent else np.zeros(0, np.int64))
     return cad, ranks, lists
@@ -52,11 +53,11 @@ def _decoded(prog_like, t, l2g, if_gid, if_cad):
     return int(l2g[d["g0"]]) if d["n_own"] else None, d["n_own"], cells, rows
 
 
-@pytest.mark.parametrize("name,R,lts", [("cfg1", 2, True), ("cfg1", 3, True), ("cfg1", 8, True), ("cfg1", 4, False),
-                                        ("mini3d", 4, True)])
-def test_rank_programs_read_the_same_nodes(name, R, lts):
+@pytest.mark.parametrize("name,R,lts,split", [("cfg1", 2, True, False), ("cfg1", 3, True, True), ("cfg1", 8, True, False),
+                                              ("cfg1", 4, False, False), ("mini3d", 4, True, True)])
+def test_rank_programs_read_the_same_nodes(name, R, lts, split):
     mesh = config_mesh(name, ranks=R)
-    cad, ranks, lists = _ranks(mesh, lts)
+    cad, ranks, lists = _ranks(mesh, lts, split)
     one = _Rank(mesh, cad, lts, int(cad.max()), 0, np.arange(len(cad)))
     one.layout(np.zeros(0, np.int64))
     assert one.identity and one.l2g is None
@@ -72,10 +73,27 @@ def test_rank_programs_read_the_same_nodes(name, R, lts):
         assert np.array_equal(rk.l2g, want)
         assert rk.n_boundary == int(np.isin(rk.tiles, np.concatenate(
             [v for (q, _), v in lists.items() if q == r] or [np.zeros(0, np.int64)])).sum())
-        tb = np.arange(len(rk.tiles)) < rk.n_boundary
-        for part in (tb, ~tb):  # each part finest cadence first
-            c = cad[rk.tiles[part]]
-            assert np.all(np.diff(c) <= 0)
+        # launch groups: (boundary | interior) x (lean | full), back to back, each finest cadence first;
+        # with `split` the tiles on a physical face are the full groups
+        an, lvl = mesh.tree.arrays()
+        side = 1 << (mesh.L - lvl.astype(np.int64))
+        on_face = np.any((an == 0) | (an + side[:, None] == (1 << mesh.L)), axis=1)
+        pos = 0
+        for part in (True, False):
+            for full in (False, True):
+                off, prefix = rk.groups[(part, full)]
+                assert off == pos
+                grp = rk.tiles[off: off + prefix[0]]
+                pos += len(grp)
+                assert np.all(np.diff(cad[grp]) <= 0)
+                assert np.all((np.arange(off, off + len(grp)) < rk.n_boundary) == part)
+                if split:
+                    assert np.all(on_face[grp] == full)
+                else:
+                    assert not full or len(grp) == 0
+                for c in range(int(cad.max()) + 1):
+                    assert prefix[c] == int(np.sum(cad[grp] >= c))
+        assert pos == len(rk.tiles)
         for t, leaf in enumerate(rk.tiles):
             got = _decoded(rk.host, t, rk.l2g, rk.host["if_gid"], rk.host["if_cad"])
             assert got == ref[int(leaf)], (r, int(leaf))

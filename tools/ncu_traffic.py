@@ -9,9 +9,15 @@ import sys
 
 
 def _is_lts(name: str) -> bool:
-    """stage_{kernel,blob,pipe}<DIM, PPO, LTS, NT> as ncu prints it (demangled forms vary)."""
+    """stage_cross<DIM, PPO, LTS, NT, NTH, FULL> as ncu prints it (demangled forms vary)."""
     m = re.search(r"stage_(?:kernel|blob|pipe|cross)<\(?\w*\)?(\d+), \(?\w*\)?(\d+), \(?\w*\)?(\w+)", name)
     return bool(m) and m.group(3) in ("1", "true")
+
+
+def _is_full(name: str) -> bool:
+    args = re.search(r"stage_cross<([^>]*)>", name)
+    last = args.group(1).split(",")[-1].strip() if args else "1"
+    return re.sub(r"\(\w+\)", "", last) in ("1", "true")
 
 import numpy as np
 
@@ -28,21 +34,29 @@ def main(rep, out="profiles/traffic.json", cfg="cfg2"):
     lts = []
     for r in rows[2:]:
         if _is_lts(r[i_n]):
-            lts.append((float(r[i_r]) * scale[units[i_r]] + float(r[i_w]) * scale[units[i_w]], int(float(r[i_g]))))
-    # algorithmic bytes: 68 B x owned nodes of the launched tiles
+            lts.append((float(r[i_r]) * scale[units[i_r]] + float(r[i_w]) * scale[units[i_w]], int(float(r[i_g])),
+                        _is_full(r[i_n])))
+    # algorithmic bytes: 68 B x owned nodes of the launched tiles.  The LTS engine launches the lean
+    # kernel instance (last template argument false) on the tiles off the physical faces and the full
+    # one on the rest, each group finest cadence first: a launch is a prefix of its group.
     sys.path.insert(0, ".")
     from bench import build_mesh
+    from paper_2011_10570_b200.stepper import Engine
 
-    _, mesh = build_mesh(cfg, 1, "lts")
-    lv = mesh.tree.arrays()[1]
+    c, mesh = build_mesh(cfg, 1, "lts")
+    rk = Engine(mesh, tableau=c.tableau, cfl=c.cfl, mode="lts", nonlinear=c.nonlinear)._rank_list[0]
     counts = np.diff(mesh.leaf_starts)
-    order = np.lexsort((np.arange(len(lv)), -lv))
-    cum = np.concatenate([[0], np.cumsum(counts[order])])
-    alg = [68.0 * cum[g] for _, g in lts]
+    cum = np.concatenate([[0], np.cumsum(counts[rk.tiles])])
+
+    def alg_bytes(grid, full):
+        off = rk.groups[(False, full)][0]
+        return 68.0 * (cum[off + grid] - cum[off])
+
+    alg = [alg_bytes(g, f) for _, g, f in lts]
     d = {"source": rep.split("/")[-1], "config": cfg, "lts_launches": len(lts),
-         "lts_bytes_per_launch": float(np.mean([b for b, _ in lts])),
+         "lts_bytes_per_launch": float(np.mean([b for b, _, _ in lts])),
          "lts_algorithmic_bytes_per_launch": float(np.mean(alg)),
-         "ratio": float(np.sum([b for b, _ in lts]) / np.sum(alg))}
+         "ratio": float(np.sum([b for b, _, _ in lts]) / np.sum(alg))}
     json.dump(d, open(out, "w"), indent=1)
     print(d)
 
