@@ -27,7 +27,9 @@ def main(path):
     for n, r in enumerate(rows[2:]):
         name = r[idx["Kernel Name"]]
         lts = _is_lts(name)
-        short = ("interp" if "interp" in name else "stage") + ("_lts" if lts else "_gts")
+        args = re.search(r"stage_cross<([^>]*)>", name)
+        last = re.sub(r"\(\w+\)", "", args.group(1).split(",")[-1].strip()) if args else "1"
+        short = "stage" + ("_lts" if lts else "_gts") + ("" if last in ("1", "true") else "_lean")
         def g(m, scale=1.0):
             try:
                 return float(r[idx[m]]) * scale

@@ -1,6 +1,7 @@
-"""Short driver for ncu: cfg2 mesh, 1 warm LTS round + 1 GTS step, then
-`--n` profiled slices (LTS slice 0 = all tiles, LTS slice 1 = finest only,
-GTS step).  Run plain first, then under ncu (see profiles/README.md)."""
+"""Short driver for ncu: 1 warm LTS round + 1 GTS step, then the profiled
+launches between cudaProfilerStart/Stop (run ncu with --profile-from-start off):
+an LTS round start (all tiles), the next LTS slice (finest level only) and a
+GTS step.  Run plain first, then under ncu (see profiles/README.md)."""
 import argparse
 import os
 import sys
@@ -23,8 +24,10 @@ for e in (lts, gts):
 lts.lts_coarse_step()   # 16 slices x 4 launches
 gts.gts_step()          # 4 launches
 torch.cuda.synchronize()
-lts.advance_slice()     # slice 16 = round start: all tiles (profiled: launches 68..71)
-lts.advance_slice()     # slice 17: finest level only (72..75)
-gts.gts_step()          # all tiles, GTS kernel (76..79)
+torch.cuda.profiler.start()  # ncu --profile-from-start off: only the launches below are profiled
+lts.advance_slice()     # round start: all tiles (4 lean-instance launches, 4 full-instance ones on the face tiles)
+lts.advance_slice()     # next slice: finest level only (4 launches)
+gts.gts_step()          # all tiles, GTS kernel (4 launches)
 torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("ok", mesh.n_nodes)

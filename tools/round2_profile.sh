@@ -16,22 +16,23 @@ python bench.py --steps 1 --warmup 1 --no-cpu --side none > gpurun_out/bench_sma
       --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 1 --warmup 1 --no-cpu --side none > gpurun_out/ncu_launches_$TAG.log 2>&1
 python tools/launch_summary.py gpurun_out/launches_$TAG.csv > gpurun_out/launches_summary_$TAG.md 2>&1
 python tools/profile_stage.py > gpurun_out/prof_plain_$TAG.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"$K" -s 68 -c 12 \
+  ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"$K" \
       -o /tmp/prof_$TAG python tools/profile_stage.py > gpurun_out/ncu_$TAG.log 2>&1
 python tools/ncu_summary.py /tmp/prof_$TAG.ncu-rep > gpurun_out/sum_$TAG.md 2>&1
 python tools/ncu_traffic.py /tmp/prof_$TAG.ncu-rep gpurun_out/traffic_$TAG.json cfg2 > /dev/null 2>&1
-for k in 1 9; do python tools/ncu_lines.py /tmp/prof_$TAG.ncu-rep $K $k 30 > gpurun_out/lines_${TAG}_$k.txt 2>&1; done
-python tools/ncu_stalls.py /tmp/prof_$TAG.ncu-rep $K 9 20 > gpurun_out/stalls_$TAG.txt 2>&1
+# captured launches: LTS round start = (lean, full) x 4 stages (0..7), finest-only slice (8..11), GTS step (12..15)
+for k in 2 13; do python tools/ncu_lines.py /tmp/prof_$TAG.ncu-rep $K $k 30 > gpurun_out/lines_${TAG}_$k.txt 2>&1; done
+python tools/ncu_stalls.py /tmp/prof_$TAG.ncu-rep $K 13 20 > gpurun_out/stalls_$TAG.txt 2>&1
+python tools/ncu_stalls.py /tmp/prof_$TAG.ncu-rep $K 2 20 > gpurun_out/stalls_${TAG}_lts.txt 2>&1
 cat gpurun_out/sum_$TAG.md
-# cfg3: a round is 32 slices -> 128 LTS + 4 GTS stage launches before the profiled ones
+# cfg3, cfg4: the same driver (the profiled launches are bracketed by cudaProfilerStart/Stop)
 python tools/profile_stage.py --config cfg3 > gpurun_out/prof_plain_${TAG}_cfg3.log 2>&1 && \
-  ncu --set full --clock-control none -k regex:"$K" -s 132 -c 8 \
+  ncu --set full --clock-control none --profile-from-start off -k regex:"$K" \
       -o /tmp/prof_${TAG}_cfg3 python tools/profile_stage.py --config cfg3 > gpurun_out/ncu_${TAG}_cfg3.log 2>&1
 python tools/ncu_summary.py /tmp/prof_${TAG}_cfg3.ncu-rep > gpurun_out/sum_${TAG}_cfg3.md 2>&1
 python tools/ncu_traffic.py /tmp/prof_${TAG}_cfg3.ncu-rep gpurun_out/traffic_${TAG}_cfg3.json cfg3 > /dev/null 2>&1
-# cfg4: a round is 1024 slices -> 4096 + 4
 python tools/profile_stage.py --config cfg4 > gpurun_out/prof_plain_${TAG}_cfg4.log 2>&1 && \
-  ncu --set full --clock-control none -k regex:"$K" -s 4100 -c 8 \
+  ncu --set full --clock-control none --profile-from-start off -k regex:"$K" \
       -o /tmp/prof_${TAG}_cfg4 python tools/profile_stage.py --config cfg4 > gpurun_out/ncu_${TAG}_cfg4.log 2>&1
 python tools/ncu_summary.py /tmp/prof_${TAG}_cfg4.ncu-rep > gpurun_out/sum_${TAG}_cfg4.md 2>&1
 python tools/ncu_traffic.py /tmp/prof_${TAG}_cfg4.ncu-rep gpurun_out/traffic_${TAG}_cfg4.json cfg4 > /dev/null 2>&1
