@@ -400,6 +400,9 @@ __device__ __forceinline__ void rhs_pass2(const AmrStageParams& P, const TileCtx
 #ifndef AMR_CROSS_MINB
 #define AMR_CROSS_MINB 4  // resident 256-thread CTAs per SM the register budget is sized for
 #endif
+#ifndef AMR_ALT_NTH
+#define AMR_ALT_NTH 128  // the second CTA size compiled in (AmrStageParams.threads selects it)
+#endif
 
 #ifdef AMR_PHASE_PROBE
 __device__ __forceinline__ long long gtimer() {
@@ -427,7 +430,7 @@ __device__ __forceinline__ long long gtimer() {
 // first head fetch is exposed; many CTAs stay resident per SM, so tiles in
 // different phases interleave.
 template <int DIM, int PPO, bool LTS, int NT, int NTH, bool FULL>
-__global__ void __launch_bounds__(NTH, (NTH <= 128 ? 2 * AMR_CROSS_MINB : AMR_CROSS_MINB))
+__global__ void __launch_bounds__(NTH, (AMR_CROSS_MINB * 256) / NTH)
     stage_cross(const __grid_constant__ AmrStageParams P) {
   using T = Tile<DIM, PPO>;
   using CK = CrossK<DIM, PPO>;

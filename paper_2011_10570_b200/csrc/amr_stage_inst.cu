@@ -43,10 +43,10 @@ int launch_stage_nt(const AmrStageParams* p, cudaStream_t st) {
   if (p->lean) {  // the caller vouches: no physical face, no coordinate-dependent source
     if (p->nonlinear == 1) return AMR_EINVAL;
     if (p->threads == 256) return launch_cross_nt<DIM, PPO, LTS, 256, false>(p, st);
-    return launch_cross_nt<DIM, PPO, LTS, 128, false>(p, st);
+    return launch_cross_nt<DIM, PPO, LTS, AMR_ALT_NTH, false>(p, st);
   }
   if (p->threads == 256) return launch_cross_nt<DIM, PPO, LTS, 256, true>(p, st);
-  return launch_cross_nt<DIM, PPO, LTS, 128, true>(p, st);
+  return launch_cross_nt<DIM, PPO, LTS, AMR_ALT_NTH, true>(p, st);
 }
 
 }  // namespace
