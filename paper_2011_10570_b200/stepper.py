@@ -218,6 +218,9 @@ class _Rank:
         self.rank = rank
         self.owned = np.asarray(owned, dtype=np.int64)
         self.split = False  # set by the engine: launch the lean kernel instance on tiles off the physical faces
+        self.merge = os.environ.get("AMR_MERGE", "1") == "1"  # one launch when all tiles of a part step
+        self.lts_kernel = lts_kernel
+        self.slots = 4 * 148  # resident stage-kernel CTAs; set by the engine from the device's SM count
         cad = leaf_cad
         order = np.lexsort((self.owned, -cad[self.owned]))
         self.tiles = self.owned[order]  # cadence order; reordered by layout()
@@ -261,7 +264,7 @@ class _Rank:
         a = an[self.tiles].astype(np.int64)
         on_face = np.any((a == 0) | (a + side == (1 << mesh.L)), axis=1) if len(self.tiles) else np.zeros(0, bool)
         tf = on_face if self.split else np.zeros(len(self.tiles), dtype=bool)
-        perm = np.lexsort((self.tiles, -cad[self.tiles], tf, ~tb))
+        perm = np.lexsort((self.tiles, -cad[self.tiles], ~tf, ~tb))
         self.tiles = self.tiles[perm]
         pdev = prog["heads"].device
         heads = prog["heads"][torch.from_numpy(perm).to(pdev)] if len(perm) else prog["heads"]
@@ -271,11 +274,13 @@ class _Rank:
         levels = range(self.l_max + 2)
         self.prefix_b = [int(np.sum(tcad[tb] >= c)) for c in levels]
         self.prefix_i = [int(np.sum(tcad[~tb] >= c)) for c in levels]
-        # launch groups: (boundary | interior) x (lean | full), each finest cadence first
+        # launch groups: (boundary | interior) x (full | lean), each finest cadence first.  The full
+        # group comes first so that, when every tile of a part steps, one launch of the full instance
+        # covers both groups with the long face tiles at the front of the grid (launch_plan)
         self.groups = {}
         off = 0
         for part, pm in ((True, tb), (False, ~tb)):
-            for full, fm in ((False, ~tf), (True, tf)):
+            for full, fm in ((True, tf), (False, ~tf)):
                 sel = pm & fm
                 self.groups[(part, full)] = (off, [int(np.sum(tcad[sel] >= c)) for c in levels])
                 off += int(sel.sum())
@@ -446,16 +451,29 @@ class _Rank:
             if rc:
                 _native.check(rc, "amr_iface")
 
+    def launch_plan(self, cmin: int, boundary: bool):
+        """(first tile, tiles, lean instance?) of the stage launches of one part at cadence >= cmin.
+        Lean tiles, then the face tiles (full instance).  When every tile of the part steps, both
+        groups go in one launch of the full instance instead: the face tiles are about 3x a normal
+        tile, and at the front of a mixed grid they overlap the rest, where a launch of their own
+        leaves most of the SMs idle."""
+        (off_f, pre_f), (off_l, pre_l) = self.groups[(boundary, True)], self.groups[(boundary, False)]
+        n_f, n_l = pre_f[cmin], pre_l[cmin]
+        if self.merge and n_f and n_l and n_f == pre_f[0] and n_l == pre_l[0]:
+            # LTS: the full instance runs a lean tile about 3 % slower, and a face launch of several
+            # waves is already well packed: merge when the idle slots of its last wave (x 3 tile times)
+            # outweigh that (cfg2: 296 face tiles of 7 344, merged; cfg3: not).  GTS: always one launch
+            idle = -n_f % self.slots
+            if not self.lts_kernel or 100 * idle > n_l:
+                return [(off_f, n_f + n_l, False)]
+        return [(o, n, lean) for o, n, lean in ((off_l, n_l, self.split), (off_f, n_f, False)) if n]
+
     def launch_tiles(self, cmin: int, boundary: bool) -> None:
         P = self.prm
-        for full in (False, True):
-            off, prefix = self.groups[(boundary, full)]
-            n = prefix[cmin]
-            if not n:
-                continue
+        for off, n, lean in self.launch_plan(cmin, boundary):
             P.n_tiles = n
             P.heads = self.heads_ptr + off * self.max_head
-            P.lean = 1 if (self.split and not full) else 0
+            P.lean = 1 if lean else 0
             with self.eng._phase("rhs"):
                 rc = self.eng._lib.amr_stage(C.byref(P), self.eng._stream())
             if rc:
@@ -792,9 +810,13 @@ class Engine:
                 local = {0: _Rank(mesh, leaf_cad, self._lts_kernel, self.l_max, 0, np.arange(n_leaves))}
                 need = {}
             lists = _ship_lists(need, rr) if need else {}
-            split = self._lts_kernel and self._nl != 1 and os.environ.get("AMR_SPLIT", "1") == "1"
+            # GTS engines use the split only for its tile order (face tiles first, one launch)
+            split = self._nl != 1 and os.environ.get("AMR_SPLIT", "1") == "1" \
+                and (self._lts_kernel or os.environ.get("AMR_SPLIT_GTS", "1") == "1")
+            slots = 4 * torch.cuda.get_device_properties(self.device).multi_processor_count
             for r, rk in local.items():
                 rk.split = split
+                rk.slots = slots
                 sent = [lv for (q, _), lv in lists.items() if q == r]
                 rk.layout(np.unique(np.concatenate(sent)) if sent else np.zeros(0, np.int64))
                 rk.upload(self)
@@ -1233,7 +1255,7 @@ class Engine:
         c = min(el)
         n = 0
         for rk in self._rank_list:
-            tiles = sum(1 for (_, prefix) in rk.groups.values() if prefix[c])
+            tiles = len(rk.launch_plan(c, True)) + len(rk.launch_plan(c, False))
             iface = (1 if len(el) == 1 else self.p) if tiles and rk.if_prefix[c] else 0
             n += self.p * tiles + iface
         return n

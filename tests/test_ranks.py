@@ -73,14 +73,14 @@ def test_rank_programs_read_the_same_nodes(name, R, lts, split):
         assert np.array_equal(rk.l2g, want)
         assert rk.n_boundary == int(np.isin(rk.tiles, np.concatenate(
             [v for (q, _), v in lists.items() if q == r] or [np.zeros(0, np.int64)])).sum())
-        # launch groups: (boundary | interior) x (lean | full), back to back, each finest cadence first;
+        # launch groups: (boundary | interior) x (full | lean), back to back, each finest cadence first;
         # with `split` the tiles on a physical face are the full groups
         an, lvl = mesh.tree.arrays()
         side = 1 << (mesh.L - lvl.astype(np.int64))
         on_face = np.any((an == 0) | (an + side[:, None] == (1 << mesh.L)), axis=1)
         pos = 0
         for part in (True, False):
-            for full in (False, True):
+            for full in (True, False):
                 off, prefix = rk.groups[(part, full)]
                 assert off == pos
                 grp = rk.tiles[off: off + prefix[0]]
