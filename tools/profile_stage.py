@@ -25,7 +25,7 @@ lts.lts_coarse_step()   # 16 slices x 4 launches
 gts.gts_step()          # 4 launches
 torch.cuda.synchronize()
 torch.cuda.profiler.start()  # ncu --profile-from-start off: only the launches below are profiled
-lts.advance_slice()     # round start: all tiles (4 lean-instance launches, 4 full-instance ones on the face tiles)
+lts.advance_slice()     # round start: all tiles (cfg2: 4 launches of the full instance, face tiles first; cfg3/cfg4: 4 lean + 4 full)
 lts.advance_slice()     # next slice: finest level only (4 launches)
 gts.gts_step()          # all tiles, GTS kernel (4 launches)
 torch.cuda.synchronize()

@@ -20,9 +20,9 @@ python tools/profile_stage.py > gpurun_out/prof_plain_$TAG.log 2>&1 && \
       -o /tmp/prof_$TAG python tools/profile_stage.py > gpurun_out/ncu_$TAG.log 2>&1
 python tools/ncu_summary.py /tmp/prof_$TAG.ncu-rep > gpurun_out/sum_$TAG.md 2>&1
 python tools/ncu_traffic.py /tmp/prof_$TAG.ncu-rep gpurun_out/traffic_$TAG.json cfg2 > /dev/null 2>&1
-# captured launches: LTS round start = (lean, full) x 4 stages (0..7), finest-only slice (8..11), GTS step (12..15)
-for k in 2 13; do python tools/ncu_lines.py /tmp/prof_$TAG.ncu-rep $K $k 30 > gpurun_out/lines_${TAG}_$k.txt 2>&1; done
-python tools/ncu_stalls.py /tmp/prof_$TAG.ncu-rep $K 13 20 > gpurun_out/stalls_$TAG.txt 2>&1
+# captured launches (cfg2): LTS round start, all tiles in one launch per stage (0..3), finest-only slice (4..7, lean), GTS step (8..11)
+for k in 2 9; do python tools/ncu_lines.py /tmp/prof_$TAG.ncu-rep $K $k 30 > gpurun_out/lines_${TAG}_$k.txt 2>&1; done
+python tools/ncu_stalls.py /tmp/prof_$TAG.ncu-rep $K 9 20 > gpurun_out/stalls_$TAG.txt 2>&1
 python tools/ncu_stalls.py /tmp/prof_$TAG.ncu-rep $K 2 20 > gpurun_out/stalls_${TAG}_lts.txt 2>&1
 cat gpurun_out/sum_$TAG.md
 # cfg3, cfg4: the same driver (the profiled launches are bracketed by cudaProfilerStart/Stop)
